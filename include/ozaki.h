@@ -1,0 +1,168 @@
+/*
+ * ozaki.h -- C ABI of the B200 (sm_100a) INT8 Ozaki-I emulation of FP64 GEMM.
+ *
+ * The operation (§2.2): Ozaki-I "splits high-precision input
+ * matrices into slices as lower-precision components based on their significant
+ * bits and exponent alignment, then performs low-precision matrix
+ * multiplications on these slices and accumulates them in higher precision".
+ * The precision knob is the slice count s = num_slices: the paper's modes
+ * "mantissa bits 31, 39, 47, 55, 63" (§3.2) are s = 4..8
+ * (bits = 8s - 1, reading R2).  The complex routines serve the ZGEMM
+ * calls that dominate LSMS in MuST (§3.2).
+ *
+ * What every call computes (readings R1-R15):
+ *   e_i  = power-of-two exponent of row i of op(A)   (127-rule, R3)
+ *   f_j  = power-of-two exponent of column j of op(B)
+ *   each entry x -> X = RNE(x * 2^(8s-1-e)) -> s balanced INT8 digits (R4)
+ *   S_L  = sum_{t+u=L} A_t * B_u^T  exactly (INT8 x INT8 -> INT32), L = 2..s+1 (R1)
+ *   acc  = sum_{L=s+1..2} S_L 2^(-8(L-2)) in FP64, ascending (R6)
+ *   P    = acc * 2^(e_i + f_j - 14)            (one correctly rounded scaling)
+ *   C    = alpha * P + beta * C   in FP64, BLAS semantics (R7)
+ * Results are bit-identical to the CPU oracle (oracle/) for every s.
+ *
+ * Conventions (all routines):
+ *   - Matrices are column-major with leading dimensions, exactly as BLAS
+ *     dgemm/zgemm.  Complex matrices are interleaved (re, im) doubles.
+ *   - A, B, C (and strided-batched bases) are DEVICE pointers owned by the
+ *     caller (e.g. torch tensors).  A and B are read-only; C must not alias A
+ *     or B.  When beta == 0, C is never read (NaN-safe).
+ *   - transa/transb in {'N','n','T','t','C','c'}; for real routines 'C' == 'T'.
+ *   - num_slices in [1, 16].
+ *   - Calls enqueue work on the calling thread's stream (ozaki_set_stream,
+ *     default: the legacy default stream 0) and return without synchronising.
+ *     Workspace is allocated stream-ordered (cudaMallocAsync) and freed in
+ *     stream order.
+ *   - Return value: 0 on success.  -i: parameter i (BLAS position, counted as
+ *     in the prototype below) is invalid; NOTHING is enqueued or written.
+ *     > 0: runtime error (OZAKI_ERR_*); ozaki_last_error() has the message.
+ *   - Non-finite inputs: a row of op(A) / column of op(B) containing Inf/NaN
+ *     gives NaN in the corresponding row / column of alpha*P, and the sticky
+ *     non-finite counter in ozaki_stats_t is incremented (R10).  There is no
+ *     CPU fallback.
+ *   - Thread safety: re-entrant; the stream and last-error are thread-local.
+ */
+#ifndef OZAKI_H
+#define OZAKI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    OZAKI_OK = 0,
+    OZAKI_ERR_CUDA = 1,        /* a CUDA call or kernel launch failed          */
+    OZAKI_ERR_ALLOC = 2,       /* workspace allocation failed                 */
+    OZAKI_ERR_ARCH = 3,        /* current device is not sm_100 (B200/GB200)   */
+    OZAKI_ERR_UNSUPPORTED = 4, /* argument combination not supported          */
+    OZAKI_ERR_ALIAS = 5        /* C overlaps A or B                           */
+};
+
+/* Counters (monotonic since load or ozaki_reset_stats).  int8_gemm_equiv
+ * counts INT8 slice-pair GEMMs in the closed forms of SPEC.md:305-310:
+ * s(s+1)/2 per real product, x4 for 4M, x3 for 3M, times batch entries.  */
+typedef struct ozaki_stats {
+    uint64_t dgemm_calls;
+    uint64_t zgemm_calls;     /* 4M */
+    uint64_t zgemm3m_calls;   /* 3M */
+    uint64_t batch_entries;   /* products computed (1 per non-batched call)   */
+    uint64_t int8_gemm_equiv; /* slice-pair INT8 GEMMs (closed form)          */
+    uint64_t int8_macs;       /* INT8 multiply-accumulates issued (padded)    */
+    uint64_t k_chunks;        /* extra INT32 K-chunks needed (R8)             */
+    uint64_t nonfinite_rows;  /* rows/cols that contained Inf/NaN (synced)    */
+    uint64_t kernel_launches; /* device kernels launched by the library      */
+} ozaki_stats_t;
+
+/* --- real: C = alpha op(A) op(B) + beta C,  op(A) m x k, op(B) k x n ---------
+ * params: 1 transa 2 transb 3 m 4 n 5 k 6 alpha 7 A 8 lda 9 B 10 ldb
+ *         11 beta 12 C 13 ldc 14 num_slices                                  */
+int ozaki_dgemm(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                double alpha, const double *A, int64_t lda,
+                const double *B, int64_t ldb,
+                double beta, double *C, int64_t ldc, int num_slices);
+
+/* --- complex, 4M real embedding [[Ar,-Ai],[Ai,Ar]] [Br;Bi] (R9) -------------
+ * alpha, beta: HOST pointers to {re, im}.  Same parameter numbering.        */
+int ozaki_zgemm(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                const double *alpha, const double *A, int64_t lda,
+                const double *B, int64_t ldb,
+                const double *beta, double *C, int64_t ldc, int num_slices);
+
+/* --- complex, 3M: T1=ArBr, T2=AiBi, T3=fl(Ar+Ai)fl(Br+Bi) each emulated,
+ *     C_re = fl(T1-T2), C_im = fl(fl(T3-T1)-T2), then alpha/beta (R9)       */
+int ozaki_zgemm3m(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                  const double *alpha, const double *A, int64_t lda,
+                  const double *B, int64_t ldb,
+                  const double *beta, double *C, int64_t ldc, int num_slices);
+
+/* --- strided batched: entry b uses A + b*strideA, B + b*strideB,
+ *     C + b*strideC (strides in ELEMENTS: doubles for d, complex for z).
+ * params: 1 transa 2 transb 3 m 4 n 5 k 6 alpha 7 A 8 lda 9 strideA 10 B
+ *         11 ldb 12 strideB 13 beta 14 C 15 ldc 16 strideC 17 batch
+ *         18 num_slices.  All entries run in ONE persistent GEMM launch.    */
+int ozaki_dgemm_strided_batched(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                                double alpha, const double *A, int64_t lda, int64_t strideA,
+                                const double *B, int64_t ldb, int64_t strideB,
+                                double beta, double *C, int64_t ldc, int64_t strideC,
+                                int64_t batch, int num_slices);
+
+int ozaki_zgemm_strided_batched(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                                const double *alpha, const double *A, int64_t lda, int64_t strideA,
+                                const double *B, int64_t ldb, int64_t strideB,
+                                const double *beta, double *C, int64_t ldc, int64_t strideC,
+                                int64_t batch, int num_slices);
+
+int ozaki_zgemm3m_strided_batched(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                                  const double *alpha, const double *A, int64_t lda, int64_t strideA,
+                                  const double *B, int64_t ldb, int64_t strideB,
+                                  const double *beta, double *C, int64_t ldc, int64_t strideC,
+                                  int64_t batch, int num_slices);
+
+/* --- streams, stats, errors --------------------------------------------- */
+/* stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
+ * thread-local; returns 0.                                                 */
+int ozaki_set_stream(void *stream);
+void *ozaki_get_stream(void);
+/* Synchronises the device once to read the non-finite counter.           */
+int ozaki_get_stats(ozaki_stats_t *out);
+int ozaki_reset_stats(void);
+/* Bytes of device workspace one call of this shape needs.
+ * kind: 'd' real, 'z' 4M complex, '3' 3M complex.  -1 on bad arguments.   */
+int64_t ozaki_workspace_size(char kind, int64_t m, int64_t n, int64_t k, int64_t batch,
+                             int num_slices);
+/* Message of the last error on this thread ("" if none).                  */
+const char *ozaki_last_error(void);
+/* Library version string.                                                 */
+const char *ozaki_version(void);
+
+/* --- test-only debug entry points (same kernels, extra outputs) -----------
+ * ozaki_debug_split: run the split kernels on one operand.
+ *   side 'A': rows of op(X) where op(X) = X ('N') or X^T ('T'/'C');
+ *             X is rows x cols if trans=='N' else cols x rows (column-major).
+ *   side 'B': columns of op(X) where op(X) is cols x rows ... i.e. the
+ *             "rows" of the split are the columns of op(B): X is cols x rows
+ *             if trans == 'N' else rows x cols.
+ *   kind 'd' (real), 'z' (4M embedding; rows_out = 2*rows for side A),
+ *        'r','i','s' (3M operands Re, Im, fl(Re+Im) of complex X).
+ *   Outputs (DEVICE pointers): slices_out[t][r][l] int8 (t = 0..s-1 most
+ *   significant first, r over output rows, l over the output K depth
+ *   K' = cols (real/3M) or 2*round_up(cols,32) (4M)),
+ *   exps_out[r] int32 (0x3fffffff marks a non-finite row).
+ *   Returns the same codes as the GEMM routines.                           */
+int ozaki_debug_split(char side, char kind, char trans, int64_t rows, int64_t cols,
+                      const double *X, int64_t ldx, int num_slices,
+                      int8_t *slices_out, int32_t *exps_out, int64_t *kdepth_out);
+
+/* ozaki_debug_level_sums: the exact INT32 level sums S_L of a real product,
+ * S_out[(L-2)*m*n + j*m + i] for L = 2..s+1 (DEVICE pointer, column-major
+ * per level).  Same operand conventions as ozaki_dgemm.                   */
+int ozaki_debug_level_sums(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                           const double *A, int64_t lda, const double *B, int64_t ldb,
+                           int num_slices, int32_t *S_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OZAKI_H */

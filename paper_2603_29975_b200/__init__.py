@@ -1,0 +1,295 @@
+"""ozaki-b200: INT8 Ozaki-I emulation of FP64 DGEMM/ZGEMM on B200 (sm_100a).
+
+Thin Python binding over the C ABI in ``include/ozaki.h`` (``libozaki.so``,
+built in-tree by ``_build.py``).  The binding only marshals arguments: every
+step of the method runs in the library's CUDA kernels.  There is no CPU
+fallback -- importing this package on a machine without the built library, or
+calling it on a non-sm_100 device, raises.
+
+Matrix convention: BLAS column-major.  A torch tensor ``X`` of shape
+(rows, cols) is passed as-is when ``X.stride(0) == 1`` (column-major, leading
+dimension ``X.stride(1)``); use :func:`colmajor` to obtain such a tensor.
+Batched tensors are (batch, rows, cols) with ``stride(1) == 1``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = [
+    "OzakiError", "lib", "dgemm", "zgemm", "zgemm3m", "dgemm_strided_batched",
+    "zgemm_strided_batched", "zgemm3m_strided_batched", "set_stream", "get_stats",
+    "reset_stats", "workspace_size", "debug_split", "debug_level_sums", "colmajor",
+    "version", "pairs", "LIB_PATH",
+]
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libozaki.so")
+_lib = None
+
+
+class OzakiError(RuntimeError):
+    def __init__(self, code: int, where: str, msg: str):
+        super().__init__(f"{where}: code {code}: {msg}")
+        self.code = code
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in (
+        "dgemm_calls", "zgemm_calls", "zgemm3m_calls", "batch_entries", "int8_gemm_equiv",
+        "int8_macs", "k_chunks", "nonfinite_rows", "kernel_launches")]
+
+    def as_dict(self):
+        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
+def lib():
+    """Load libozaki.so (build it first if the sources are newer and nvcc exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        try:
+            from . import _build
+            _build.build()
+        except Exception as exc:  # noqa: BLE001
+            raise ImportError(f"libozaki.so missing and could not be built: {exc}") from exc
+    L = ctypes.CDLL(LIB_PATH)
+    c, i64, i32, dbl, p = ctypes.c_char, ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_void_p
+    dP = ctypes.POINTER(ctypes.c_double)
+    L.ozaki_dgemm.argtypes = [c, c, i64, i64, i64, dbl, p, i64, p, i64, dbl, p, i64, i32]
+    L.ozaki_zgemm.argtypes = [c, c, i64, i64, i64, dP, p, i64, p, i64, dP, p, i64, i32]
+    L.ozaki_zgemm3m.argtypes = L.ozaki_zgemm.argtypes
+    L.ozaki_dgemm_strided_batched.argtypes = [c, c, i64, i64, i64, dbl, p, i64, i64, p, i64, i64,
+                                              dbl, p, i64, i64, i64, i32]
+    L.ozaki_zgemm_strided_batched.argtypes = [c, c, i64, i64, i64, dP, p, i64, i64, p, i64, i64,
+                                              dP, p, i64, i64, i64, i32]
+    L.ozaki_zgemm3m_strided_batched.argtypes = L.ozaki_zgemm_strided_batched.argtypes
+    for f in ("ozaki_dgemm", "ozaki_zgemm", "ozaki_zgemm3m", "ozaki_dgemm_strided_batched",
+              "ozaki_zgemm_strided_batched", "ozaki_zgemm3m_strided_batched"):
+        getattr(L, f).restype = i32
+    L.ozaki_set_stream.argtypes = [p]
+    L.ozaki_set_stream.restype = i32
+    L.ozaki_get_stream.restype = p
+    L.ozaki_get_stats.argtypes = [ctypes.POINTER(Stats)]
+    L.ozaki_get_stats.restype = i32
+    L.ozaki_reset_stats.restype = i32
+    L.ozaki_workspace_size.argtypes = [c, i64, i64, i64, i64, i32]
+    L.ozaki_workspace_size.restype = i64
+    L.ozaki_last_error.restype = ctypes.c_char_p
+    L.ozaki_version.restype = ctypes.c_char_p
+    L.ozaki_debug_split.argtypes = [c, c, c, i64, i64, p, i64, i32, p, p, ctypes.POINTER(i64)]
+    L.ozaki_debug_split.restype = i32
+    L.ozaki_debug_level_sums.argtypes = [c, c, i64, i64, i64, p, i64, p, i64, i32, p]
+    L.ozaki_debug_level_sums.restype = i32
+    _lib = L
+    return L
+
+
+def version() -> str:
+    return lib().ozaki_version().decode()
+
+
+def pairs(s: int) -> int:
+    return s * (s + 1) // 2
+
+
+def _check(rc: int, where: str):
+    if rc != 0:
+        raise OzakiError(rc, where, lib().ozaki_last_error().decode())
+
+
+def _ch(t: str) -> bytes:
+    return t.encode()[:1]
+
+
+# ------------------------------------------------------------------ plumbing
+def colmajor(x):
+    """Return a column-major (Fortran-order) copy/view of a 2-D or batched tensor."""
+    import torch
+    if x.dim() == 2:
+        return x.t().contiguous().t() if x.stride(0) != 1 else x
+    if x.dim() == 3:
+        return x.transpose(1, 2).contiguous().transpose(1, 2) if x.stride(1) != 1 else x
+    raise ValueError("expected a 2-D or 3-D tensor")
+
+
+def _ld(x) -> int:
+    rows, cols = x.shape[-2], x.shape[-1]
+    if x.numel() == 0:
+        return max(1, rows)
+    if rows > 1 and x.stride(-2) != 1:
+        raise ValueError("matrix must be column-major (stride(-2) == 1); use colmajor()")
+    return max(1, x.stride(-1) if cols > 1 else rows)
+
+
+def _cuda(x, dtype, name):
+    import torch
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise TypeError(f"{name} must be a CUDA torch tensor")
+    if x.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {x.dtype}")
+    return x
+
+
+def _bind_stream(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    lib().ozaki_set_stream(ctypes.c_void_p(s.cuda_stream))
+
+
+def _dims(transa, transb, A, B):
+    ta, tb = transa.upper(), transb.upper()
+    m, k = (A.shape[-2], A.shape[-1]) if ta == "N" else (A.shape[-1], A.shape[-2])
+    kb, n = (B.shape[-2], B.shape[-1]) if tb == "N" else (B.shape[-1], B.shape[-2])
+    if k != kb:
+        raise ValueError(f"inner dimensions differ: op(A) is {m}x{k}, op(B) is {kb}x{n}")
+    return m, n, k
+
+
+def _cpair(z):
+    z = complex(z)
+    return (ctypes.c_double * 2)(z.real, z.imag)
+
+
+# ------------------------------------------------------------------ GEMMs
+def dgemm(transa, transb, alpha, A, B, beta, C, num_slices, stream=None):
+    """C <- alpha op(A) op(B) + beta C, emulated with ``num_slices`` INT8 slices."""
+    import torch
+    for x, nm in ((A, "A"), (B, "B"), (C, "C")):
+        _cuda(x, torch.float64, nm)
+    m, n, k = _dims(transa, transb, A, B)
+    if tuple(C.shape) != (m, n):
+        raise ValueError(f"C must be {m}x{n}")
+    _bind_stream(stream)
+    rc = lib().ozaki_dgemm(_ch(transa), _ch(transb), m, n, k, float(alpha), A.data_ptr(), _ld(A),
+                           B.data_ptr(), _ld(B), float(beta), C.data_ptr(), _ld(C), int(num_slices))
+    _check(rc, "ozaki_dgemm")
+    return C
+
+
+def _zgemm(fn, transa, transb, alpha, A, B, beta, C, num_slices, stream):
+    import torch
+    for x, nm in ((A, "A"), (B, "B"), (C, "C")):
+        _cuda(x, torch.complex128, nm)
+    m, n, k = _dims(transa, transb, A, B)
+    if tuple(C.shape) != (m, n):
+        raise ValueError(f"C must be {m}x{n}")
+    _bind_stream(stream)
+    rc = fn(_ch(transa), _ch(transb), m, n, k, _cpair(alpha), A.data_ptr(), _ld(A), B.data_ptr(),
+            _ld(B), _cpair(beta), C.data_ptr(), _ld(C), int(num_slices))
+    _check(rc, fn.__name__)
+    return C
+
+
+def zgemm(transa, transb, alpha, A, B, beta, C, num_slices, stream=None):
+    """Complex GEMM through the 4M real embedding (one INT8 GEMM of 2m x 2k x n)."""
+    return _zgemm(lib().ozaki_zgemm, transa, transb, alpha, A, B, beta, C, num_slices, stream)
+
+
+def zgemm3m(transa, transb, alpha, A, B, beta, C, num_slices, stream=None):
+    """Complex GEMM through 3M (three emulated real products)."""
+    return _zgemm(lib().ozaki_zgemm3m, transa, transb, alpha, A, B, beta, C, num_slices, stream)
+
+
+def _batched(fn, dtype, transa, transb, alpha, A, B, beta, C, num_slices, stream, cplx):
+    import torch
+    for x, nm in ((A, "A"), (B, "B"), (C, "C")):
+        _cuda(x, dtype, nm)
+        if x.dim() != 3:
+            raise ValueError(f"{nm} must be (batch, rows, cols)")
+    batch = A.shape[0]
+    if B.shape[0] != batch or C.shape[0] != batch:
+        raise ValueError("batch sizes differ")
+    m, n, k = _dims(transa, transb, A, B)
+    if tuple(C.shape[1:]) != (m, n):
+        raise ValueError(f"C entries must be {m}x{n}")
+    _bind_stream(stream)
+    al = _cpair(alpha) if cplx else float(alpha)
+    be = _cpair(beta) if cplx else float(beta)
+    sA = A.stride(0) if batch > 1 else 0
+    sB = B.stride(0) if batch > 1 else 0
+    sC = C.stride(0) if batch > 1 else 0
+    rc = fn(_ch(transa), _ch(transb), m, n, k, al, A.data_ptr(), _ld(A), sA, B.data_ptr(), _ld(B),
+            sB, be, C.data_ptr(), _ld(C), sC, batch, int(num_slices))
+    _check(rc, fn.__name__)
+    return C
+
+
+def dgemm_strided_batched(transa, transb, alpha, A, B, beta, C, num_slices, stream=None):
+    import torch
+    return _batched(lib().ozaki_dgemm_strided_batched, torch.float64, transa, transb, alpha, A, B,
+                    beta, C, num_slices, stream, False)
+
+
+def zgemm_strided_batched(transa, transb, alpha, A, B, beta, C, num_slices, stream=None):
+    import torch
+    return _batched(lib().ozaki_zgemm_strided_batched, torch.complex128, transa, transb, alpha, A,
+                    B, beta, C, num_slices, stream, True)
+
+
+def zgemm3m_strided_batched(transa, transb, alpha, A, B, beta, C, num_slices, stream=None):
+    import torch
+    return _batched(lib().ozaki_zgemm3m_strided_batched, torch.complex128, transa, transb, alpha,
+                    A, B, beta, C, num_slices, stream, True)
+
+
+# ------------------------------------------------------------- utilities
+def set_stream(stream) -> None:
+    lib().ozaki_set_stream(ctypes.c_void_p(getattr(stream, "cuda_stream", stream) or 0))
+
+
+def get_stats() -> dict:
+    st = Stats()
+    _check(lib().ozaki_get_stats(ctypes.byref(st)), "ozaki_get_stats")
+    return st.as_dict()
+
+
+def reset_stats() -> None:
+    lib().ozaki_reset_stats()
+
+
+def workspace_size(kind: str, m: int, n: int, k: int, batch: int, num_slices: int) -> int:
+    return int(lib().ozaki_workspace_size(_ch(kind), m, n, k, batch, num_slices))
+
+
+def debug_split(side, kind, trans, X, num_slices, stream=None):
+    """Run K1 on one operand; returns (slices[s][rows_out][kdepth] int8, exps int32).
+
+    side 'A': rows of op(X); side 'B': columns of op(X).  kind 'd' real,
+    'z' 4M embedding, 'r'/'i'/'s' 3M operands.  See include/ozaki.h."""
+    import torch
+    cplx = kind != "d"
+    _cuda(X, torch.complex128 if cplx else torch.float64, "X")
+    t = trans.upper()
+    if side.upper() == "A":
+        rows, cols = (X.shape[0], X.shape[1]) if t == "N" else (X.shape[1], X.shape[0])
+    else:
+        rows, cols = (X.shape[1], X.shape[0]) if t == "N" else (X.shape[0], X.shape[1])
+    rows_out = 2 * rows if (kind == "z" and side.upper() == "A") else rows
+    kdepth = cols if kind != "z" else 2 * ((cols + 31) // 32 * 32)
+    s = int(num_slices)
+    sl = torch.empty((s, rows_out, kdepth), dtype=torch.int8, device=X.device)
+    ex = torch.empty((rows_out,), dtype=torch.int32, device=X.device)
+    kd = ctypes.c_int64(0)
+    _bind_stream(stream)
+    rc = lib().ozaki_debug_split(_ch(side), _ch(kind), _ch(trans), rows, cols, X.data_ptr(), _ld(X),
+                                 s, sl.data_ptr(), ex.data_ptr(), ctypes.byref(kd))
+    _check(rc, "ozaki_debug_split")
+    assert kd.value == kdepth
+    return sl, ex
+
+
+def debug_level_sums(transa, transb, A, B, num_slices, stream=None):
+    """Exact INT32 level sums S[L-2] (m x n, torch row-major view) of a real product."""
+    import torch
+    _cuda(A, torch.float64, "A")
+    _cuda(B, torch.float64, "B")
+    m, n, k = _dims(transa, transb, A, B)
+    s = int(num_slices)
+    S = torch.zeros((s, n, m), dtype=torch.int32, device=A.device)   # column-major per level
+    _bind_stream(stream)
+    rc = lib().ozaki_debug_level_sums(_ch(transa), _ch(transb), m, n, k, A.data_ptr(), _ld(A),
+                                      B.data_ptr(), _ld(B), s, S.data_ptr())
+    _check(rc, "ozaki_debug_level_sums")
+    return S.transpose(1, 2)

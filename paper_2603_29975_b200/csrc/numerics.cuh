@@ -1,0 +1,67 @@
+// numerics.cuh -- FP64 bit-level helpers of the Ozaki-I path (device side).
+//
+// Written from the definitions in DESIGN.md §3 (R3 exponent rule, R4 fixed
+// point + balanced digits, R6 one correctly-rounded final scaling) using
+// integer operations on IEEE-754 bit patterns; deliberately NOT libm.
+#pragma once
+#include <cstdint>
+
+namespace ozk {
+
+constexpr int32_t kNonFinite = 0x3fffffff;      // exponent sentinel: row/col had Inf/NaN
+constexpr uint64_t kAbsMask = 0x7fffffffffffffffull;
+constexpr uint64_t kExpInf = 0x7ff0000000000000ull;
+constexpr uint64_t kFracMask = 0x000fffffffffffffull;
+
+// R3: exponent of a row/column from the bit pattern `u` of max |x| (finite,
+// any value incl. 0 and subnormals).  M = max|x|; e = least integer with
+// M < 2^e (frexp convention); if M * 2^(7-e) > 127 then e += 1.  M == 0 -> 0.
+// With M = 1.f * 2^E: e = E + 1 and M*2^(7-e) = 64 * 1.f, which exceeds 127
+// exactly when f > 63/64, i.e. the 52-bit fraction field > 63 * 2^46.
+__device__ __forceinline__ int32_t exponent_from_maxbits(uint64_t u) {
+    if (u == 0) return 0;
+    int32_t ex = (int32_t)(u >> 52);
+    uint64_t frac = u & kFracMask;
+    int32_t e;
+    if (ex == 0) {                        // subnormal: M = frac * 2^-1074
+        int32_t bl = 64 - __clzll((long long)frac);   // bit length of frac
+        e = bl - 1074;
+        frac = (frac << (53 - bl)) & kFracMask;   // normalised fraction bits
+    } else {
+        e = ex - 1022;
+    }
+    if (frac > (63ull << 46)) e += 1;
+    return e;
+}
+
+__device__ __forceinline__ double pow2(int n) {   // 2^n for n in [-1022, 1023]
+    return __longlong_as_double((long long)((uint64_t)(n + 1023) << 52));
+}
+
+// x * 2^n correctly rounded (RNE), x finite.  Normal results are exact
+// exponent adjustments; subnormal results come from ONE rounding multiply of
+// an exact operand; overflow gives +-Inf.
+__device__ __forceinline__ double ldexp_rn(double x, int n) {
+    uint64_t b = (uint64_t)__double_as_longlong(x);
+    uint64_t sign = b & ~kAbsMask;
+    uint64_t a = b & kAbsMask;
+    if (a == 0 || n == 0) return x;
+    int32_t ex = (int32_t)(a >> 52);
+    if (ex == 0) {                         // subnormal input: normalise exactly
+        x = __dmul_rn(x, 18014398509481984.0);   // 2^54, exact
+        n -= 54;
+        b = (uint64_t)__double_as_longlong(x);
+        a = b & kAbsMask;
+        ex = (int32_t)(a >> 52);
+    }
+    int32_t E = ex - 1023 + n;             // unbiased exponent of the result
+    if (E > 1023) return __longlong_as_double((long long)(sign | kExpInf));
+    if (E >= -1022)
+        return __longlong_as_double((long long)(sign | ((uint64_t)(E + 1023) << 52) | (a & kFracMask)));
+    if (E < -1075) return __longlong_as_double((long long)sign);   // below half the min subnormal
+    // y = 1.f * 2^-1022 exactly, then one rounding multiply by 2^(E+1022) in [2^-53, 2^-1]
+    double y = __longlong_as_double((long long)(sign | (1ull << 52) | (a & kFracMask)));
+    return __dmul_rn(y, pow2(E + 1022));
+}
+
+}  // namespace ozk

@@ -1,0 +1,755 @@
+// ozaki.cu -- host runtime of the C ABI declared in include/ozaki.h.
+//
+// Per call: BLAS argument checks (xerbla-style codes, nothing enqueued on
+// error) -> quick returns -> a plan (slice layout, tile grid, pipeline depth)
+// -> stream-ordered workspace -> K1 (exponents, slices) for both operands ->
+// K2+K3 persistent GEMM with the fused FP64 epilogue.  Everything is enqueued
+// on the caller's stream; nothing synchronises the host.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "gemm.cuh"
+#include "ozaki.h"
+#include "split.cuh"
+
+using namespace ozk;
+
+namespace {
+
+thread_local cudaStream_t t_stream = nullptr;
+thread_local std::string t_err;
+
+struct Stats {
+    std::atomic<uint64_t> dgemm{0}, zgemm{0}, zgemm3m{0}, entries{0}, equiv{0}, macs{0},
+        chunks{0}, launches{0};
+} g_stats;
+
+constexpr int kMaxDev = 64;
+struct DevState {
+    bool init = false;
+    bool ok = false;
+    int sms = 0;
+    unsigned long long *nonfinite = nullptr;
+    uint64_t nonfinite_base = 0;
+};
+DevState g_dev[kMaxDev];
+std::mutex g_mu;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    t_err = buf;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+    do {                                                                                 \
+        cudaError_t _e = (expr);                                                         \
+        if (_e != cudaSuccess)                                                           \
+            return fail(OZAKI_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e)); \
+    } while (0)
+
+template <int BN, int EPI>
+int set_gemm_attr(size_t smem) {
+    static std::atomic<size_t> done{0};
+    if (done.load() >= smem) return 0;
+    CUDA_TRY(cudaFuncSetAttribute(k_gemm<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)std::max<size_t>(smem, 48 * 1024)));
+    done.store(smem);
+    return 0;
+}
+
+int device_state(DevState **out) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= kMaxDev) return fail(OZAKI_ERR_CUDA, "device index %d out of range", dev);
+    std::lock_guard<std::mutex> lk(g_mu);
+    DevState &d = g_dev[dev];
+    if (!d.init) {
+        cudaDeviceProp prop;
+        CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
+        d.init = true;
+        d.ok = (prop.major == 10 && prop.minor == 0);
+        d.sms = prop.multiProcessorCount;
+        if (d.ok) {
+            CUDA_TRY(cudaMalloc(&d.nonfinite, sizeof(unsigned long long)));
+            CUDA_TRY(cudaMemset(d.nonfinite, 0, sizeof(unsigned long long)));
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;   // keep freed workspace cached in the pool
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+        }
+    }
+    if (!d.ok) return fail(OZAKI_ERR_ARCH, "device %d is not sm_100 (B200/GB200)", dev);
+    *out = &d;
+    return 0;
+}
+
+bool trans_ok(char t) {
+    return t == 'N' || t == 'n' || t == 'T' || t == 't' || t == 'C' || t == 'c';
+}
+char up(char t) { return (char)(t >= 'a' ? t - 32 : t); }
+int64_t rup(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+enum Kind { KIND_REAL = 0, KIND_4M = 1, KIND_3M = 2 };
+
+// ------------------------------------------------------------------- plan
+struct Plan {
+    int s, BN;
+    int64_t m, n, k, batch;
+    int64_t Mp;          // output rows of the real product (2m for 4M)
+    int64_t kh;          // 4M half width
+    int64_t Kp, KB;      // padded depth (bytes) and 32-B blocks
+    int64_t tiles_m, tiles_n;
+    size_t a_bytes, b_bytes, ea_bytes, fb_bytes;   // per whole batch, 256-B aligned
+    int kps, stages;
+    size_t smem;
+};
+
+size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+int make_plan(Kind kind, int64_t m, int64_t n, int64_t k, int64_t batch, int s, Plan &P) {
+    P.s = s;
+    P.BN = (s <= 8) ? 64 : 32;
+    P.m = m;
+    P.n = n;
+    P.k = k;
+    P.batch = batch;
+    if (kind == KIND_4M) {
+        P.Mp = 2 * m;
+        P.kh = rup(k, 32);
+        P.Kp = 2 * P.kh;
+    } else {
+        P.Mp = m;
+        P.kh = 0;
+        P.Kp = rup(k, 32);
+    }
+    // R8: a level sums (L-1) * k_eff products of magnitude <= 2^14 in INT32.
+    const int64_t keff = (kind == KIND_4M) ? 2 * k : k;
+    if ((int64_t)s * keff > 131071)
+        return fail(OZAKI_ERR_UNSUPPORTED,
+                    "s*k_eff = %lld exceeds the INT32 level-sum bound 131071 (K-chunking not in "
+                    "this build)",
+                    (long long)((int64_t)s * keff));
+    P.KB = P.Kp / 32;
+    P.tiles_m = (P.Mp + kBM - 1) / kBM;
+    P.tiles_n = (n + P.BN - 1) / P.BN;
+    const size_t a_kb = (size_t)s * kBM * kKB, b_kb = (size_t)s * P.BN * kKB;
+    P.a_bytes = al256(a_kb * P.KB * P.tiles_m * batch);
+    P.b_bytes = al256(b_kb * P.KB * P.tiles_n * batch);
+    P.ea_bytes = al256(sizeof(int32_t) * P.Mp * batch);
+    P.fb_bytes = al256(sizeof(int32_t) * n * batch);
+    const size_t kb_bytes = a_kb + b_kb;
+    const size_t budget = 224 * 1024;
+    P.kps = (int)std::max<size_t>(1, std::min<size_t>(40960 / kb_bytes, (size_t)P.KB));
+    P.stages = (int)std::min<size_t>(8, (budget - 2048) / (P.kps * kb_bytes));
+    if (P.stages < 2) return fail(OZAKI_ERR_UNSUPPORTED, "pipeline does not fit in shared memory");
+    P.smem = (size_t)P.stages * P.kps * kb_bytes + 1024 /*align*/ + 256 /*barriers*/;
+    return 0;
+}
+
+size_t plan_workspace(const Plan &P) { return P.a_bytes + P.b_bytes + P.ea_bytes + P.fb_bytes; }
+
+// ------------------------------------------------------------ small kernels
+__global__ void k_scale_real(double *C, int64_t m, int64_t n, int64_t ldc, int64_t strideC,
+                             double beta) {
+    const int64_t b = blockIdx.z;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < m * n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = idx % m, j = idx / m;
+        double *cp = C + b * strideC + i + j * ldc;
+        *cp = (beta == 0.0) ? 0.0 : __dmul_rn(beta, *cp);
+    }
+}
+
+__global__ void k_scale_cplx(double *C, int64_t m, int64_t n, int64_t ldc, int64_t strideC,
+                             double br, double bi) {
+    const int64_t b = blockIdx.z;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < m * n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = idx % m, j = idx / m;
+        double2 *cp = reinterpret_cast<double2 *>(C) + b * strideC + i + j * ldc;
+        if (br == 0.0 && bi == 0.0) {
+            *cp = make_double2(0.0, 0.0);
+        } else {
+            double2 c = *cp;
+            *cp = make_double2(__fma_rn(br, c.x, -__dmul_rn(bi, c.y)), __fma_rn(br, c.y, __dmul_rn(bi, c.x)));
+        }
+    }
+}
+
+// 3M: C_re = fl(T1-T2), C_im = fl(fl(T3-T1)-T2), then complex alpha/beta (R7, R9).
+__global__ void k_combine_3m(const double *T1, const double *T2, const double *T3, double *C,
+                             int64_t m, int64_t n, int64_t ldc, int64_t strideC, double ar,
+                             double ai, double br, double bi) {
+    const int64_t b = blockIdx.z;
+    const int64_t off = b * m * n;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < m * n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx % m, j = idx / m;
+        const double t1 = T1[off + idx], t2 = T2[off + idx], t3 = T3[off + idx];
+        const double pr = __dsub_rn(t1, t2);
+        const double pi = __dsub_rn(__dsub_rn(t3, t1), t2);
+        double2 *cp = reinterpret_cast<double2 *>(C) + b * strideC + i + j * ldc;
+        double tr = 0.0, ti = 0.0;
+        if (!(br == 0.0 && bi == 0.0)) {
+            double2 c = *cp;
+            tr = __fma_rn(br, c.x, -__dmul_rn(bi, c.y));
+            ti = __fma_rn(br, c.y, __dmul_rn(bi, c.x));
+        }
+        *cp = make_double2(__fma_rn(ar, pr, __fma_rn(-ai, pi, tr)), __fma_rn(ar, pi, __fma_rn(ai, pr, ti)));
+    }
+}
+
+// Debug: tiled slices -> plain [s][rows_out][kdepth] int8.
+__global__ void k_unpack(const int8_t *tiled, int8_t *out, int64_t rows_out, int64_t kdepth,
+                         int s, int tile_h, int64_t KB) {
+    const int64_t total = (int64_t)s * rows_out * kdepth;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t l = idx % kdepth;
+        const int64_t r = (idx / kdepth) % rows_out;
+        const int64_t t = idx / (kdepth * rows_out);
+        const int64_t tile = r / tile_h, rr = r % tile_h, kb = l / 32, c = (l % 32) / 16, x = l % 16;
+        const int64_t off = ((tile * KB + kb) * s + t) * (int64_t)tile_h * 32 + (rr >> 3) * 256 +
+                            c * 128 + (rr & 7) * 16 + x;
+        out[idx] = tiled[off];
+    }
+}
+
+unsigned grid1d(int64_t work, int sms) {
+    int64_t g = (work + 255) / 256;
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)sms * 16));
+}
+
+// ---------------------------------------------------------------- K1 launch
+struct Operand {
+    const void *X;
+    int64_t rs, ls, bstride;
+    int64_t rows, k;
+    int mode, conj;
+};
+
+int launch_split(const Plan &P, const Operand &op, bool sideA, int8_t *slices, int32_t *exps,
+                 DevState *dev, cudaStream_t st) {
+    SplitParams sp{};
+    sp.X = op.X;
+    sp.rs = op.rs;
+    sp.ls = op.ls;
+    sp.bstride = op.bstride;
+    sp.rows = op.rows;
+    sp.k = op.k;
+    sp.mode = op.mode;
+    sp.conj = op.conj;
+    sp.s = P.s;
+    sp.tile_h = sideA ? kBM : P.BN;
+    sp.tiles = sideA ? P.tiles_m : P.tiles_n;
+    sp.KB = P.KB;
+    sp.kh = P.kh;
+    sp.rows_out = (op.mode == SPLIT_A4M) ? 2 * op.rows : op.rows;
+    sp.rows_grid = (op.mode == SPLIT_A4M) ? sp.tiles * sp.tile_h / 2 : sp.tiles * sp.tile_h;
+    sp.out = slices;
+    sp.exps = exps;
+    sp.nonfinite = dev->nonfinite;
+    if (op.rows == 0) return 0;
+    const bool rcontig = (op.rs == 1);
+    const dim3 blk(32, 8);
+    if (rcontig) {
+        dim3 grid((unsigned)((op.rows + 31) / 32), 1, (unsigned)P.batch);
+        k_exponent<true><<<grid, blk, 0, st>>>(sp);
+    } else {
+        dim3 grid((unsigned)((op.rows + 7) / 8), 1, (unsigned)P.batch);
+        k_exponent<false><<<grid, blk, 0, st>>>(sp);
+    }
+    CUDA_TRY(cudaGetLastError());
+    const bool four_m = (op.mode == SPLIT_A4M || op.mode == SPLIT_B4M);
+    const int64_t nchunks = four_m ? (P.kh >> 4) : (P.KB * 2);
+    dim3 grid2((unsigned)((sp.rows_grid + 63) / 64), (unsigned)((nchunks + 3) / 4), (unsigned)P.batch);
+    if (P.s <= 8)
+        k_slice<8><<<grid2, dim3(64, 4), 0, st>>>(sp);
+    else
+        k_slice<16><<<grid2, dim3(64, 4), 0, st>>>(sp);
+    CUDA_TRY(cudaGetLastError());
+    g_stats.launches += 2;
+    return 0;
+}
+
+// ---------------------------------------------------------------- K2 launch
+template <int BN, int EPI>
+int launch_gemm_t(const Plan &P, const GemmParams &gp, DevState *dev, cudaStream_t st) {
+    if (int rc = set_gemm_attr<BN, EPI>(P.smem)) return rc;
+    const int64_t tiles = P.batch * P.tiles_m * P.tiles_n;
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, dev->sms);
+    k_gemm<BN, EPI><<<grid, kGemmThreads, P.smem, st>>>(gp);
+    CUDA_TRY(cudaGetLastError());
+    g_stats.launches += 1;
+    return 0;
+}
+
+int launch_gemm(const Plan &P, int epi, const int8_t *sa, const int8_t *sb, const int32_t *ea,
+                const int32_t *fb, double *C, int64_t ldc, int64_t strideC, const double al[2],
+                const double be[2], int32_t *S_out, DevState *dev, cudaStream_t st) {
+    GemmParams gp{};
+    gp.A = sa;
+    gp.B = sb;
+    gp.ea = ea;
+    gp.fb = fb;
+    gp.Mp = P.Mp;
+    gp.N = P.n;
+    gp.KB = P.KB;
+    gp.tiles_m = P.tiles_m;
+    gp.tiles_n = P.tiles_n;
+    gp.batch = P.batch;
+    gp.s = P.s;
+    gp.kps = P.kps;
+    gp.stages = P.stages;
+    gp.a_kb_bytes = (uint32_t)(P.s * kBM * kKB);
+    gp.b_kb_bytes = (uint32_t)(P.s * P.BN * kKB);
+    gp.C = C;
+    gp.ldc = ldc;
+    gp.strideC = strideC;
+    gp.alpha_r = al[0];
+    gp.alpha_i = al[1];
+    gp.beta_r = be[0];
+    gp.beta_i = be[1];
+    gp.S_out = S_out;
+    if (P.BN == 64) {
+        if (epi == EPI_REAL) return launch_gemm_t<64, EPI_REAL>(P, gp, dev, st);
+        if (epi == EPI_CPLX4M) return launch_gemm_t<64, EPI_CPLX4M>(P, gp, dev, st);
+        return launch_gemm_t<64, EPI_LEVELS>(P, gp, dev, st);
+    }
+    if (epi == EPI_REAL) return launch_gemm_t<32, EPI_REAL>(P, gp, dev, st);
+    if (epi == EPI_CPLX4M) return launch_gemm_t<32, EPI_CPLX4M>(P, gp, dev, st);
+    return launch_gemm_t<32, EPI_LEVELS>(P, gp, dev, st);
+}
+
+// Views of op(A) rows / op(B) columns over column-major storage.
+Operand view_A(const double *A, char ta, int64_t m, int64_t k, int64_t lda, int64_t strideA,
+               int mode) {
+    Operand o{};
+    o.X = A;
+    o.rows = m;
+    o.k = k;
+    o.bstride = strideA;
+    o.mode = mode;
+    if (ta == 'N') {   // row i of A: A[i + l*lda]
+        o.rs = 1;
+        o.ls = lda;
+    } else {           // row i of A^T: column i of A
+        o.rs = lda;
+        o.ls = 1;
+        o.conj = (ta == 'C' && mode != SPLIT_REAL) ? 1 : 0;
+    }
+    return o;
+}
+
+Operand view_B(const double *B, char tb, int64_t n, int64_t k, int64_t ldb, int64_t strideB,
+               int mode) {
+    Operand o{};
+    o.X = B;
+    o.rows = n;
+    o.k = k;
+    o.bstride = strideB;
+    o.mode = mode;
+    if (tb == 'N') {   // column j of B: B[l + j*ldb]
+        o.rs = ldb;
+        o.ls = 1;
+    } else {           // column j of B^T: row j of B
+        o.rs = 1;
+        o.ls = ldb;
+        o.conj = (tb == 'C' && mode != SPLIT_REAL) ? 1 : 0;
+    }
+    return o;
+}
+
+bool overlaps(const void *a, size_t abytes, const void *b, size_t bbytes) {
+    const char *x = (const char *)a, *y = (const char *)b;
+    return abytes && bbytes && x < y + bbytes && y < x + abytes;
+}
+
+size_t span_bytes(int64_t rows, int64_t cols, int64_t ld, int64_t stride, int64_t batch, size_t es) {
+    if (rows == 0 || cols == 0 || batch == 0) return 0;
+    return es * (size_t)((batch - 1) * stride + (cols - 1) * ld + rows);
+}
+
+struct Call {
+    Kind kind;
+    char ta, tb;
+    int64_t m, n, k;
+    double al[2], be[2];
+    const double *A;
+    int64_t lda, sA;
+    const double *B;
+    int64_t ldb, sB;
+    double *C;
+    int64_t ldc, sC, batch;
+    int s;
+    bool batched;
+    int32_t *S_out;   // debug level dump (real only)
+};
+
+int validate(const Call &c) {
+    const bool b = c.batched;
+    if (!trans_ok(c.ta)) return fail(-1, "transa");
+    if (!trans_ok(c.tb)) return fail(-2, "transb");
+    if (c.m < 0) return fail(-3, "m < 0");
+    if (c.n < 0) return fail(-4, "n < 0");
+    if (c.k < 0) return fail(-5, "k < 0");
+    const char ta = up(c.ta), tb = up(c.tb);
+    if (c.lda < std::max<int64_t>(1, ta == 'N' ? c.m : c.k)) return fail(-8, "lda too small");
+    if (b && c.sA < 0) return fail(-9, "strideA < 0");
+    if (c.ldb < std::max<int64_t>(1, tb == 'N' ? c.k : c.n)) return fail(b ? -11 : -10, "ldb too small");
+    if (b && c.sB < 0) return fail(-12, "strideB < 0");
+    if (c.ldc < std::max<int64_t>(1, c.m)) return fail(b ? -15 : -13, "ldc too small");
+    if (b && c.sC < 0) return fail(-16, "strideC < 0");
+    if (b && c.batch < 0) return fail(-17, "batch < 0");
+    if (c.s < 1 || c.s > 16) return fail(b ? -18 : -14, "num_slices not in [1,16]");
+    return 0;
+}
+
+int run(const Call &c0) {
+    t_err.clear();
+    if (int rc = validate(c0)) return rc;
+    Call c = c0;
+    c.ta = up(c.ta);
+    c.tb = up(c.tb);
+    if (c.kind == KIND_REAL) {   // 'C' == 'T' for real operands
+        if (c.ta == 'C') c.ta = 'T';
+        if (c.tb == 'C') c.tb = 'T';
+    }
+    if (c.m == 0 || c.n == 0 || c.batch == 0) return 0;
+    DevState *dev = nullptr;
+    if (int rc = device_state(&dev)) return rc;
+    cudaStream_t st = t_stream;
+    const size_t es = (c.kind == KIND_REAL) ? 8 : 16;
+    const bool cplx = c.kind != KIND_REAL;
+    const bool alpha0 = c.al[0] == 0.0 && c.al[1] == 0.0;
+    const bool beta1 = c.be[0] == 1.0 && c.be[1] == 0.0;
+
+    // C must not alias A or B (only checked when A/B are read)
+    if (!alpha0 && c.k > 0) {
+        const size_t cb = span_bytes(c.m, c.n, c.ldc, c.sC, c.batch, es);
+        const int64_t ar = c.ta == 'N' ? c.m : c.k, ac = c.ta == 'N' ? c.k : c.m;
+        const int64_t br = c.tb == 'N' ? c.k : c.n, bc = c.tb == 'N' ? c.n : c.k;
+        if (overlaps(c.C, cb, c.A, span_bytes(ar, ac, c.lda, c.sA, c.batch, es)) ||
+            overlaps(c.C, cb, c.B, span_bytes(br, bc, c.ldb, c.sB, c.batch, es)))
+            return fail(OZAKI_ERR_ALIAS, "C overlaps A or B");
+    }
+    // quick return (R7): alpha == 0 or k == 0 -> C = beta C
+    if (alpha0 || c.k == 0) {
+        if (beta1 || c.S_out) return 0;
+        dim3 grid(grid1d(c.m * c.n, dev->sms), 1, (unsigned)c.batch);
+        if (cplx)
+            k_scale_cplx<<<grid, 256, 0, st>>>(c.C, c.m, c.n, c.ldc, c.sC, c.be[0], c.be[1]);
+        else
+            k_scale_real<<<grid, 256, 0, st>>>(c.C, c.m, c.n, c.ldc, c.sC, c.be[0]);
+        CUDA_TRY(cudaGetLastError());
+        g_stats.launches += 1;
+        return 0;
+    }
+
+    Plan P;
+    const Kind pk = (c.kind == KIND_4M) ? KIND_4M : KIND_REAL;
+    if (int rc = make_plan(pk, c.m, c.n, c.k, c.batch, c.s, P)) return rc;
+    size_t ws = plan_workspace(P);
+    size_t t_bytes = 0;
+    if (c.kind == KIND_3M) t_bytes = al256(sizeof(double) * c.m * c.n * c.batch);
+    ws += 3 * t_bytes;
+
+    void *base = nullptr;
+    {
+        cudaError_t e = cudaMallocAsync(&base, ws, st);
+        if (e != cudaSuccess) return fail(OZAKI_ERR_ALLOC, "cudaMallocAsync(%zu): %s", ws, cudaGetErrorString(e));
+    }
+    int8_t *sa = (int8_t *)base;
+    int8_t *sb = sa + P.a_bytes;
+    int32_t *ea = (int32_t *)(sb + P.b_bytes);
+    int32_t *fb = (int32_t *)((char *)ea + P.ea_bytes);
+    double *T = (double *)((char *)fb + P.fb_bytes);
+    int rc = 0;
+
+    if (c.kind == KIND_REAL || c.kind == KIND_4M) {
+        const int ma = (c.kind == KIND_4M) ? SPLIT_A4M : SPLIT_REAL;
+        const int mb = (c.kind == KIND_4M) ? SPLIT_B4M : SPLIT_REAL;
+        rc = launch_split(P, view_A(c.A, c.ta, c.m, c.k, c.lda, c.sA, ma), true, sa, ea, dev, st);
+        if (!rc) rc = launch_split(P, view_B(c.B, c.tb, c.n, c.k, c.ldb, c.sB, mb), false, sb, fb, dev, st);
+        if (!rc) {
+            const int epi = c.S_out ? EPI_LEVELS : (c.kind == KIND_4M ? EPI_CPLX4M : EPI_REAL);
+            rc = launch_gemm(P, epi, sa, sb, ea, fb, c.C, c.ldc, c.sC, c.al, c.be, c.S_out, dev, st);
+        }
+    } else {   // 3M: three emulated real products into T, then the combine
+        const int modes[3] = {SPLIT_RE, SPLIT_IM, SPLIT_SUM};
+        const double one[2] = {1.0, 0.0}, zero[2] = {0.0, 0.0};
+        for (int x = 0; x < 3 && !rc; ++x) {
+            double *Tx = (double *)((char *)T + x * t_bytes);
+            rc = launch_split(P, view_A(c.A, c.ta, c.m, c.k, c.lda, c.sA, modes[x]), true, sa, ea, dev, st);
+            if (!rc) rc = launch_split(P, view_B(c.B, c.tb, c.n, c.k, c.ldb, c.sB, modes[x]), false, sb, fb, dev, st);
+            if (!rc) rc = launch_gemm(P, EPI_REAL, sa, sb, ea, fb, Tx, c.m, c.m * c.n, one, zero, nullptr, dev, st);
+        }
+        if (!rc) {
+            dim3 grid(grid1d(c.m * c.n, dev->sms), 1, (unsigned)c.batch);
+            k_combine_3m<<<grid, 256, 0, st>>>(T, (double *)((char *)T + t_bytes),
+                                              (double *)((char *)T + 2 * t_bytes), c.C, c.m, c.n,
+                                              c.ldc, c.sC, c.al[0], c.al[1], c.be[0], c.be[1]);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) rc = fail(OZAKI_ERR_CUDA, "combine_3m: %s", cudaGetErrorString(e));
+            g_stats.launches += 1;
+        }
+    }
+    cudaFreeAsync(base, st);
+    if (rc) return rc;
+
+    const uint64_t pr = (uint64_t)c.s * (c.s + 1) / 2;
+    const uint64_t mult = c.kind == KIND_REAL ? 1 : (c.kind == KIND_4M ? 4 : 3);
+    g_stats.entries += (uint64_t)c.batch;
+    g_stats.equiv += pr * mult * (uint64_t)c.batch;
+    g_stats.macs += pr * (uint64_t)(c.kind == KIND_3M ? 3 : 1) * (uint64_t)P.tiles_m * kBM *
+                    (uint64_t)P.tiles_n * P.BN * (uint64_t)P.Kp * (uint64_t)c.batch;
+    if (c.kind == KIND_REAL) g_stats.dgemm += 1;
+    if (c.kind == KIND_4M) g_stats.zgemm += 1;
+    if (c.kind == KIND_3M) g_stats.zgemm3m += 1;
+    return 0;
+}
+
+Call make_call(Kind kind, char ta, char tb, int64_t m, int64_t n, int64_t k, const double *al,
+               const double *A, int64_t lda, int64_t sA, const double *B, int64_t ldb, int64_t sB,
+               const double *be, double *C, int64_t ldc, int64_t sC, int64_t batch, int s,
+               bool batched) {
+    Call c{};
+    c.kind = kind;
+    c.ta = ta;
+    c.tb = tb;
+    c.m = m;
+    c.n = n;
+    c.k = k;
+    c.al[0] = al[0];
+    c.al[1] = kind == KIND_REAL ? 0.0 : al[1];
+    c.be[0] = be[0];
+    c.be[1] = kind == KIND_REAL ? 0.0 : be[1];
+    c.A = A;
+    c.lda = lda;
+    c.sA = sA;
+    c.B = B;
+    c.ldb = ldb;
+    c.sB = sB;
+    c.C = C;
+    c.ldc = ldc;
+    c.sC = sC;
+    c.batch = batch;
+    c.s = s;
+    c.batched = batched;
+    return c;
+}
+
+}  // namespace
+
+// =========================================================================
+extern "C" {
+
+int ozaki_dgemm(char transa, char transb, int64_t m, int64_t n, int64_t k, double alpha,
+                const double *A, int64_t lda, const double *B, int64_t ldb, double beta, double *C,
+                int64_t ldc, int num_slices) {
+    const double al[2] = {alpha, 0.0}, be[2] = {beta, 0.0};
+    return run(make_call(KIND_REAL, transa, transb, m, n, k, al, A, lda, 0, B, ldb, 0, be, C, ldc,
+                         0, 1, num_slices, false));
+}
+
+int ozaki_zgemm(char transa, char transb, int64_t m, int64_t n, int64_t k, const double *alpha,
+                const double *A, int64_t lda, const double *B, int64_t ldb, const double *beta,
+                double *C, int64_t ldc, int num_slices) {
+    return run(make_call(KIND_4M, transa, transb, m, n, k, alpha, A, lda, 0, B, ldb, 0, beta, C,
+                         ldc, 0, 1, num_slices, false));
+}
+
+int ozaki_zgemm3m(char transa, char transb, int64_t m, int64_t n, int64_t k, const double *alpha,
+                  const double *A, int64_t lda, const double *B, int64_t ldb, const double *beta,
+                  double *C, int64_t ldc, int num_slices) {
+    return run(make_call(KIND_3M, transa, transb, m, n, k, alpha, A, lda, 0, B, ldb, 0, beta, C,
+                         ldc, 0, 1, num_slices, false));
+}
+
+int ozaki_dgemm_strided_batched(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                                double alpha, const double *A, int64_t lda, int64_t strideA,
+                                const double *B, int64_t ldb, int64_t strideB, double beta,
+                                double *C, int64_t ldc, int64_t strideC, int64_t batch,
+                                int num_slices) {
+    const double al[2] = {alpha, 0.0}, be[2] = {beta, 0.0};
+    return run(make_call(KIND_REAL, transa, transb, m, n, k, al, A, lda, strideA, B, ldb, strideB,
+                         be, C, ldc, strideC, batch, num_slices, true));
+}
+
+int ozaki_zgemm_strided_batched(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                                const double *alpha, const double *A, int64_t lda,
+                                int64_t strideA, const double *B, int64_t ldb, int64_t strideB,
+                                const double *beta, double *C, int64_t ldc, int64_t strideC,
+                                int64_t batch, int num_slices) {
+    return run(make_call(KIND_4M, transa, transb, m, n, k, alpha, A, lda, strideA, B, ldb, strideB,
+                         beta, C, ldc, strideC, batch, num_slices, true));
+}
+
+int ozaki_zgemm3m_strided_batched(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                                  const double *alpha, const double *A, int64_t lda,
+                                  int64_t strideA, const double *B, int64_t ldb, int64_t strideB,
+                                  const double *beta, double *C, int64_t ldc, int64_t strideC,
+                                  int64_t batch, int num_slices) {
+    return run(make_call(KIND_3M, transa, transb, m, n, k, alpha, A, lda, strideA, B, ldb, strideB,
+                         beta, C, ldc, strideC, batch, num_slices, true));
+}
+
+int ozaki_set_stream(void *stream) {
+    t_stream = (cudaStream_t)stream;
+    return 0;
+}
+
+void *ozaki_get_stream(void) { return (void *)t_stream; }
+
+int ozaki_get_stats(ozaki_stats_t *out) {
+    if (!out) return -1;
+    std::memset(out, 0, sizeof *out);
+    out->dgemm_calls = g_stats.dgemm;
+    out->zgemm_calls = g_stats.zgemm;
+    out->zgemm3m_calls = g_stats.zgemm3m;
+    out->batch_entries = g_stats.entries;
+    out->int8_gemm_equiv = g_stats.equiv;
+    out->int8_macs = g_stats.macs;
+    out->k_chunks = g_stats.chunks;
+    out->kernel_launches = g_stats.launches;
+    uint64_t nf = 0;
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (int d = 0; d < kMaxDev; ++d) {
+        if (g_dev[d].init && g_dev[d].ok && g_dev[d].nonfinite) {
+            int cur = 0;
+            cudaGetDevice(&cur);
+            cudaSetDevice(d);
+            cudaDeviceSynchronize();
+            unsigned long long v = 0;
+            cudaMemcpy(&v, g_dev[d].nonfinite, sizeof v, cudaMemcpyDeviceToHost);
+            nf += v - g_dev[d].nonfinite_base;
+            cudaSetDevice(cur);
+        }
+    }
+    out->nonfinite_rows = nf;
+    return 0;
+}
+
+int ozaki_reset_stats(void) {
+    g_stats.dgemm = 0;
+    g_stats.zgemm = 0;
+    g_stats.zgemm3m = 0;
+    g_stats.entries = 0;
+    g_stats.equiv = 0;
+    g_stats.macs = 0;
+    g_stats.chunks = 0;
+    g_stats.launches = 0;
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (int d = 0; d < kMaxDev; ++d) {
+        if (g_dev[d].init && g_dev[d].ok && g_dev[d].nonfinite) {
+            int cur = 0;
+            cudaGetDevice(&cur);
+            cudaSetDevice(d);
+            cudaDeviceSynchronize();
+            unsigned long long v = 0;
+            cudaMemcpy(&v, g_dev[d].nonfinite, sizeof v, cudaMemcpyDeviceToHost);
+            g_dev[d].nonfinite_base = v;
+            cudaSetDevice(cur);
+        }
+    }
+    return 0;
+}
+
+int64_t ozaki_workspace_size(char kind, int64_t m, int64_t n, int64_t k, int64_t batch,
+                             int num_slices) {
+    if (m < 0 || n < 0 || k < 0 || batch < 0 || num_slices < 1 || num_slices > 16) return -1;
+    Plan P;
+    const Kind kd = kind == 'z' ? KIND_4M : KIND_REAL;
+    if (make_plan(kd, m, n, k, batch, num_slices, P)) return -1;
+    int64_t ws = (int64_t)plan_workspace(P);
+    if (kind == '3') ws += 3 * (int64_t)al256(sizeof(double) * m * n * batch);
+    return ws;
+}
+
+const char *ozaki_last_error(void) { return t_err.c_str(); }
+
+const char *ozaki_version(void) { return "ozaki-b200 0.1 (sm_100a, tcgen05 kind::i8)"; }
+
+int ozaki_debug_split(char side, char kind, char trans, int64_t rows, int64_t cols,
+                      const double *X, int64_t ldx, int num_slices, int8_t *slices_out,
+                      int32_t *exps_out, int64_t *kdepth_out) {
+    t_err.clear();
+    side = up(side);
+    trans = up(trans);
+    if (side != 'A' && side != 'B') return fail(-1, "side");
+    int mode;
+    switch (kind) {
+        case 'd': mode = SPLIT_REAL; break;
+        case 'z': mode = side == 'A' ? SPLIT_A4M : SPLIT_B4M; break;
+        case 'r': mode = SPLIT_RE; break;
+        case 'i': mode = SPLIT_IM; break;
+        case 's': mode = SPLIT_SUM; break;
+        default: return fail(-2, "kind");
+    }
+    if (!trans_ok(trans)) return fail(-3, "trans");
+    if (rows < 0) return fail(-4, "rows");
+    if (cols < 0) return fail(-5, "cols");
+    if (num_slices < 1 || num_slices > 16) return fail(-8, "num_slices");
+    if (mode == SPLIT_REAL && trans == 'C') trans = 'T';
+    DevState *dev = nullptr;
+    if (int rc = device_state(&dev)) return rc;
+    cudaStream_t st = t_stream;
+    // describe the operand as side A (m = rows, k = cols) or side B (n = rows, k = cols)
+    Plan P;
+    const Kind pk = (kind == 'z') ? KIND_4M : KIND_REAL;
+    if (int rc = make_plan(pk, side == 'A' ? rows : 1, side == 'B' ? rows : 1, cols, 1, num_slices, P)) return rc;
+    const int64_t stored_rows = (side == 'A') == (trans == 'N') ? rows : cols;
+    if (ldx < std::max<int64_t>(1, stored_rows)) return fail(-7, "ldx");
+    const bool sideA = side == 'A';
+    Operand op = sideA ? view_A(X, trans, rows, cols, ldx, 0, mode) : view_B(X, trans, rows, cols, ldx, 0, mode);
+    const size_t sl_bytes = sideA ? P.a_bytes : P.b_bytes;
+    const int64_t rows_out = (mode == SPLIT_A4M) ? 2 * rows : rows;
+    void *base = nullptr;
+    CUDA_TRY(cudaMallocAsync(&base, sl_bytes + al256(4 * (rows_out + 1)), st));
+    int8_t *sl = (int8_t *)base;
+    int32_t *ex = (int32_t *)(sl + sl_bytes);
+    int rc = launch_split(P, op, sideA, sl, ex, dev, st);
+    const int64_t kdepth = (mode == SPLIT_A4M || mode == SPLIT_B4M) ? P.Kp : cols;
+    if (!rc && rows_out > 0 && kdepth > 0) {
+        const int64_t total = (int64_t)num_slices * rows_out * kdepth;
+        k_unpack<<<grid1d(total, dev->sms), 256, 0, st>>>(sl, slices_out, rows_out, kdepth, num_slices,
+                                                        sideA ? kBM : P.BN, P.KB);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = fail(OZAKI_ERR_CUDA, "unpack: %s", cudaGetErrorString(e));
+        if (!rc && exps_out) {
+            e = cudaMemcpyAsync(exps_out, ex, 4 * rows_out, cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) rc = fail(OZAKI_ERR_CUDA, "copy exps: %s", cudaGetErrorString(e));
+        }
+    }
+    cudaFreeAsync(base, st);
+    if (kdepth_out) *kdepth_out = kdepth;
+    return rc;
+}
+
+int ozaki_debug_level_sums(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                           const double *A, int64_t lda, const double *B, int64_t ldb,
+                           int num_slices, int32_t *S_out) {
+    const double al[2] = {1.0, 0.0}, be[2] = {0.0, 0.0};
+    Call c = make_call(KIND_REAL, transa, transb, m, n, k, al, A, lda, 0, B, ldb, 0, be, nullptr,
+                       std::max<int64_t>(1, m), 0, 1, num_slices, false);
+    c.S_out = S_out;
+    if (!S_out) return fail(-11, "S_out");
+    return run(c);
+}
+
+}  // extern "C"

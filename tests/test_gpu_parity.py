@@ -1,0 +1,284 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit for bit.
+
+Bars: exponents, INT8 slices and INT32 level sums bit-exact;
+final FP64 C bit-exact (the GPU executes the oracle's FP64 operation sequence,
+readings R6/R7), NaN where the oracle has NaN.
+"""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2603_29975_b200 as oz  # noqa: E402
+
+
+def dev(x):
+    """numpy (Fortran-order) -> column-major CUDA tensor."""
+    t = torch.from_numpy(np.asfortranarray(x)).to("cuda")
+    return oz.colmajor(t)
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def same(a, b):
+    """Bitwise-equal up to the sign of zero; NaN matches NaN."""
+    a = np.asarray(a)
+    b = np.asarray(b)
+    if np.iscomplexobj(a) or np.iscomplexobj(b):
+        return same(np.real(a), np.real(b)) and same(np.imag(a), np.imag(b))
+    if a.shape != b.shape:
+        return False
+    na, nb = np.isnan(a), np.isnan(b)
+    return bool((na == nb).all() and ((a == b) | na).all())
+
+
+# ------------------------------------------------------------------ K1 split
+def _oracle_rows(orc, X, side, trans, kind):
+    """Rows the oracle splits for this operand (op(A) rows / op(B) columns)."""
+    opX = orc.op(X, trans)
+    rows = opX if side == "A" else opX.T
+    return np.ascontiguousarray(rows)
+
+
+@pytest.mark.parametrize("side", ["A", "B"])
+@pytest.mark.parametrize("trans", ["N", "T"])
+@pytest.mark.parametrize("s", [1, 3, 7, 8, 9, 16])
+def test_split_real_bitexact(orc, side, trans, s):
+    g = synth.rng(s)
+    for fam, shape in (("spread", (37, 53)), ("uniform", (130, 70)), ("integer", (5, 300))):
+        X = synth.make(fam, *shape, seed=int(g.integers(1 << 30)))
+        if fam == "spread":
+            X[3, 5] = 2.0 ** -1074 * 7      # subnormal
+            X[4, :] = 0.0                   # zero row / column
+            X[0, 0] = 1.5e300
+        sl, ex = oz.debug_split(side, "d", trans, dev(X), s)
+        rows = _oracle_rows(orc, X, side, trans, "d")
+        D, e, nf = orc.split_rows(rows, s)
+        assert (host(ex) == e).all()
+        assert (host(sl) == D).all()
+
+
+@pytest.mark.parametrize("side", ["A", "B"])
+@pytest.mark.parametrize("trans", ["N", "T", "C"])
+@pytest.mark.parametrize("s", [2, 7, 11])
+def test_split_complex_bitexact(orc, side, trans, s):
+    X = synth.kkr(45, 39, seed=s, gamma=3.0)
+    opX = orc.op(X, trans)
+    rows = opX if side == "A" else opX.T       # complex rows x k
+    k = rows.shape[1]
+    # 3M operands
+    for kind, val in (("r", rows.real), ("i", rows.imag), ("s", rows.real + rows.imag)):
+        sl, ex = oz.debug_split(side, kind, trans, dev(X), s)
+        D, e, nf = orc.split_rows(np.ascontiguousarray(val), s)
+        assert (host(ex) == e).all(), kind
+        assert (host(sl) == D).all(), kind
+    # 4M embedding: A rows 2r = [Re | -Im], 2r+1 = [Im | Re]; B columns [Re ; Im];
+    # halves start at 0 and kh = round_up(k, 32)
+    sl, ex = oz.debug_split(side, "z", trans, dev(X), s)
+    sl, ex = host(sl), host(ex)
+    kh = (k + 31) // 32 * 32
+    if side == "A":
+        D, e, _ = orc.split_rows(np.ascontiguousarray(np.vstack([np.hstack([rows.real, -rows.imag]),
+                                                                 np.hstack([rows.imag, rows.real])])), s)
+        m = rows.shape[0]
+        for r in range(m):
+            for half, src in ((0, D[:, r, :]), (1, D[:, m + r, :])):
+                got = sl[:, 2 * r + half, :]
+                assert (got[:, :k] == src[:, :k]).all()
+                assert (got[:, kh:kh + k] == src[:, k:]).all()
+                assert not got[:, k:kh].any() and not got[:, kh + k:].any()
+            assert ex[2 * r] == e[r] == ex[2 * r + 1]
+    else:
+        D, e, _ = orc.split_rows(np.ascontiguousarray(np.hstack([rows.real, rows.imag])), s)
+        assert (ex == e).all()
+        assert (sl[:, :, :k] == D[:, :, :k]).all()
+        assert (sl[:, :, kh:kh + k] == D[:, :, k:]).all()
+        assert not sl[:, :, k:kh].any() and not sl[:, :, kh + k:].any()
+
+
+# ------------------------------------------------------------ level sums
+@pytest.mark.parametrize("s", [1, 2, 5, 8, 9, 13])
+@pytest.mark.parametrize("shape", [(64, 64, 64), (200, 150, 97), (129, 65, 33)])
+def test_level_sums_bitexact(orc, s, shape):
+    m, n, k = shape
+    A = synth.spread(m, k, seed=s, phi=1.5)
+    B = synth.uniform(k, n, seed=100 + s)
+    S = host(oz.debug_level_sums("N", "N", dev(A), dev(B), s))
+    DA, _, _ = orc.split_rows(np.ascontiguousarray(A), s)
+    DB, _, _ = orc.split_rows(np.ascontiguousarray(B.T), s)
+    So = orc.level_sums(DA, DB, s)
+    assert np.abs(So).max() < 2 ** 31
+    assert (S.astype(np.int64) == So).all()
+
+
+# ---------------------------------------------------------------- DGEMM
+CASES_D = [
+    # (m, n, k, transa, transb, alpha, beta, family)
+    (64, 64, 64, "N", "N", 1.0, 0.0, "uniform"),
+    (37, 53, 71, "T", "N", -1.5, 0.25, "spread"),
+    (300, 200, 150, "N", "T", 1.0, 1.0, "uniform"),
+    (129, 65, 33, "T", "T", 0.5, -2.0, "spread"),
+    (1, 1, 1, "N", "N", 1.0, 0.0, "uniform"),
+    (256, 128, 1, "N", "N", 3.0, 0.0, "integer"),
+    (17, 300, 260, "C", "C", 1.0, 0.5, "uniform"),
+]
+
+
+@pytest.mark.parametrize("case", CASES_D)
+@pytest.mark.parametrize("s", [1, 3, 4, 6, 7, 8, 9, 16])
+def test_dgemm_bitexact(orc, case, s):
+    m, n, k, ta, tb, al, be, fam = case
+    seed = hash((m, n, k, ta, tb, s)) % (1 << 30)
+    A = synth.make(fam, *((m, k) if ta == "N" else (k, m)), seed=seed)
+    B = synth.make(fam, *((k, n) if tb == "N" else (n, k)), seed=seed + 1)
+    C = synth.uniform(m, n, seed=seed + 2)
+    want = orc.dgemm(ta, tb, al, A, B, be, C, s)
+    Cd = dev(C)
+    oz.dgemm(ta, tb, al, dev(A), dev(B), be, Cd, s)
+    assert same(host(Cd), want)
+
+
+def test_dgemm_leading_dims_and_views(orc):
+    """lda/ldb/ldc larger than the rows: operate on sub-views of bigger buffers."""
+    s = 6
+    bigA = synth.uniform(90, 70, seed=1)
+    bigB = synth.uniform(80, 60, seed=2)
+    bigC = synth.uniform(100, 50, seed=3)
+    A, B, C = bigA[5:55, 3:43], bigB[7:47, 2:32], bigC[10:60, 4:34]
+    want = orc.dgemm("N", "N", 1.25, A, B, 0.5, C, s)
+    tA, tB, tC = dev(bigA), dev(bigB), dev(bigC)
+    vC = tC[10:60, 4:34]
+    oz.dgemm("N", "N", 1.25, tA[5:55, 3:43], tB[7:47, 2:32], 0.5, vC, s)
+    assert same(host(vC), want)
+    out = host(tC)
+    untouched = np.ones_like(out, bool)
+    untouched[10:60, 4:34] = False
+    assert (out[untouched] == bigC[untouched]).all()
+
+
+def test_dgemm_edge_cases(orc):
+    s = 5
+    A = synth.spread(40, 30, seed=4, phi=3.0)
+    B = synth.spread(30, 20, seed=5, phi=3.0)
+    # non-finite rows/cols -> NaN rows/cols (R10)
+    A2, B2 = A.copy(), B.copy()
+    A2[3, 7] = np.inf
+    B2[11, 4] = np.nan
+    want = orc.dgemm("N", "N", 1.0, A2, B2, 0.0, None, s)
+    C = torch.zeros((40, 20), dtype=torch.float64, device="cuda").t().contiguous().t()
+    oz.reset_stats()
+    oz.dgemm("N", "N", 1.0, dev(A2), dev(B2), 0.0, C, s)
+    got = host(C)
+    assert same(got, want)
+    assert np.isnan(got[3]).all() and np.isnan(got[:, 4]).all()
+    assert oz.get_stats()["nonfinite_rows"] == 2
+    # beta == 0: C is never read (NaN in C does not leak)
+    Cn = dev(np.full((40, 20), np.nan))
+    oz.dgemm("N", "N", 1.0, dev(A), dev(B), 0.0, Cn, s)
+    assert same(host(Cn), orc.dgemm("N", "N", 1.0, A, B, 0.0, None, s))
+    # alpha == 0 quick return: C = beta C, and beta == 0 gives zeros without reading
+    C0 = synth.uniform(40, 20, seed=6)
+    Cd = dev(C0)
+    oz.dgemm("N", "N", 0.0, dev(A), dev(B), -3.0, Cd, s)
+    assert same(host(Cd), orc.dgemm("N", "N", 0.0, A, B, -3.0, C0, s))
+    Cd = dev(np.full((40, 20), np.nan))
+    oz.dgemm("N", "N", 0.0, dev(A), dev(B), 0.0, Cd, s)
+    assert (host(Cd) == 0).all()
+    # k == 0
+    Cd = dev(C0)
+    oz.dgemm("N", "N", 1.0, dev(np.zeros((40, 0))), dev(np.zeros((0, 20))), 2.0, Cd, s)
+    assert same(host(Cd), 2.0 * C0)
+    # extreme exponents: huge, tiny, subnormal outputs
+    A3 = A * 1e300
+    B3 = B * 1e-300
+    A4 = A * 2.0 ** -540
+    B4 = B * 2.0 ** -540
+    for a, b in ((A3, B3), (A4, B4), (A * 2.0 ** 500, B * 2.0 ** 500)):
+        want = orc.dgemm("N", "N", 1.0, a, b, 0.0, None, s)
+        Cd = dev(np.zeros((40, 20)))
+        oz.dgemm("N", "N", 1.0, dev(a), dev(b), 0.0, Cd, s)
+        assert same(host(Cd), want)
+
+
+def test_dgemm_rejects_kchunk_overflow():
+    A = dev(np.zeros((8, 20000)))
+    B = dev(np.zeros((20000, 8)))
+    C = dev(np.zeros((8, 8)))
+    with pytest.raises(oz.OzakiError) as ei:
+        oz.dgemm("N", "N", 1.0, A, B, 0.0, C, 8)
+    assert ei.value.code == 4
+
+
+# ---------------------------------------------------------------- ZGEMM
+CASES_Z = [
+    (48, 40, 36, "N", "N", 1.0, 0.0),
+    (70, 33, 65, "C", "N", 0.5 - 1.25j, -0.75 + 0.5j),
+    (129, 64, 100, "N", "C", 1j, 1.0),
+    (20, 150, 40, "T", "T", -1.0, 0.0),
+]
+
+
+@pytest.mark.parametrize("case", CASES_Z)
+@pytest.mark.parametrize("s", [2, 4, 7, 8, 10])
+@pytest.mark.parametrize("method", ["4m", "3m"])
+def test_zgemm_bitexact(orc, case, s, method):
+    m, n, k, ta, tb, al, be = case
+    seed = hash((m, n, k, ta, tb, s, method)) % (1 << 30)
+    A = synth.kkr(*((m, k) if ta == "N" else (k, m)), seed=seed, gamma=1.0)
+    B = synth.spread(*((k, n) if tb == "N" else (n, k)), seed=seed + 1, phi=1.0, complex_=True)
+    C = synth.uniform(m, n, seed=seed + 2, complex_=True)
+    want = orc.zgemm(ta, tb, al, A, B, be, C, s, method)
+    Cd = dev(C)
+    fn = oz.zgemm if method == "4m" else oz.zgemm3m
+    fn(ta, tb, al, dev(A), dev(B), be, Cd, s)
+    assert same(host(Cd), want)
+
+
+# ------------------------------------------------------------ batched
+@pytest.mark.parametrize("s", [3, 8])
+def test_batched_bitexact(orc, s):
+    batch, m, n, k = 5, 70, 90, 50
+    As = [synth.uniform(m, k, seed=10 + i) for i in range(batch)]
+    Bs = [synth.spread(k, n, seed=20 + i, phi=1.0) for i in range(batch)]
+    Cs = [synth.uniform(m, n, seed=30 + i) for i in range(batch)]
+    tA = torch.stack([dev(a) for a in As]).transpose(1, 2).contiguous().transpose(1, 2)
+    tB = torch.stack([dev(b) for b in Bs]).transpose(1, 2).contiguous().transpose(1, 2)
+    tC = torch.stack([dev(c) for c in Cs]).transpose(1, 2).contiguous().transpose(1, 2)
+    oz.dgemm_strided_batched("N", "N", 2.0, tA, tB, -1.0, tC, s)
+    got = host(tC)
+    for i in range(batch):
+        assert same(got[i], orc.dgemm("N", "N", 2.0, As[i], Bs[i], -1.0, Cs[i], s))
+    zA = [synth.kkr(m, k, seed=40 + i) for i in range(batch)]
+    zB = [synth.kkr(k, n, seed=50 + i) for i in range(batch)]
+    for method, fn in (("4m", oz.zgemm_strided_batched), ("3m", oz.zgemm3m_strided_batched)):
+        tA = torch.stack([dev(a) for a in zA]).transpose(1, 2).contiguous().transpose(1, 2)
+        tB = torch.stack([dev(b) for b in zB]).transpose(1, 2).contiguous().transpose(1, 2)
+        tC = torch.zeros((batch, n, m), dtype=torch.complex128, device="cuda").transpose(1, 2)
+        fn("N", "N", 1.0, tA, tB, 0.0, tC, s)
+        got = host(tC)
+        for i in range(batch):
+            assert same(got[i], orc.zgemm("N", "N", 1.0, zA[i], zB[i], 0.0, None, s, method))
+
+
+def test_stats_closed_forms():
+    oz.reset_stats()
+    A = dev(synth.uniform(32, 32, seed=1))
+    C = dev(np.zeros((32, 32)))
+    oz.dgemm("N", "N", 1.0, A, A, 0.0, C, 5)
+    Z = dev(synth.uniform(16, 16, seed=2, complex_=True))
+    Zc = dev(np.zeros((16, 16), np.complex128))
+    oz.zgemm("N", "N", 1.0, Z, Z, 0.0, Zc, 5)
+    oz.zgemm3m("N", "N", 1.0, Z, Z, 0.0, Zc, 5)
+    st = oz.get_stats()
+    # s(s+1)/2 per real product, x4 (4M), x3 (3M)
+    assert st["int8_gemm_equiv"] == 15 + 4 * 15 + 3 * 15
+    assert st["dgemm_calls"] == 1 and st["zgemm_calls"] == 1 and st["zgemm3m_calls"] == 1
+    assert st["kernel_launches"] == 5 + 5 + (3 * 5 + 1)
