@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""bench.py -- FP64-equivalent TFLOP/s of the INT8 Ozaki-I ZGEMM/DGEMM path on B200.
+
+Metric (BASELINE.json): "FP64-equiv TFLOP/s (ZGEMM/DGEMM) vs slice count; INT8
+pipe util; max rel err".  Default workload = BASELINE configs[1]: LSMS-shaped
+KKR blocks, ZGEMM 512 x 512 x 512 complex with wide exponent spread
+(synth.kkr gamma=3), 4M path, s = 7 (the paper's 55-bit mode),
+one step = one strided-batched call over a batch of 30 energy-point blocks
+(the ~30-point contour quadrature) per GPU.  Multi-GPU: every
+rank owns its own 30 blocks (weak scaling, no data-path collective).
+
+FP64-equivalent flops: 8 m n k per complex product (2 m n k real).
+`--impl reference` times the CPU oracle (oracle/) on a bounded sample of the
+same workload on the host cores (the reference arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+BURST_FALLBACK_BF16 = 1590.0    # B200_PROFILING.md fallback (TFLOP/s) if MEASURED_PEAKS.json absent
+INT8_OVER_BF16 = 4.5 / 2.25     # nominal dense ratio (B200_PROFILING.md / datasheet)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--slices", type=int, default=7)
+    ap.add_argument("--method", default="4m", choices=["4m", "3m"])
+    ap.add_argument("--batch", type=int, default=30)
+    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--gamma", type=float, default=3.0)
+    ap.add_argument("--no-extras", action="store_true", help="skip sweep / e2e / cpu baseline")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+    except Exception:  # noqa: BLE001
+        return BURST_FALLBACK_BF16, 1400.0, "fallback"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.index = index
+        self.period = period_s
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # noqa: BLE001
+            self.ok = False
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def start(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self._t:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0,
+                    "source": "nvml unavailable" if not self.ok else "no samples"}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and v != "gpu_idle"]
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples), "source": "nvml 5 ms"}
+
+
+# ------------------------------------------------------------ workload
+def make_inputs(batch, n, gamma, seed0):
+    """Batch of KKR-like complex blocks (column-major per entry), numpy."""
+    A = np.empty((batch, n, n), dtype=np.complex128, order="C")
+    B = np.empty((batch, n, n), dtype=np.complex128, order="C")
+    for i in range(batch):
+        A[i] = synth.kkr(n, n, seed=seed0 + 2 * i, gamma=gamma)
+        B[i] = synth.kkr(n, n, seed=seed0 + 2 * i + 1, gamma=gamma)
+    return A, B
+
+
+def to_dev_batched(torch, X, device):
+    # (batch, n, n) numpy with Fortran entries -> column-major per entry on device
+    t = torch.from_numpy(np.ascontiguousarray(np.transpose(X, (0, 2, 1))))  # row-major of X^T
+    return t.to(device).transpose(1, 2)
+
+
+def fp64_equiv_flops(batch, n, cplx=True):
+    return batch * (8 if cplx else 2) * n ** 3
+
+
+def int8_ops(batch, n, s, method):
+    mult = 4 if method == "4m" else 3
+    return 2 * mult * (s * (s + 1) // 2) * n ** 3 * batch
+
+
+# ------------------------------------------------------------------ main
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2603_29975_b200 as oz
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+
+    n, batch, s = args.n, args.batch, args.slices
+    fn = oz.zgemm_strided_batched if args.method == "4m" else oz.zgemm3m_strided_batched
+    A_h, B_h = make_inputs(batch, n, args.gamma, seed0=1000 * (rank + 1))
+    A = to_dev_batched(torch, A_h, device)
+    B = to_dev_batched(torch, B_h, device)
+    C = torch.zeros((batch, n, n), dtype=torch.complex128, device=device).transpose(1, 2)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        fn("N", "N", 1.0, A, B, 0.0, C, s)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    st0 = oz.get_stats()
+    oz.profile_enable(True)
+    oz.profile_read()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks.stop()
+    if world > 1:
+        dist.barrier()
+    prof = oz.profile_read()
+    oz.profile_enable(False)
+    st1 = oz.get_stats()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    flops_all = fp64_equiv_flops(batch, n) * world
+    value = flops_all / (ms_step * 1e-3) / 1e12
+
+    bf16_burst, bf16_sus, peak_src = peaks()
+    peak_int8 = bf16_burst * INT8_OVER_BF16
+    gemm = prof["k2_gemm"]
+    gemm_ms = gemm["ms"] / max(1, gemm["launches"])
+    alg_ops = int8_ops(batch, n, s, args.method) / (1 if args.method == "4m" else 3)   # per launch
+    achieved = alg_ops / (gemm_ms * 1e-3) / 1e12
+    step_phase_ms = {k: v["ms"] / args.steps for k, v in prof.items()}
+    launches = int(st1["kernel_launches"] - st0["kernel_launches"])
+
+    out = {
+        "metric": "FP64-equiv TFLOP/s (ZGEMM/DGEMM) vs slice count; INT8 pipe util; max rel err",
+        "value": round(value, 3),
+        "unit": "TFLOP/s (FP64-equivalent, 8mnk per ZGEMM)",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(3, args.warmup),
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64 in/out; int8 x int8 -> int32 tensor-core products; f64 epilogue",
+        "data": "synthetic (synth.kkr: graded-channel KKR blocks, seeded)",
+        "config": {
+            "workload": (f"BASELINE configs[1]: ZGEMM {n}x{n}x{n} KKR blocks (gamma={args.gamma}), "
+                         f"{args.method.upper()}, s={s} ({8 * s - 1}-bit mode), strided-batched "
+                         f"over {batch} energy points per GPU"),
+            "slices": s, "method": args.method, "m": n, "n": n, "k": n,
+            "batch_per_gpu": batch, "global_batch": batch * world,
+            "parallelism": f"batch-sharded x{world} (no collective)",
+            "l2": "inputs exceed L2 (%.0f MB per GPU > 126 MB)" % (batch * 3 * n * n * 16 / 1e6),
+        },
+        "roofline": {
+            "bound": "tensor",
+            "kernel": "k_gemm (K2+K3: tcgen05 kind::i8 slice GEMM + FP64 epilogue)",
+            "achieved": round(achieved, 2),
+            "peak": round(peak_int8, 1),
+            "unit": "TOPS (INT8 dense)",
+            "frac": round(achieved / peak_int8, 4),
+            "peak_source": f"{peak_src} bf16 burst {bf16_burst} TF/s x nominal int8/bf16 ratio 2",
+            "algorithmic_ops_per_launch": alg_ops,
+            "traffic": None,
+            "kernel_ms_per_launch": round(gemm_ms, 5),
+            "kernel_share_of_step": round(gemm["ms"] / max(1e-9, ms), 4),
+        },
+        "phase_ms_per_step": {k: round(v, 5) for k, v in step_phase_ms.items()},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    # e2e through the public API with HOST buffers (pinned), H2D + compute + D2H per step
+    if not args.no_extras:
+        out["e2e"] = e2e_leg(torch, oz, fn, A_h, B_h, batch, n, s, device, args, world)
+        out["accuracy"] = accuracy_leg(torch, oz, A_h, B_h, C, s, args.method)
+        out["sweep"] = sweep_leg(torch, oz, A, B, C, batch, n)
+    if rank == 0 and not args.no_extras and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(A_h, B_h, s, args.method, n)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_leg(torch, oz, fn, A_h, B_h, batch, n, s, device, args, world):
+    import torch.distributed as dist
+    stream = torch.cuda.current_stream()
+    Ap = torch.from_numpy(np.ascontiguousarray(np.transpose(A_h, (0, 2, 1)))).pin_memory()
+    Bp = torch.from_numpy(np.ascontiguousarray(np.transpose(B_h, (0, 2, 1)))).pin_memory()
+    Cp = torch.empty((batch, n, n), dtype=torch.complex128).pin_memory()
+    Ad = torch.empty_like(Ap, device=device)
+    Bd = torch.empty_like(Bp, device=device)
+    Cd = torch.empty((batch, n, n), dtype=torch.complex128, device=device)
+
+    def step():
+        Ad.copy_(Ap, non_blocking=True)
+        Bd.copy_(Bp, non_blocking=True)
+        fn("N", "N", 1.0, Ad.transpose(1, 2), Bd.transpose(1, 2), 0.0, Cd.transpose(1, 2), s)
+        Cp.copy_(Cd, non_blocking=True)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    steps = max(3, min(args.steps, 10))
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    val = fp64_equiv_flops(batch, n) * world / (ms * 1e-3) / 1e12
+    return {"value": round(val, 3), "unit": "TFLOP/s (FP64-equivalent)", "ms_per_step": round(ms, 3),
+            "h2d_bytes_per_step": int(Ap.numel() * 16 + Bp.numel() * 16),
+            "d2h_bytes_per_step": int(Cp.numel() * 16),
+            "path": "pinned host -> device copy, ozaki_zgemm_strided_batched, device -> pinned host"}
+
+
+def accuracy_leg(torch, oz, A_h, B_h, C, s, method):
+    """Entry 0: parity vs the oracle and error vs the TRUE product on a sample."""
+    import oracle
+    n = A_h.shape[1]
+    rows = np.unique(np.r_[0, 1, 127, 128, 255, n - 1, np.arange(3, n, 37)])
+    cols = np.unique(np.r_[0, 63, 64, 127, n - 1, np.arange(5, n, 41)])
+    A0 = np.asfortranarray(A_h[0])
+    B0 = np.asfortranarray(B_h[0])
+    got = C[0].cpu().numpy()[np.ix_(rows, cols)]
+    want = oracle.zgemm("N", "N", 1.0, A0[rows], B0[:, cols], 0.0, None, s, method)
+    truth = oracle.exact_zproduct(A0[rows], B0[:, cols])
+    absab = np.abs(A0[rows]) @ np.abs(B0[:, cols])
+    nz = truth != 0
+    bitexact = bool((got.real == want.real).all() and (got.imag == want.imag).all())
+    return {"sample": f"entry 0, {len(rows)}x{len(cols)} entries incl. tile edges",
+            "bitexact_vs_oracle": bitexact,
+            "max_rel_err_vs_true_fp64": float(np.max(np.abs(got - truth)[nz] / np.abs(truth[nz]))),
+            "max_err_over_absAB": float(np.max(np.abs(got - truth) / absab))}
+
+
+def sweep_leg(torch, oz, A, B, C, batch, n):
+    """FP64-eq TFLOP/s vs s for 4M and 3M on the same inputs (short timing)."""
+    res = {}
+    for method, fn in (("4m", oz.zgemm_strided_batched), ("3m", oz.zgemm3m_strided_batched)):
+        for s in (3, 4, 5, 6, 7, 8, 9):
+            for _ in range(2):
+                fn("N", "N", 1.0, A, B, 0.0, C, s)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            reps = 5
+            e0.record()
+            for _ in range(reps):
+                fn("N", "N", 1.0, A, B, 0.0, C, s)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            res[f"{method}_s{s}"] = round(fp64_equiv_flops(batch, n) / (ms * 1e-3) / 1e12, 2)
+    return res
+
+
+def cpu_baseline(A_h, B_h, s, method, n):
+    import oracle
+    cores = oracle.num_threads()
+    A0 = np.asfortranarray(A_h[0])
+    B0 = np.asfortranarray(B_h[0])
+    rows = n // 4   # bounded sample: a 128-row slab of one 512^3 block
+    t0 = time.perf_counter()
+    oracle.zgemm("N", "N", 1.0, A0[:rows], B0, 0.0, None, s, method)
+    dt = time.perf_counter() - t0
+    flops = 8 * rows * n * n
+    return {"value": round(flops / dt / 1e12, 6), "unit": "TFLOP/s (FP64-equivalent)", "cores": cores,
+            "kind": "oracle",
+            "sample": f"{rows} rows x {n} cols of one {n}^3 ZGEMM ({method}, s={s}), exact-integer oracle",
+            "seconds": round(dt, 3)}
+
+
+def run_reference(args):
+    """Reference arm of this tier: the CPU oracle, as it stands, on host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    n, s = args.n, args.slices
+    A_h, B_h = make_inputs(1, n, args.gamma, seed0=1000)
+    A0 = np.asfortranarray(A_h[0])
+    B0 = np.asfortranarray(B_h[0])
+    rows = max(8, n // 16)     # bounded sample per step: a 32-row slab of one block
+    for _ in range(max(0, min(args.warmup, 1))):
+        oracle.zgemm("N", "N", 1.0, A0[:rows], B0, 0.0, None, s, args.method)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.zgemm("N", "N", 1.0, A0[:rows], B0, 0.0, None, s, args.method)
+    dt = (time.perf_counter() - t0) / args.steps
+    val = 8 * rows * n * n / dt / 1e12
+    cores = oracle.num_threads()
+    line = {
+        "impl": "reference",
+        "metric": "FP64-equiv TFLOP/s (ZGEMM/DGEMM) vs slice count; INT8 pipe util; max rel err",
+        "value": round(val, 6),
+        "unit": "TFLOP/s (FP64-equivalent, 8mnk per ZGEMM)",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64 / exact int64 (CPU oracle)",
+        "data": "synthetic (synth.kkr, seeded)",
+        "config": {"workload": (f"BASELINE configs[1]: ZGEMM {n}^3 KKR block (gamma={args.gamma}), "
+                                f"{args.method.upper()}, s={s}; each step a {rows}x{n} row slab"),
+                   "slices": s, "method": args.method},
+        "cpu_baseline": {"value": round(val, 6), "unit": "TFLOP/s (FP64-equivalent)", "cores": cores,
+                         "kind": "oracle", "sample": f"{rows} rows of one {n}^3 ZGEMM per step"},
+        "e2e": {"value": round(val, 6), "unit": "TFLOP/s (FP64-equivalent)", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -82,7 +82,7 @@ int ozaki_dgemm(char transa, char transb, int64_t m, int64_t n, int64_t k,
                 const double *B, int64_t ldb,
                 double beta, double *C, int64_t ldc, int num_slices);
 
-/* --- complex, 4M real embedding [[Ar,-Ai],[Ai,Ar]] [Br;Bi] (R9) -------------
+/* --- complex, 4M real embedding [Ar|Ai] [[Br,Bi],[-Bi,Br]] (R9, N side) -----
  * alpha, beta: HOST pointers to {re, im}.  Same parameter numbering.        */
 int ozaki_zgemm(char transa, char transb, int64_t m, int64_t n, int64_t k,
                 const double *alpha, const double *A, int64_t lda,
@@ -136,6 +136,19 @@ const char *ozaki_last_error(void);
 /* Library version string.                                                 */
 const char *ozaki_version(void);
 
+/* --- phase profiler (tracing subsystem) ---------------------
+ * When enabled, every kernel the library launches is bracketed by CUDA
+ * events on its stream; ozaki_profile_read synchronises on the recorded
+ * events, returns per-phase device time and launch counts accumulated since
+ * the last read, and clears them.  Phases: 0 = K1 exponent scan, 1 = K1
+ * slicing, 2 = K2/K3 slice GEMM + epilogue, 3 = other (3M combine, scale). */
+typedef struct ozaki_profile {
+    double ms[4];
+    uint64_t launches[4];
+} ozaki_profile_t;
+int ozaki_profile_enable(int on);
+int ozaki_profile_read(ozaki_profile_t *out);
+
 /* --- test-only debug entry points (same kernels, extra outputs) -----------
  * ozaki_debug_split: run the split kernels on one operand.
  *   side 'A': rows of op(X) where op(X) = X ('N') or X^T ('T'/'C');
@@ -143,7 +156,7 @@ const char *ozaki_version(void);
  *   side 'B': columns of op(X) where op(X) is cols x rows ... i.e. the
  *             "rows" of the split are the columns of op(B): X is cols x rows
  *             if trans == 'N' else rows x cols.
- *   kind 'd' (real), 'z' (4M embedding; rows_out = 2*rows for side A),
+ *   kind 'd' (real), 'z' (4M embedding; rows_out = 2*rows for side B),
  *        'r','i','s' (3M operands Re, Im, fl(Re+Im) of complex X).
  *   Outputs (DEVICE pointers): slices_out[t][r][l] int8 (t = 0..s-1 most
  *   significant first, r over output rows, l over the output K depth
@@ -160,6 +173,13 @@ int ozaki_debug_split(char side, char kind, char trans, int64_t rows, int64_t co
 int ozaki_debug_level_sums(char transa, char transb, int64_t m, int64_t n, int64_t k,
                            const double *A, int64_t lda, const double *B, int64_t ldb,
                            int num_slices, int32_t *S_out);
+
+/* ozaki_debug_timing: enable (1) / disable (0) per-role clock64 timers in the
+ * GEMM kernel; when `out` is non-null, synchronises, copies up to `nslots`
+ * counters (summed over CTAs: producer wait, MMA wait-operands, MMA
+ * wait-TMEM-drain, MMA lifetime, epilogue wait, drain, store, CTA lifetime)
+ * and clears them.  Returns the number of counters.                       */
+int ozaki_debug_timing(int enable, uint64_t *out, int nslots);
 
 #ifdef __cplusplus
 }

@@ -218,21 +218,25 @@ def dgemm(transa, transb, alpha, A, B, beta, C, s: int) -> np.ndarray:
 
 
 def emb_4m(Aop, Bop):
-    """Real embedding used by 4M (reading R9): [[Ar,-Ai],[Ai,Ar]] @ [Br;Bi]."""
+    """Real embedding used by 4M (reading R9, N-side form):
+    C = A B with A = Ar + i Ai, B = Br + i Bi is
+        [Cr | Ci] = [Ar | Ai] @ [[Br, Bi], [-Bi, Br]]
+    i.e. op(A)' = [Ar, Ai] (m x 2k) and op(B)' (2k x 2n); the -Bi block is
+    split from the negated FP64 values.  Returns (A2, B2)."""
     Ar, Ai = Aop.real, Aop.imag
     Br, Bi = Bop.real, Bop.imag
-    A2 = np.block([[Ar, -Ai], [Ai, Ar]])
-    B2 = np.vstack([Br, Bi])
+    A2 = np.hstack([Ar, Ai])
+    B2 = np.block([[Br, Bi], [-Bi, Br]])
     return A2, B2
 
 
 def zproduct(Aop, Bop, s: int, method: str = "4m"):
     """Emulated complex product P = Pr + i Pi (O2..O6, 4M or 3M)."""
-    m = Aop.shape[0]
+    n = Bop.shape[1]
     if method == "4m":
         A2, B2 = emb_4m(Aop, Bop)
         P2 = emulated_product(A2, B2, s)
-        return P2[:m].copy(), P2[m:].copy()
+        return P2[:, :n].copy(), P2[:, n:].copy()
     if method == "3m":
         Ar, Ai = np.ascontiguousarray(Aop.real), np.ascontiguousarray(Aop.imag)
         Br, Bi = np.ascontiguousarray(Bop.real), np.ascontiguousarray(Bop.imag)
@@ -283,8 +287,8 @@ def exact_zproduct(A_op, B_op) -> np.ndarray:
     """TRUE complex product, re and im each rounded once."""
     A2, B2 = emb_4m(A_op, B_op)
     T2 = exact_product(A2, B2)
-    m = A_op.shape[0]
-    return _cplx(T2[:m], T2[m:])
+    n = B_op.shape[1]
+    return _cplx(T2[:, :n], T2[:, n:])
 
 
 def exact_dot(a, b) -> float:

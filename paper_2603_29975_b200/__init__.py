@@ -20,7 +20,7 @@ __all__ = [
     "OzakiError", "lib", "dgemm", "zgemm", "zgemm3m", "dgemm_strided_batched",
     "zgemm_strided_batched", "zgemm3m_strided_batched", "set_stream", "get_stats",
     "reset_stats", "workspace_size", "debug_split", "debug_level_sums", "colmajor",
-    "version", "pairs", "LIB_PATH",
+    "version", "pairs", "LIB_PATH", "profile_enable", "profile_read",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -32,6 +32,13 @@ class OzakiError(RuntimeError):
     def __init__(self, code: int, where: str, msg: str):
         super().__init__(f"{where}: code {code}: {msg}")
         self.code = code
+
+
+class Profile(ctypes.Structure):
+    _fields_ = [("ms", ctypes.c_double * 4), ("launches", ctypes.c_uint64 * 4)]
+
+
+PHASES = ("k1_exponent", "k1_slice", "k2_gemm", "other")
 
 
 class Stats(ctypes.Structure):
@@ -78,10 +85,16 @@ def lib():
     L.ozaki_workspace_size.restype = i64
     L.ozaki_last_error.restype = ctypes.c_char_p
     L.ozaki_version.restype = ctypes.c_char_p
+    L.ozaki_profile_enable.argtypes = [i32]
+    L.ozaki_profile_enable.restype = i32
+    L.ozaki_profile_read.argtypes = [ctypes.POINTER(Profile)]
+    L.ozaki_profile_read.restype = i32
     L.ozaki_debug_split.argtypes = [c, c, c, i64, i64, p, i64, i32, p, p, ctypes.POINTER(i64)]
     L.ozaki_debug_split.restype = i32
     L.ozaki_debug_level_sums.argtypes = [c, c, i64, i64, i64, p, i64, p, i64, i32, p]
     L.ozaki_debug_level_sums.restype = i32
+    L.ozaki_debug_timing.argtypes = [i32, ctypes.POINTER(ctypes.c_uint64), i32]
+    L.ozaki_debug_timing.restype = i32
     _lib = L
     return L
 
@@ -249,6 +262,18 @@ def reset_stats() -> None:
     lib().ozaki_reset_stats()
 
 
+def profile_enable(on: bool = True) -> None:
+    """Bracket every library kernel with CUDA events (per-phase device time)."""
+    lib().ozaki_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    """Per-phase device ms and launch counts since the last read (synchronises)."""
+    pr = Profile()
+    _check(lib().ozaki_profile_read(ctypes.byref(pr)), "ozaki_profile_read")
+    return {ph: {"ms": float(pr.ms[i]), "launches": int(pr.launches[i])} for i, ph in enumerate(PHASES)}
+
+
 def workspace_size(kind: str, m: int, n: int, k: int, batch: int, num_slices: int) -> int:
     return int(lib().ozaki_workspace_size(_ch(kind), m, n, k, batch, num_slices))
 
@@ -266,7 +291,7 @@ def debug_split(side, kind, trans, X, num_slices, stream=None):
         rows, cols = (X.shape[0], X.shape[1]) if t == "N" else (X.shape[1], X.shape[0])
     else:
         rows, cols = (X.shape[1], X.shape[0]) if t == "N" else (X.shape[0], X.shape[1])
-    rows_out = 2 * rows if (kind == "z" and side.upper() == "A") else rows
+    rows_out = 2 * rows if (kind == "z" and side.upper() == "B") else rows
     kdepth = cols if kind != "z" else 2 * ((cols + 31) // 32 * 32)
     s = int(num_slices)
     sl = torch.empty((s, rows_out, kdepth), dtype=torch.int8, device=X.device)
@@ -278,6 +303,17 @@ def debug_split(side, kind, trans, X, num_slices, stream=None):
     _check(rc, "ozaki_debug_split")
     assert kd.value == kdepth
     return sl, ex
+
+
+TIMER_NAMES = ("prod_wait_empty", "mma_wait_full", "mma_wait_slot", "mma_total", "epi_wait_pass",
+               "epi_drain", "epi_store", "cta_total")
+
+
+def debug_timing(enable: bool = True, read: bool = False) -> dict | None:
+    """Per-role clock64 timers inside the GEMM kernel (summed over CTAs)."""
+    buf = (ctypes.c_uint64 * len(TIMER_NAMES))()
+    lib().ozaki_debug_timing(1 if enable else 0, buf if read else None, len(TIMER_NAMES))
+    return {n: int(buf[i]) for i, n in enumerate(TIMER_NAMES)} if read else None
 
 
 def debug_level_sums(transa, transb, A, B, num_slices, stream=None):

@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libozaki.so")
 SOURCES = ["ozaki.cu"]
-HEADERS = ["gemm.cuh", "split.cuh", "numerics.cuh", "ptx.cuh"]
+HEADERS = ["gemm_lv2.cuh", "passplan.cuh", "gemm_lv.cuh", "gemm.cuh", "split.cuh", "numerics.cuh", "ptx.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

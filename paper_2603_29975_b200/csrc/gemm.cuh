@@ -50,6 +50,20 @@ struct GemmParams {
     int64_t ldc, strideC;   // in elements (complex elements for EPI_CPLX4M)
     double alpha_r, alpha_i, beta_r, beta_i;
     int32_t *S_out;         // EPI_LEVELS
+    unsigned long long *dbg;   // optional per-CTA role timers (ozaki_debug_timing), null = off
+};
+
+// Role timer slots (clock64 cycles summed per CTA) written when p.dbg != null.
+enum DbgSlot : int {
+    DBG_PROD_WAIT = 0,   // producer waiting for a free stage
+    DBG_MMA_WAIT_FULL,   // MMA thread waiting for operands
+    DBG_MMA_WAIT_SLOT,   // MMA thread waiting for the epilogue to drain TMEM
+    DBG_MMA_TOTAL,       // MMA thread lifetime
+    DBG_EPI_WAIT,        // epilogue waiting for a completed pass (warp 2, lane 0)
+    DBG_EPI_DRAIN,       // epilogue TMEM -> FP64 accumulate (warp 2)
+    DBG_EPI_STORE,       // epilogue ldexp + alpha/beta + store (warp 2)
+    DBG_TOTAL,           // CTA lifetime (warp 1)
+    DBG_NSLOT
 };
 
 __device__ __forceinline__ void decode_tile(const GemmParams &p, int64_t tile, int64_t &b,
@@ -206,36 +220,36 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm(const __grid_constant_
                         acc[j] = __fma_rn(__int2double_rn((int32_t)v[j]), sc, acc[j]);   // exact product
                 }
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
+                for (int j = 0; j < 16; j += 2) {
                     const int64_t gcol = tn * BN + col_local + j;
-                    const bool ok = row_ok && gcol < p.N;
                     const int32_t f = (gcol < p.N) ? p.fb[b * p.N + gcol] : 0;
-                    double P = (e == kNonFinite || f == kNonFinite)
-                                   ? __longlong_as_double(0x7ff8000000000000ll)
-                                   : ldexp_rn(acc[j], e + f - 14);
+                    const int32_t f1 = (gcol + 1 < p.N) ? p.fb[b * p.N + gcol + 1] : 0;
+                    const bool enan = (e == kNonFinite);
+                    const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+                    const double P0 = (enan || f == kNonFinite) ? qnan : ldexp_rn(acc[j], e + f - 14);
+                    const double P1 = (enan || f1 == kNonFinite) ? qnan : ldexp_rn(acc[j + 1], e + f1 - 14);
                     if constexpr (EPI == EPI_REAL) {
-                        if (ok) {
+                        if (row_ok && gcol < p.N) {
                             double *cp = p.C + b * p.strideC + grow + gcol * p.ldc;
-                            *cp = (p.beta_r == 0.0) ? __dmul_rn(p.alpha_r, P)
-                                                    : __fma_rn(p.alpha_r, P, __dmul_rn(p.beta_r, *cp));
+                            *cp = (p.beta_r == 0.0) ? __dmul_rn(p.alpha_r, P0)
+                                                    : __fma_rn(p.alpha_r, P0, __dmul_rn(p.beta_r, *cp));
                         }
-                    } else {   // EPI_CPLX4M: rows 2i (Re) and 2i+1 (Im) sit in adjacent lanes
-                        const int comp = (int)(grow & 1);
-                        double *cp = p.C + 2 * (b * p.strideC + (grow >> 1) + gcol * p.ldc);
-                        const bool rd = ok && !(p.beta_r == 0.0 && p.beta_i == 0.0);
-                        const double cown = rd ? cp[comp] : 0.0;
-                        const double coth = __shfl_xor_sync(0xffffffffu, cown, 1);
-                        const double Po = __shfl_xor_sync(0xffffffffu, P, 1);
-                        if (ok) {
-                            const double Pr = comp ? Po : P, Pi = comp ? P : Po;
-                            const double cr = comp ? coth : cown, ci = comp ? cown : coth;
+                        if (row_ok && gcol + 1 < p.N) {
+                            double *cp = p.C + b * p.strideC + grow + (gcol + 1) * p.ldc;
+                            *cp = (p.beta_r == 0.0) ? __dmul_rn(p.alpha_r, P1)
+                                                    : __fma_rn(p.alpha_r, P1, __dmul_rn(p.beta_r, *cp));
+                        }
+                    } else {   // EPI_CPLX4M, R9 N-side embedding: columns (2c, 2c+1) = (Re, Im)
+                        if (row_ok && gcol < p.N) {
+                            double2 *cp = reinterpret_cast<double2 *>(p.C) + b * p.strideC + grow + (gcol >> 1) * p.ldc;
                             double tr = 0.0, ti = 0.0;
-                            if (rd) {
-                                tr = __fma_rn(p.beta_r, cr, -__dmul_rn(p.beta_i, ci));
-                                ti = __fma_rn(p.beta_r, ci, __dmul_rn(p.beta_i, cr));
+                            if (!(p.beta_r == 0.0 && p.beta_i == 0.0)) {
+                                const double2 cv = *cp;
+                                tr = __fma_rn(p.beta_r, cv.x, -__dmul_rn(p.beta_i, cv.y));
+                                ti = __fma_rn(p.beta_r, cv.y, __dmul_rn(p.beta_i, cv.x));
                             }
-                            cp[comp] = comp ? __fma_rn(p.alpha_r, Pi, __fma_rn(p.alpha_i, Pr, ti))
-                                            : __fma_rn(p.alpha_r, Pr, __fma_rn(-p.alpha_i, Pi, tr));
+                            *cp = make_double2(__fma_rn(p.alpha_r, P0, __fma_rn(-p.alpha_i, P1, tr)),
+                                               __fma_rn(p.alpha_r, P1, __fma_rn(p.alpha_i, P0, ti)));
                         }
                     }
                 }

@@ -1,0 +1,271 @@
+// gemm_lv2.cuh -- K2 + K3 on CTA pairs (tcgen05 cta_group::2), the production
+// slice GEMM for s <= 12.
+//
+// Same method and pass structure as gemm_lv.cuh (§2.2; readings
+// R1, R6, R7; passes of <= 4 levels in 4 TMEM slots).  The difference is the
+// MMA shape: a cluster of two CTAs on one TPC issues M=256 x N=128 x K=32
+// kind::i8 MMAs (leader CTA issues).  Each CTA stages only its own 128 rows of
+// A and HALF (64 columns) of B, so the shared-memory operand traffic per SM
+// drops from 8 KB to 6 KB per 64-clk MMA -- the 1-CTA kernel was bound by the
+// SMEM port (MMA operand reads + incoming copies).
+//
+// Synchronisation (all barriers at identical offsets in both CTAs):
+//   full[stage]   leader only: both CTAs' TMA loads (cta_group::2) credit it
+//   empty[stage]  both: the leader's MMA commit multicasts to the pair
+//   pass_full     both: multicast commit when a level pass is complete
+//   slot_empty[j] leader only: 16 arrivals (8 epilogue warps x 2 CTAs)
+#pragma once
+#include <cstdint>
+
+#include "gemm_lv.cuh"
+
+namespace ozk {
+
+constexpr int kMaxPassMaps = 4;
+
+struct Lv2Params {
+    LvParams lv;                          // operands / epilogue / pass plan
+    CUtensorMap tmA[kMaxPassMaps];        // A slices as [rows of 256 B], box = 16 n rows
+    CUtensorMap tmB[kMaxPassMaps];        // B slices (64-row tiles), box = 8 n rows
+};
+
+template <int S>
+__device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem, uint64_t *full,
+                                             uint64_t *empty, uint64_t *pass_full,
+                                             uint64_t *slot_empty, uint32_t tbase) {
+    constexpr PassPlan PP = make_pass_plan(S);
+    constexpr uint32_t idesc = idesc_i8(256, kLvBN);
+    const LvParams &lp = P2.lv;
+    const GemmParams &p = lp.g;
+    const int64_t total = p.batch * p.tiles_m * p.tiles_n;   // super-tiles (256 x 128)
+    const int Sg = p.stages;
+    uint32_t stage = 0, phase = 0;
+    uint32_t slot_par[kSlots] = {1u, 1u, 1u, 1u};
+    long long t_full = 0, t_slot = 0;
+    const long long t_begin = clock64();
+    const uint64_t dA = smem_desc_kmajor_noswz(0, 128, 256);   // 128-row A operand per CTA
+    const uint64_t dB = smem_desc_kmajor_noswz(0, 128, 256);   // 64-row B half per CTA
+    for (int64_t tile = blockIdx.x >> 1; tile < total; tile += gridDim.x >> 1) {
+#pragma unroll
+        for (int ps = 0; ps < PP.npass; ++ps) {
+            const int hi = PP.hi[ps], lo = PP.lo[ps], tlo = PP.tlo[ps], n = PP.n[ps];
+            const uint32_t abytes = (uint32_t)n * kBlk, bbytes = (uint32_t)n * (kBlk / 2);
+            const int kpp = lp.pass[ps].kpp;
+            for (int64_t kb0 = 0; kb0 < p.KB; kb0 += kpp) {
+                const int nk = (int)min((int64_t)kpp, p.KB - kb0);
+                long long w0 = p.dbg ? clock64() : 0;
+                mbar_wait(&full[stage], phase);
+                if (p.dbg) t_full += clock64() - w0;
+                tc_fence_after();
+                const uint32_t sbase = smem_u32(smem + (size_t)stage * lp.stage_bytes);
+                for (int kk = 0; kk < nk; ++kk) {
+                    const uint32_t abase = sbase + (uint32_t)kk * (abytes + bbytes);
+                    const uint64_t ad0 = dA + (abase >> 4);
+                    const uint64_t bd0 = dB + ((abase + abytes) >> 4);
+                    if (kb0 == 0 && kk == 0) {
+#pragma unroll
+                        for (int j = 0; j < hi - lo + 1; ++j) {
+                            w0 = p.dbg ? clock64() : 0;
+                            mbar_wait(&slot_empty[j], slot_par[j]);
+                            slot_par[j] ^= 1u;
+                            if (p.dbg) t_slot += clock64() - w0;
+                        }
+                        tc_fence_after();
+                    }
+#pragma unroll
+                    for (int r = 0; r < S; ++r) {
+#pragma unroll
+                        for (int j = 0; j < hi - lo + 1; ++j) {
+                            const int L = hi - j;
+                            const int t0 = pp_max(1, L - S), t1 = pp_min(S, L - 1);
+                            const int t = t0 + r;
+                            if (t <= t1) {
+                                const int u = L - t;
+                                const uint32_t acc = (r == 0) ? (uint32_t)(kb0 != 0 || kk != 0) : 1u;
+                                mma_i8_pair_elect(tbase + (uint32_t)(j * kLvBN),
+                                                  ad0 + (uint64_t)(((t - tlo) * kBlk) >> 4),
+                                                  bd0 + (uint64_t)(((u - tlo) * (kBlk / 2)) >> 4), idesc, acc);
+                            }
+                        }
+                    }
+                }
+                mma_commit_pair_elect(&empty[stage]);
+                if (++stage == (uint32_t)Sg) { stage = 0; phase ^= 1; }
+            }
+            mma_commit_pair_elect(pass_full);
+        }
+    }
+    if (p.dbg && (threadIdx.x & 31) == 0) {
+        atomicAdd(p.dbg + DBG_MMA_WAIT_FULL, (unsigned long long)t_full);
+        atomicAdd(p.dbg + DBG_MMA_WAIT_SLOT, (unsigned long long)t_slot);
+        atomicAdd(p.dbg + DBG_MMA_TOTAL, (unsigned long long)(clock64() - t_begin));
+    }
+}
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    k_gemm_lv2(const __grid_constant__ Lv2Params P2) {
+    const LvParams &lp = P2.lv;
+    const GemmParams &p = lp.g;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int S = p.stages;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * lp.stage_bytes);
+    uint64_t *empty = full + S;
+    uint64_t *pass_full = empty + S;
+    uint64_t *slot_empty = pass_full + 1;
+    uint32_t *tholder = reinterpret_cast<uint32_t *>(slot_empty + kSlots);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const int s = p.s;
+    const int64_t total = p.batch * p.tiles_m * p.tiles_n;
+
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(pass_full, 1);
+        for (int j = 0; j < kSlots; ++j) mbar_init(&slot_empty[j], 2 * kNumEpiWarps);
+        fence_mbar_init();
+        for (int q = 0; q < lp.npass; ++q) {
+            tma_prefetch_desc(&P2.tmA[q]);
+            tma_prefetch_desc(&P2.tmB[q]);
+        }
+    }
+    if (warp == 1) tmem_alloc_pair(tholder, 512);
+    tc_fence_before();
+    cluster_sync();          // barriers of both CTAs initialised, TMEM allocated
+    tc_fence_after();
+    const uint32_t tbase = *tholder;
+
+    if (warp == 0) {
+        // ========================= producer (both CTAs): own A rows, own B half
+        if (lane == 0) {
+            uint32_t stage = 0, phase = 0;
+            long long t_wait = 0;
+            for (int64_t tile = blockIdx.x >> 1; tile < total; tile += gridDim.x >> 1) {
+                int64_t b, tm, tn;
+                decode_tile(p, tile, b, tm, tn);
+                // A tiles of 128 rows: this CTA's is 2*tm + rank;  B tiles of 64 rows: 2*tn + rank
+                const int64_t arow0 = ((b * (2 * p.tiles_m) + 2 * tm + rank) * p.KB) * (int64_t)s * (kBlk / 256);
+                const int64_t brow0 = ((b * (2 * p.tiles_n) + 2 * tn + rank) * p.KB) * (int64_t)s * (kBlk / 512);
+                for (int ps = 0; ps < lp.npass; ++ps) {
+                    const LvPass pa = lp.pass[ps];
+                    const uint32_t abytes = (uint32_t)pa.n * kBlk, bbytes = (uint32_t)pa.n * (kBlk / 2);
+                    for (int64_t kb0 = 0; kb0 < p.KB; kb0 += pa.kpp) {
+                        const int nk = (int)min((int64_t)pa.kpp, p.KB - kb0);
+                        const long long w0 = p.dbg ? clock64() : 0;
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        if (p.dbg) t_wait += clock64() - w0;
+                        const uint32_t leader_full = mapa_shared(smem_u32(&full[stage]), 0);
+                        if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2u * (abytes + bbytes) * nk);
+                        uint8_t *dst = smem + (size_t)stage * lp.stage_bytes;
+                        for (int kk = 0; kk < nk; ++kk) {
+                            const int64_t kb = kb0 + kk;
+                            const int ra = (int)(arow0 + (kb * s + pa.tlo - 1) * (kBlk / 256));
+                            const int rb = (int)(brow0 + (kb * s + pa.tlo - 1) * (kBlk / 512));
+                            tma_load_2d_pair(dst, &P2.tmA[ps], 0, ra, leader_full);
+                            tma_load_2d_pair(dst + abytes, &P2.tmB[ps], 0, rb, leader_full);
+                            dst += abytes + bbytes;
+                        }
+                        if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+            if (p.dbg) atomicAdd(p.dbg + DBG_PROD_WAIT, (unsigned long long)t_wait);
+        }
+    } else if (warp == 1) {
+        // ========================= MMA issuer: leader CTA only
+        if (rank == 0) {
+            switch (s) {
+#define OZK_MMA2_CASE(SS) case SS: lv2_mma_role<SS>(P2, smem, full, empty, pass_full, slot_empty, tbase); break;
+                OZK_MMA2_CASE(1) OZK_MMA2_CASE(2) OZK_MMA2_CASE(3) OZK_MMA2_CASE(4)
+                OZK_MMA2_CASE(5) OZK_MMA2_CASE(6) OZK_MMA2_CASE(7) OZK_MMA2_CASE(8)
+                OZK_MMA2_CASE(9) OZK_MMA2_CASE(10) OZK_MMA2_CASE(11) OZK_MMA2_CASE(12)
+#undef OZK_MMA2_CASE
+                default: break;
+            }
+        }
+    } else {
+        // ========================= epilogue (8 warps per CTA, own 128 rows)
+        const int ew = warp - 2;
+        const int q = warp & 3;
+        const int half = ew >> 2;
+        const uint32_t tl = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(half * 64);
+        uint32_t pphase = 0;
+        long long t_w = 0, t_d = 0, t_s = 0;
+        uint32_t slot_remote[kSlots];
+#pragma unroll
+        for (int j = 0; j < kSlots; ++j) slot_remote[j] = mapa_shared(smem_u32(&slot_empty[j]), 0);
+        for (int64_t tile = blockIdx.x >> 1; tile < total; tile += gridDim.x >> 1) {
+            int64_t b, tm, tn;
+            decode_tile(p, tile, b, tm, tn);
+            const int64_t grow = (2 * tm + rank) * kBM + q * 32 + lane;
+            const int32_t e = (grow < p.Mp) ? __ldg(p.ea + b * p.Mp + grow) : 0;
+            double acc[64];
+#pragma unroll
+            for (int j = 0; j < 64; ++j) acc[j] = 0.0;
+            for (int ps = 0; ps < lp.npass; ++ps) {
+                const LvPass pa = lp.pass[ps];
+                long long w0 = p.dbg ? clock64() : 0;
+                mbar_wait(pass_full, pphase);
+                long long w1 = p.dbg ? clock64() : 0;
+                t_w += w1 - w0;
+                pphase ^= 1;
+                tc_fence_after();
+                for (int L = pa.hi; L >= pa.lo; --L) {          // ascending significance (R6)
+                    const int j = pa.hi - L;
+                    const double sc = pow2(-8 * (L - 2));
+#pragma unroll
+                    for (int g = 0; g < 2; ++g) {
+                        uint32_t v0[16], v1[16];
+                        tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + g * 32), v0);
+                        tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + g * 32 + 16), v1);
+                        tmem_wait_ld();
+                        if constexpr (EPI == EPI_LEVELS) {
+                            if (b == 0 && grow < p.Mp) {
+#pragma unroll
+                                for (int i = 0; i < 32; ++i) {
+                                    const int64_t gcol = tn * kLvBN + half * 64 + g * 32 + i;
+                                    if (gcol < p.N)
+                                        p.S_out[(int64_t)(L - 2) * p.Mp * p.N + gcol * p.Mp + grow] =
+                                            (int32_t)(i < 16 ? v0[i] : v1[i - 16]);
+                                }
+                            }
+                            continue;
+                        }
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            acc[g * 32 + i] = __fma_rn(i32_to_f64(v0[i]), sc, acc[g * 32 + i]);
+                            acc[g * 32 + 16 + i] = __fma_rn(i32_to_f64(v1[i]), sc, acc[g * 32 + 16 + i]);
+                        }
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(slot_remote[j]);
+                }
+                if (p.dbg) t_d += clock64() - w1;
+            }
+            const long long s0 = p.dbg ? clock64() : 0;
+            if constexpr (EPI != EPI_LEVELS) lv_store<EPI>(p, b, grow, e, tn * kLvBN + half * 64, acc);
+            if (p.dbg) t_s += clock64() - s0;
+        }
+        if (p.dbg && warp == 2 && lane == 0) {
+            atomicAdd(p.dbg + DBG_EPI_WAIT, (unsigned long long)t_w);
+            atomicAdd(p.dbg + DBG_EPI_DRAIN, (unsigned long long)t_d);
+            atomicAdd(p.dbg + DBG_EPI_STORE, (unsigned long long)t_s);
+        }
+    }
+
+    tc_fence_before();
+    cluster_sync();          // all MMAs done and all TMEM reads of both CTAs finished
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_pair(tbase, 512);
+    }
+}
+
+}  // namespace ozk

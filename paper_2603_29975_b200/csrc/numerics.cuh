@@ -64,4 +64,12 @@ __device__ __forceinline__ double ldexp_rn(double x, int n) {
     return __dmul_rn(y, pow2(E + 1022));
 }
 
+// Exact int32 -> double without the XU pipe: 2^52 + 2^31 + x is representable,
+// built from bits (hi word 0x43300000, lo word x + 2^31); one exact DADD
+// removes the offset.  Same value as __int2double_rn, on the FP64 pipe.
+__device__ __forceinline__ double i32_to_f64(uint32_t x) {
+    const double biased = __hiloint2double(0x43300000, (int)(x ^ 0x80000000u));
+    return __dsub_rn(biased, 4503601774854144.0);   // 2^52 + 2^31
+}
+
 }  // namespace ozk

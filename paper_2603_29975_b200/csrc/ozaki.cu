@@ -5,6 +5,8 @@
 // -> stream-ordered workspace -> K1 (exponents, slices) for both operands ->
 // K2+K3 persistent GEMM with the fused FP64 epilogue.  Everything is enqueued
 // on the caller's stream; nothing synchronises the host.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -18,6 +20,8 @@
 #include <vector>
 
 #include "gemm.cuh"
+#include "gemm_lv.cuh"
+#include "gemm_lv2.cuh"
 #include "ozaki.h"
 #include "split.cuh"
 
@@ -32,6 +36,52 @@ struct Stats {
     std::atomic<uint64_t> dgemm{0}, zgemm{0}, zgemm3m{0}, entries{0}, equiv{0}, macs{0},
         chunks{0}, launches{0};
 } g_stats;
+
+// ------------------------------------------------------------ profiler
+enum Phase { PH_EXP = 0, PH_SLICE = 1, PH_GEMM = 2, PH_OTHER = 3 };
+struct ProfRec {
+    cudaEvent_t a, b;
+    int phase;
+};
+std::atomic<int> g_prof_on{0};
+std::mutex g_prof_mu;
+std::vector<ProfRec> g_prof_recs;
+std::vector<cudaEvent_t> g_prof_pool;
+
+cudaEvent_t prof_event() {
+    // called with g_prof_mu held
+    if (!g_prof_pool.empty()) {
+        cudaEvent_t e = g_prof_pool.back();
+        g_prof_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Brackets one kernel launch with events when profiling is on.
+struct ProfScope {
+    cudaEvent_t a = nullptr;
+    cudaStream_t st;
+    int phase;
+    ProfScope(cudaStream_t s, int ph) : st(s), phase(ph) {
+        if (!g_prof_on.load(std::memory_order_relaxed)) return;
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        a = prof_event();
+        cudaEventRecord(a, st);
+    }
+    ~ProfScope() {
+        if (!a) return;
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        cudaEvent_t b = prof_event();
+        cudaEventRecord(b, st);
+        g_prof_recs.push_back({a, b, phase});
+    }
+};
+
+unsigned long long *g_dbg = nullptr;   // role timers (ozaki_debug_timing)
+std::atomic<int> g_dbg_on{0};
 
 constexpr int kMaxDev = 64;
 struct DevState {
@@ -110,14 +160,55 @@ enum Kind { KIND_REAL = 0, KIND_4M = 1, KIND_3M = 2 };
 struct Plan {
     int s, BN;
     int64_t m, n, k, batch;
-    int64_t Mp;          // output rows of the real product (2m for 4M)
+    int64_t Mp;          // output rows of the real product
+    int64_t Np;          // output columns of the real product (2n for 4M: Re/Im interleaved)
     int64_t kh;          // 4M half width
     int64_t Kp, KB;      // padded depth (bytes) and 32-B blocks
     int64_t tiles_m, tiles_n;
     size_t a_bytes, b_bytes, ea_bytes, fb_bytes;   // per whole batch, 256-B aligned
     int kps, stages;
     size_t smem;
+    bool lv;                 // level-pass kernels (BN = 128)
+    bool pair;               // ... on CTA pairs (k_gemm_lv2, M = 256 per pair)
+    int a_tile_h, b_tile_h;  // operand row tiles of the split layout
+    int npass;
+    uint32_t stage_bytes;
+    LvPass pass[kMaxPass];
 };
+
+// Pass plan of the level-pass kernel: make_pass_plan (passplan.cuh, shared
+// with the device code) plus the per-pass k-blocks per stage.
+void plan_passes(int s, Plan &P) {
+    const PassPlan pp = make_pass_plan(s);
+    P.npass = pp.npass;
+    const uint32_t kb_bytes_per_slice = (uint32_t)(P.a_tile_h + P.b_tile_h) * kKB;   // A + B rows
+    uint32_t maxb = 0;
+    for (int q = 0; q < pp.npass; ++q) {
+        LvPass &pa = P.pass[q];
+        pa.hi = pp.hi[q];
+        pa.lo = pp.lo[q];
+        pa.tlo = pp.tlo[q];
+        pa.n = pp.n[q];
+        maxb = std::max<uint32_t>(maxb, (uint32_t)pa.n * kb_bytes_per_slice);
+    }
+    P.stage_bytes = maxb;
+    for (int q = 0; q < pp.npass; ++q) {
+        const uint32_t per = (uint32_t)P.pass[q].n * kb_bytes_per_slice;
+        P.pass[q].kpp = (int)std::max<int64_t>(1, std::min<int64_t>(maxb / per, P.KB));
+    }
+}
+
+// Kernel selection: OZAKI_KERNEL = "pair" (default for s <= 12), "lv1", "flat".
+int kernel_choice() {
+    static int choice = -1;
+    if (choice < 0) {
+        const char *e = getenv("OZAKI_KERNEL");
+        choice = 2;
+        if (e && !strcmp(e, "lv1")) choice = 1;
+        if (e && !strcmp(e, "flat")) choice = 0;
+    }
+    return choice;
+}
 
 size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -128,12 +219,13 @@ int make_plan(Kind kind, int64_t m, int64_t n, int64_t k, int64_t batch, int s, 
     P.n = n;
     P.k = k;
     P.batch = batch;
-    if (kind == KIND_4M) {
-        P.Mp = 2 * m;
+    P.Mp = m;
+    if (kind == KIND_4M) {   // R9: [Ar|Ai] x [[Br,Bi],[-Bi,Br]], columns interleaved
+        P.Np = 2 * n;
         P.kh = rup(k, 32);
         P.Kp = 2 * P.kh;
     } else {
-        P.Mp = m;
+        P.Np = n;
         P.kh = 0;
         P.Kp = rup(k, 32);
     }
@@ -145,19 +237,39 @@ int make_plan(Kind kind, int64_t m, int64_t n, int64_t k, int64_t batch, int s, 
                     "this build)",
                     (long long)((int64_t)s * keff));
     P.KB = P.Kp / 32;
-    P.tiles_m = (P.Mp + kBM - 1) / kBM;
-    P.tiles_n = (n + P.BN - 1) / P.BN;
+    const int kc = kernel_choice();
+    P.lv = (s <= 12) && kc >= 1;
+    P.pair = P.lv && kc == 2;
+    if (P.lv) P.BN = kLvBN;
+    P.a_tile_h = kBM;
+    P.b_tile_h = P.pair ? kLvBN / 2 : P.BN;
+    if (P.pair) {   // super-tiles of 256 x 128; A in 128-row tiles (padded to pairs), B in 64-row halves
+        P.tiles_m = (P.Mp + 2 * kBM - 1) / (2 * kBM);
+        P.tiles_n = (P.Np + kLvBN - 1) / kLvBN;
+        P.a_bytes = al256((size_t)s * kBM * kKB * P.KB * (2 * P.tiles_m) * batch);
+        P.b_bytes = al256((size_t)s * (kLvBN / 2) * kKB * P.KB * (2 * P.tiles_n) * batch);
+    } else {
+        P.tiles_m = (P.Mp + kBM - 1) / kBM;
+        P.tiles_n = (P.Np + P.BN - 1) / P.BN;
+        P.a_bytes = al256((size_t)s * kBM * kKB * P.KB * P.tiles_m * batch);
+        P.b_bytes = al256((size_t)s * P.BN * kKB * P.KB * P.tiles_n * batch);
+    }
     const size_t a_kb = (size_t)s * kBM * kKB, b_kb = (size_t)s * P.BN * kKB;
-    P.a_bytes = al256(a_kb * P.KB * P.tiles_m * batch);
-    P.b_bytes = al256(b_kb * P.KB * P.tiles_n * batch);
     P.ea_bytes = al256(sizeof(int32_t) * P.Mp * batch);
-    P.fb_bytes = al256(sizeof(int32_t) * n * batch);
-    const size_t kb_bytes = a_kb + b_kb;
-    const size_t budget = 224 * 1024;
-    P.kps = (int)std::max<size_t>(1, std::min<size_t>(40960 / kb_bytes, (size_t)P.KB));
-    P.stages = (int)std::min<size_t>(8, (budget - 2048) / (P.kps * kb_bytes));
+    P.fb_bytes = al256(sizeof(int32_t) * P.Np * batch);
+    const size_t budget = 226 * 1024;
+    if (P.lv) {
+        plan_passes(s, P);
+        P.kps = 1;
+        P.stages = (int)std::min<size_t>(8, (budget - 2048) / P.stage_bytes);
+        P.smem = (size_t)P.stages * P.stage_bytes + 1024 + 512;
+    } else {
+        const size_t kb_bytes = a_kb + b_kb;
+        P.kps = (int)std::max<size_t>(1, std::min<size_t>(40960 / kb_bytes, (size_t)P.KB));
+        P.stages = (int)std::min<size_t>(8, (budget - 2048) / (P.kps * kb_bytes));
+        P.smem = (size_t)P.stages * P.kps * kb_bytes + 1024 /*align*/ + 256 /*barriers*/;
+    }
     if (P.stages < 2) return fail(OZAKI_ERR_UNSUPPORTED, "pipeline does not fit in shared memory");
-    P.smem = (size_t)P.stages * P.kps * kb_bytes + 1024 /*align*/ + 256 /*barriers*/;
     return 0;
 }
 
@@ -255,45 +367,128 @@ int launch_split(const Plan &P, const Operand &op, bool sideA, int8_t *slices, i
     sp.mode = op.mode;
     sp.conj = op.conj;
     sp.s = P.s;
-    sp.tile_h = sideA ? kBM : P.BN;
-    sp.tiles = sideA ? P.tiles_m : P.tiles_n;
+    sp.tile_h = sideA ? P.a_tile_h : P.b_tile_h;
+    sp.tiles = (sideA ? P.tiles_m : P.tiles_n) * (P.pair ? 2 : 1);
     sp.KB = P.KB;
     sp.kh = P.kh;
-    sp.rows_out = (op.mode == SPLIT_A4M) ? 2 * op.rows : op.rows;
-    sp.rows_grid = (op.mode == SPLIT_A4M) ? sp.tiles * sp.tile_h / 2 : sp.tiles * sp.tile_h;
+    sp.rows_out = (op.mode == SPLIT_B4M) ? 2 * op.rows : op.rows;
+    sp.rows_grid = (op.mode == SPLIT_B4M) ? sp.tiles * sp.tile_h / 2 : sp.tiles * sp.tile_h;
     sp.out = slices;
     sp.exps = exps;
     sp.nonfinite = dev->nonfinite;
     if (op.rows == 0) return 0;
     const bool rcontig = (op.rs == 1);
     const dim3 blk(32, 8);
-    if (rcontig) {
-        dim3 grid((unsigned)((op.rows + 31) / 32), 1, (unsigned)P.batch);
-        k_exponent<true><<<grid, blk, 0, st>>>(sp);
-    } else {
-        dim3 grid((unsigned)((op.rows + 7) / 8), 1, (unsigned)P.batch);
-        k_exponent<false><<<grid, blk, 0, st>>>(sp);
+    {
+        ProfScope ps(st, PH_EXP);
+        if (rcontig) {
+            dim3 grid((unsigned)((op.rows + 31) / 32), 1, (unsigned)P.batch);
+            k_exponent<true><<<grid, blk, 0, st>>>(sp);
+        } else {
+            dim3 grid((unsigned)((op.rows + 7) / 8), 1, (unsigned)P.batch);
+            k_exponent<false><<<grid, blk, 0, st>>>(sp);
+        }
     }
     CUDA_TRY(cudaGetLastError());
     const bool four_m = (op.mode == SPLIT_A4M || op.mode == SPLIT_B4M);
     const int64_t nchunks = four_m ? (P.kh >> 4) : (P.KB * 2);
     dim3 grid2((unsigned)((sp.rows_grid + 63) / 64), (unsigned)((nchunks + 3) / 4), (unsigned)P.batch);
-    if (P.s <= 8)
-        k_slice<8><<<grid2, dim3(64, 4), 0, st>>>(sp);
-    else
-        k_slice<16><<<grid2, dim3(64, 4), 0, st>>>(sp);
+    {
+        ProfScope ps(st, PH_SLICE);
+        if (P.s <= 8)
+            k_slice<8><<<grid2, dim3(64, 4), 0, st>>>(sp);
+        else
+            k_slice<16><<<grid2, dim3(64, 4), 0, st>>>(sp);
+    }
     CUDA_TRY(cudaGetLastError());
     g_stats.launches += 2;
     return 0;
 }
 
 // ---------------------------------------------------------------- K2 launch
+template <int EPI>
+int launch_gemm_lv(const Plan &P, const GemmParams &gp, DevState *dev, cudaStream_t st) {
+    static std::atomic<size_t> done{0};
+    if (done.load() < P.smem) {
+        CUDA_TRY(cudaFuncSetAttribute(k_gemm_lv<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)P.smem));
+        done.store(P.smem);
+    }
+    LvParams lp{};
+    lp.g = gp;
+    lp.npass = P.npass;
+    lp.stage_bytes = P.stage_bytes;
+    for (int q = 0; q < P.npass; ++q) lp.pass[q] = P.pass[q];
+    const int64_t tiles = P.batch * P.tiles_m * P.tiles_n;
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, dev->sms);
+    {
+        ProfScope ps(st, PH_GEMM);
+        k_gemm_lv<EPI><<<grid, kGemmThreads, P.smem, st>>>(lp);
+    }
+    CUDA_TRY(cudaGetLastError());
+    g_stats.launches += 1;
+    return 0;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+int rows_map(CUtensorMap *m, const void *base, size_t bytes, uint32_t box_rows) {
+    if (!g_encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) return fail(OZAKI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }
+    cuuint64_t dims[2] = {256, (cuuint64_t)(bytes / 256)};
+    cuuint64_t strides[1] = {256};
+    cuuint32_t box[2] = {256, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(OZAKI_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return 0;
+}
+
+template <int EPI>
+int launch_gemm_lv2(const Plan &P, const GemmParams &gp, DevState *dev, cudaStream_t st) {
+    static std::atomic<size_t> done{0};
+    if (done.load() < P.smem) {
+        CUDA_TRY(cudaFuncSetAttribute(k_gemm_lv2<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)P.smem));
+        done.store(P.smem);
+    }
+    Lv2Params P2;
+    std::memset(&P2, 0, sizeof P2);
+    P2.lv.g = gp;
+    P2.lv.npass = P.npass;
+    P2.lv.stage_bytes = P.stage_bytes;
+    for (int q = 0; q < P.npass; ++q) {
+        P2.lv.pass[q] = P.pass[q];
+        if (int rc = rows_map(&P2.tmA[q], gp.A, P.a_bytes, (uint32_t)P.pass[q].n * (kBlk / 256))) return rc;
+        if (int rc = rows_map(&P2.tmB[q], gp.B, P.b_bytes, (uint32_t)P.pass[q].n * (kBlk / 512))) return rc;
+    }
+    const int64_t tiles = P.batch * P.tiles_m * P.tiles_n;
+    const unsigned pairs = (unsigned)std::min<int64_t>(tiles, dev->sms / 2);
+    {
+        ProfScope ps(st, PH_GEMM);
+        k_gemm_lv2<EPI><<<2 * pairs, kGemmThreads, P.smem, st>>>(P2);
+    }
+    CUDA_TRY(cudaGetLastError());
+    g_stats.launches += 1;
+    return 0;
+}
+
 template <int BN, int EPI>
 int launch_gemm_t(const Plan &P, const GemmParams &gp, DevState *dev, cudaStream_t st) {
     if (int rc = set_gemm_attr<BN, EPI>(P.smem)) return rc;
     const int64_t tiles = P.batch * P.tiles_m * P.tiles_n;
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, dev->sms);
-    k_gemm<BN, EPI><<<grid, kGemmThreads, P.smem, st>>>(gp);
+    {
+        ProfScope ps(st, PH_GEMM);
+        k_gemm<BN, EPI><<<grid, kGemmThreads, P.smem, st>>>(gp);
+    }
     CUDA_TRY(cudaGetLastError());
     g_stats.launches += 1;
     return 0;
@@ -308,7 +503,7 @@ int launch_gemm(const Plan &P, int epi, const int8_t *sa, const int8_t *sb, cons
     gp.ea = ea;
     gp.fb = fb;
     gp.Mp = P.Mp;
-    gp.N = P.n;
+    gp.N = P.Np;
     gp.KB = P.KB;
     gp.tiles_m = P.tiles_m;
     gp.tiles_n = P.tiles_n;
@@ -326,6 +521,23 @@ int launch_gemm(const Plan &P, int epi, const int8_t *sa, const int8_t *sb, cons
     gp.beta_r = be[0];
     gp.beta_i = be[1];
     gp.S_out = S_out;
+    if (g_dbg_on.load()) {
+        if (!g_dbg) {
+            CUDA_TRY(cudaMalloc(&g_dbg, sizeof(unsigned long long) * DBG_NSLOT));
+            CUDA_TRY(cudaMemset(g_dbg, 0, sizeof(unsigned long long) * DBG_NSLOT));
+        }
+        gp.dbg = g_dbg;
+    }
+    if (P.pair) {
+        if (epi == EPI_REAL) return launch_gemm_lv2<EPI_REAL>(P, gp, dev, st);
+        if (epi == EPI_CPLX4M) return launch_gemm_lv2<EPI_CPLX4M>(P, gp, dev, st);
+        return launch_gemm_lv2<EPI_LEVELS>(P, gp, dev, st);
+    }
+    if (P.lv) {
+        if (epi == EPI_REAL) return launch_gemm_lv<EPI_REAL>(P, gp, dev, st);
+        if (epi == EPI_CPLX4M) return launch_gemm_lv<EPI_CPLX4M>(P, gp, dev, st);
+        return launch_gemm_lv<EPI_LEVELS>(P, gp, dev, st);
+    }
     if (P.BN == 64) {
         if (epi == EPI_REAL) return launch_gemm_t<64, EPI_REAL>(P, gp, dev, st);
         if (epi == EPI_CPLX4M) return launch_gemm_t<64, EPI_CPLX4M>(P, gp, dev, st);
@@ -452,6 +664,7 @@ int run(const Call &c0) {
     if (alpha0 || c.k == 0) {
         if (beta1 || c.S_out) return 0;
         dim3 grid(grid1d(c.m * c.n, dev->sms), 1, (unsigned)c.batch);
+        ProfScope ps(st, PH_OTHER);
         if (cplx)
             k_scale_cplx<<<grid, 256, 0, st>>>(c.C, c.m, c.n, c.ldc, c.sC, c.be[0], c.be[1]);
         else
@@ -501,6 +714,7 @@ int run(const Call &c0) {
         }
         if (!rc) {
             dim3 grid(grid1d(c.m * c.n, dev->sms), 1, (unsigned)c.batch);
+            ProfScope ps(st, PH_OTHER);
             k_combine_3m<<<grid, 256, 0, st>>>(T, (double *)((char *)T + t_bytes),
                                               (double *)((char *)T + 2 * t_bytes), c.C, c.m, c.n,
                                               c.ldc, c.sC, c.al[0], c.al[1], c.be[0], c.be[1]);
@@ -516,8 +730,9 @@ int run(const Call &c0) {
     const uint64_t mult = c.kind == KIND_REAL ? 1 : (c.kind == KIND_4M ? 4 : 3);
     g_stats.entries += (uint64_t)c.batch;
     g_stats.equiv += pr * mult * (uint64_t)c.batch;
-    g_stats.macs += pr * (uint64_t)(c.kind == KIND_3M ? 3 : 1) * (uint64_t)P.tiles_m * kBM *
-                    (uint64_t)P.tiles_n * P.BN * (uint64_t)P.Kp * (uint64_t)c.batch;
+    const uint64_t rows_pad = (uint64_t)P.tiles_m * kBM * (P.pair ? 2 : 1);
+    g_stats.macs += pr * (uint64_t)(c.kind == KIND_3M ? 3 : 1) * rows_pad * (uint64_t)P.tiles_n * P.BN *
+                    (uint64_t)P.Kp * (uint64_t)c.batch;
     if (c.kind == KIND_REAL) g_stats.dgemm += 1;
     if (c.kind == KIND_4M) g_stats.zgemm += 1;
     if (c.kind == KIND_3M) g_stats.zgemm3m += 1;
@@ -683,6 +898,29 @@ int64_t ozaki_workspace_size(char kind, int64_t m, int64_t n, int64_t k, int64_t
 
 const char *ozaki_last_error(void) { return t_err.c_str(); }
 
+int ozaki_profile_enable(int on) {
+    g_prof_on.store(on ? 1 : 0);
+    return 0;
+}
+
+int ozaki_profile_read(ozaki_profile_t *out) {
+    if (!out) return -1;
+    std::memset(out, 0, sizeof *out);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    int rc = 0;
+    for (const ProfRec &r : g_prof_recs) {
+        float ms = 0.f;
+        if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess)
+            rc = OZAKI_ERR_CUDA;
+        out->ms[r.phase] += ms;
+        out->launches[r.phase] += 1;
+        g_prof_pool.push_back(r.a);
+        g_prof_pool.push_back(r.b);
+    }
+    g_prof_recs.clear();
+    return rc;
+}
+
 const char *ozaki_version(void) { return "ozaki-b200 0.1 (sm_100a, tcgen05 kind::i8)"; }
 
 int ozaki_debug_split(char side, char kind, char trans, int64_t rows, int64_t cols,
@@ -718,7 +956,7 @@ int ozaki_debug_split(char side, char kind, char trans, int64_t rows, int64_t co
     const bool sideA = side == 'A';
     Operand op = sideA ? view_A(X, trans, rows, cols, ldx, 0, mode) : view_B(X, trans, rows, cols, ldx, 0, mode);
     const size_t sl_bytes = sideA ? P.a_bytes : P.b_bytes;
-    const int64_t rows_out = (mode == SPLIT_A4M) ? 2 * rows : rows;
+    const int64_t rows_out = (mode == SPLIT_B4M) ? 2 * rows : rows;
     void *base = nullptr;
     CUDA_TRY(cudaMallocAsync(&base, sl_bytes + al256(4 * (rows_out + 1)), st));
     int8_t *sl = (int8_t *)base;
@@ -728,7 +966,7 @@ int ozaki_debug_split(char side, char kind, char trans, int64_t rows, int64_t co
     if (!rc && rows_out > 0 && kdepth > 0) {
         const int64_t total = (int64_t)num_slices * rows_out * kdepth;
         k_unpack<<<grid1d(total, dev->sms), 256, 0, st>>>(sl, slices_out, rows_out, kdepth, num_slices,
-                                                        sideA ? kBM : P.BN, P.KB);
+                                                        sideA ? P.a_tile_h : P.b_tile_h, P.KB);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) rc = fail(OZAKI_ERR_CUDA, "unpack: %s", cudaGetErrorString(e));
         if (!rc && exps_out) {
@@ -739,6 +977,18 @@ int ozaki_debug_split(char side, char kind, char trans, int64_t rows, int64_t co
     cudaFreeAsync(base, st);
     if (kdepth_out) *kdepth_out = kdepth;
     return rc;
+}
+
+int ozaki_debug_timing(int enable, uint64_t *out, int nslots) {
+    g_dbg_on.store(enable ? 1 : 0);
+    if (out && g_dbg) {
+        CUDA_TRY(cudaDeviceSynchronize());
+        unsigned long long h[DBG_NSLOT] = {0};
+        CUDA_TRY(cudaMemcpy(h, g_dbg, sizeof h, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < nslots && i < DBG_NSLOT; ++i) out[i] = h[i];
+        CUDA_TRY(cudaMemset(g_dbg, 0, sizeof h));
+    }
+    return DBG_NSLOT;
 }
 
 int ozaki_debug_level_sums(char transa, char transb, int64_t m, int64_t n, int64_t k,

@@ -24,8 +24,8 @@ namespace ozk {
 
 enum SplitMode : int {
     SPLIT_REAL = 0,   // real operand
-    SPLIT_A4M = 1,    // complex op(A) -> rows 2r: [Re | -Im], 2r+1: [Im | Re]
-    SPLIT_B4M = 2,    // complex op(B) -> column j: [Re ; Im]
+    SPLIT_A4M = 1,    // complex op(A) -> row r: [Re | Im]
+    SPLIT_B4M = 2,    // complex op(B) -> columns 2j: [Re ; -Im], 2j+1: [Im ; Re]  (R9, N side)
     SPLIT_RE = 3,     // 3M operands: Re, Im, fl(Re + Im)
     SPLIT_IM = 4,
     SPLIT_SUM = 5,
@@ -38,7 +38,7 @@ struct SplitParams {
     int64_t rows;         // valid input rows
     int64_t k;            // valid input depth
     int64_t rows_grid;    // input rows covered by the slice grid (covers all tile rows)
-    int64_t rows_out;     // valid output rows (2*rows for A4M)
+    int64_t rows_out;     // valid output rows (2*rows for B4M)
     int32_t mode, conj, s, tile_h;
     int64_t tiles;        // output row tiles per batch entry
     int64_t KB;           // 32-byte K blocks per output row
@@ -72,7 +72,7 @@ __device__ __forceinline__ void reduce_and_store(const SplitParams &p, int64_t b
                                                  uint64_t maxb, uint32_t nf) {
     int32_t e = nf ? kNonFinite : exponent_from_maxbits(maxb);
     int32_t *ex = p.exps + b * p.rows_out;
-    if (p.mode == SPLIT_A4M) {
+    if (p.mode == SPLIT_B4M) {
         ex[2 * r] = e;
         ex[2 * r + 1] = e;
     } else {
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(256) k_slice(const SplitParams p) {
 
     const bool row_ok = r < p.rows;
     int32_t e = 0;
-    if (row_ok) e = p.exps[b * p.rows_out + (p.mode == SPLIT_A4M ? 2 * r : r)];
+    if (row_ok) e = p.exps[b * p.rows_out + (p.mode == SPLIT_B4M ? 2 * r : r)];
     const bool live = row_ok && e != kNonFinite;
     const int64_t l0 = c * 16;
     DigitWords<SMAX> dw;
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(256) k_slice(const SplitParams p) {
         return;
     }
     const int64_t c2 = (p.kh >> 4) + c;   // chunk index in the second half
-    if (p.mode == SPLIT_B4M) {
+    if (p.mode == SPLIT_A4M) {            // row r = [Re | Im]
         zero_words(dw);
 #pragma unroll
         for (int i = 0; i < 16; ++i) put_digits<SMAX>(dw, i, re[i], e, p.s);
@@ -282,8 +282,8 @@ __global__ void __launch_bounds__(256) k_slice(const SplitParams p) {
         store_digits<SMAX>(p, b, r, c2, dw);
         return;
     }
-    // SPLIT_A4M: row 2r = [Re | -Im], row 2r+1 = [Im | Re]; -Im is split from
-    // the negated FP64 value (balanced digits are not sign-symmetric, R9).
+    // SPLIT_B4M: column 2r = [Re ; -Im], column 2r+1 = [Im ; Re]; -Im is split
+    // from the negated FP64 value (balanced digits are not sign-symmetric, R9).
     zero_words(dw);
 #pragma unroll
     for (int i = 0; i < 16; ++i) put_digits<SMAX>(dw, i, re[i], e, p.s);

@@ -80,28 +80,30 @@ def test_split_complex_bitexact(orc, side, trans, s):
         D, e, nf = orc.split_rows(np.ascontiguousarray(val), s)
         assert (host(ex) == e).all(), kind
         assert (host(sl) == D).all(), kind
-    # 4M embedding: A rows 2r = [Re | -Im], 2r+1 = [Im | Re]; B columns [Re ; Im];
-    # halves start at 0 and kh = round_up(k, 32)
+    # 4M embedding (R9, N side): A rows r = [Re | Im]; B columns 2j = [Re ; -Im],
+    # 2j+1 = [Im ; Re]; halves start at 0 and kh = round_up(k, 32)
     sl, ex = oz.debug_split(side, "z", trans, dev(X), s)
     sl, ex = host(sl), host(ex)
     kh = (k + 31) // 32 * 32
+
+    def check_halves(got, src):
+        assert (got[:, :k] == src[:, :k]).all()
+        assert (got[:, kh:kh + k] == src[:, k:]).all()
+        assert not got[:, k:kh].any() and not got[:, kh + k:].any()
+
     if side == "A":
-        D, e, _ = orc.split_rows(np.ascontiguousarray(np.vstack([np.hstack([rows.real, -rows.imag]),
-                                                                 np.hstack([rows.imag, rows.real])])), s)
-        m = rows.shape[0]
-        for r in range(m):
-            for half, src in ((0, D[:, r, :]), (1, D[:, m + r, :])):
-                got = sl[:, 2 * r + half, :]
-                assert (got[:, :k] == src[:, :k]).all()
-                assert (got[:, kh:kh + k] == src[:, k:]).all()
-                assert not got[:, k:kh].any() and not got[:, kh + k:].any()
-            assert ex[2 * r] == e[r] == ex[2 * r + 1]
-    else:
         D, e, _ = orc.split_rows(np.ascontiguousarray(np.hstack([rows.real, rows.imag])), s)
         assert (ex == e).all()
-        assert (sl[:, :, :k] == D[:, :, :k]).all()
-        assert (sl[:, :, kh:kh + k] == D[:, :, k:]).all()
-        assert not sl[:, :, k:kh].any() and not sl[:, :, kh + k:].any()
+        for r in range(rows.shape[0]):
+            check_halves(sl[:, r, :], D[:, r, :])
+    else:
+        nn = rows.shape[0]
+        D, e, _ = orc.split_rows(np.ascontiguousarray(np.vstack([np.hstack([rows.real, -rows.imag]),
+                                                                 np.hstack([rows.imag, rows.real])])), s)
+        for r in range(nn):
+            check_halves(sl[:, 2 * r, :], D[:, r, :])
+            check_halves(sl[:, 2 * r + 1, :], D[:, nn + r, :])
+            assert ex[2 * r] == e[r] == ex[2 * r + 1] == e[nn + r]
 
 
 # ------------------------------------------------------------ level sums

@@ -1,0 +1,17 @@
+#!/bin/bash
+# One gpurun call: smoke, bench, launch list, ncu full captures.  Outputs in gpurun_out/.
+set -x
+cd "$GRAFT_REPO_ROOT" 2>/dev/null || true
+mkdir -p gpurun_out
+TAG=${TAG:-r1}
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1
+timeout 600 python bench.py ${BENCH_ARGS} > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
+if [ "${NCU:-1}" = "1" ]; then
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv \
+    python bench.py --steps 2 --warmup 3 --no-extras ${BENCH_ARGS} > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 3 -c 1 -f -o gpurun_out/prof_gemm_$TAG \
+    python bench.py --steps 1 --warmup 3 --no-extras ${BENCH_ARGS} > gpurun_out/ncu_gemm_$TAG.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_slice -s 6 -c 2 -f -o gpurun_out/prof_slice_$TAG \
+    python bench.py --steps 1 --warmup 3 --no-extras ${BENCH_ARGS} > gpurun_out/ncu_slice_$TAG.log 2>&1
+fi
+ls -la gpurun_out
