@@ -46,16 +46,6 @@ struct LvParams {
     LvPass pass[kMaxPass];
 };
 
-// P = acc * 2^n: exact exponent-field add when acc and the result are normal
-// (the common case, branch-free); otherwise the general correctly-rounded path.
-__device__ __forceinline__ double scale_pow2(double acc, int n) {
-    const long long b = __double_as_longlong(acc);
-    const int ex = (int)((b >> 52) & 0x7ff);
-    const int E = ex + n;
-    const bool fast = (ex != 0) && (E >= 1) && (E <= 2046);
-    return fast ? __longlong_as_double(b + ((long long)n << 52)) : ldexp_rn(acc, n);
-}
-
 // Final epilogue of one thread: its row `grow`, 64 consecutive product
 // columns col0 .. col0+63 held in acc[].  Complex (4M, R9 N-side embedding):
 // columns 2c / 2c+1 are Re / Im of complex column col0/2 + c, so each thread

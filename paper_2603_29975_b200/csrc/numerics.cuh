@@ -64,6 +64,17 @@ __device__ __forceinline__ double ldexp_rn(double x, int n) {
     return __dmul_rn(y, pow2(E + 1022));
 }
 
+// x * 2^n, correctly rounded: exact exponent-field add when x and the result
+// are normal (the common case, branch-free select); otherwise ldexp_rn.
+__device__ __forceinline__ double scale_pow2(double x, int n) {
+    const long long b = __double_as_longlong(x);
+    const int ex = (int)((b >> 52) & 0x7ff);
+    const int E = ex + n;
+    const bool fast = (ex != 0) && (ex != 0x7ff) && (E >= 1) && (E <= 2046);
+    if (fast) return __longlong_as_double(b + ((long long)n << 52));
+    return ldexp_rn(x, n);
+}
+
 // Exact int32 -> double without the XU pipe: 2^52 + 2^31 + x is representable,
 // built from bits (hi word 0x43300000, lo word x + 2^31); one exact DADD
 // removes the offset.  Same value as __int2double_rn, on the FP64 pipe.

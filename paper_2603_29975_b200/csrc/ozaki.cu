@@ -378,30 +378,34 @@ int launch_split(const Plan &P, const Operand &op, bool sideA, int8_t *slices, i
     sp.nonfinite = dev->nonfinite;
     if (op.rows == 0) return 0;
     const bool rcontig = (op.rs == 1);
-    const dim3 blk(32, 8);
-    {
-        ProfScope ps(st, PH_EXP);
-        if (rcontig) {
-            dim3 grid((unsigned)((op.rows + 31) / 32), 1, (unsigned)P.batch);
-            k_exponent<true><<<grid, blk, 0, st>>>(sp);
-        } else {
-            dim3 grid((unsigned)((op.rows + 7) / 8), 1, (unsigned)P.batch);
-            k_exponent<false><<<grid, blk, 0, st>>>(sp);
-        }
-    }
-    CUDA_TRY(cudaGetLastError());
-    const bool four_m = (op.mode == SPLIT_A4M || op.mode == SPLIT_B4M);
-    const int64_t nchunks = four_m ? (P.kh >> 4) : (P.KB * 2);
-    dim3 grid2((unsigned)((sp.rows_grid + 63) / 64), (unsigned)((nchunks + 3) / 4), (unsigned)P.batch);
+    const bool cplx = op.mode != SPLIT_REAL;
+    dim3 grid((unsigned)((sp.rows_grid + 7) / 8), (unsigned)P.batch);
+    // SMEM window: 8 rows x KW elements (+ pad), 64 KB
+    const int KW = cplx ? 512 : 1024;
+    const size_t smem = (size_t)8 * (KW + (cplx ? 1 : 2)) * (cplx ? 16 : 8);
     {
         ProfScope ps(st, PH_SLICE);
-        if (P.s <= 8)
-            k_slice<8><<<grid2, dim3(64, 4), 0, st>>>(sp);
-        else
-            k_slice<16><<<grid2, dim3(64, 4), 0, st>>>(sp);
+#define OZK_SPLIT(SM, RC, CX)                                                                       \
+        {                                                                                           \
+            static bool attr = false;                                                               \
+            if (!attr) {                                                                            \
+                cudaFuncSetAttribute(k_split_sm<SM, RC, CX>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     (int)smem);                                                    \
+                attr = true;                                                                        \
+            }                                                                                       \
+            k_split_sm<SM, RC, CX><<<grid, 256, smem, st>>>(sp, KW);                                \
+        }
+        if (P.s <= 8) {
+            if (rcontig) { if (cplx) OZK_SPLIT(8, true, true) else OZK_SPLIT(8, true, false) }
+            else { if (cplx) OZK_SPLIT(8, false, true) else OZK_SPLIT(8, false, false) }
+        } else {
+            if (rcontig) { if (cplx) OZK_SPLIT(16, true, true) else OZK_SPLIT(16, true, false) }
+            else { if (cplx) OZK_SPLIT(16, false, true) else OZK_SPLIT(16, false, false) }
+        }
+#undef OZK_SPLIT
     }
     CUDA_TRY(cudaGetLastError());
-    g_stats.launches += 2;
+    g_stats.launches += 1;
     return 0;
 }
 

@@ -3,10 +3,10 @@
 // Method (§2.2 "splits high-precision input matrices into slices
 // ... based on their significant bits and exponent alignment"; readings R3/R4
 // in DESIGN.md §3):
-//   phase 1 (k_exponent): e_r = exponent rule R3 applied to max |x| of the
+//   pass 1 (k_split): e_r = exponent rule R3 applied to max |x| of the
 //            r-th "row" (row of op(A) / column of op(B)), by a max-reduction of
-//            IEEE bit patterns (warp shuffles).
-//   phase 2 (k_slice):    X = RNE(x * 2^(8s-1-e_r)), then s balanced base-256
+//            IEEE bit patterns.
+//   pass 2 (k_split): X = RNE(x * 2^(8s-1-e_r)), then s balanced base-256
 //            digits, written as INT8 into the GEMM's tiled operand layout
 //            (DESIGN.md §5): per (row tile, 32-byte K block, slice) one
 //            canonical K-major SWIZZLE_NONE block of tile_h rows x 32 bytes,
@@ -18,9 +18,15 @@
 #pragma once
 #include <cstdint>
 
+#include <type_traits>
+
 #include "numerics.cuh"
 
 namespace ozk {
+
+__device__ __forceinline__ uint32_t smem_u32_split(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
 
 enum SplitMode : int {
     SPLIT_REAL = 0,   // real operand
@@ -81,222 +87,410 @@ __device__ __forceinline__ void reduce_and_store(const SplitParams &p, int64_t b
     if (nf) atomicAdd(p.nonfinite, 1ull);
 }
 
-// Phase 1.  RCONTIG: consecutive rows are contiguous (rs == 1): block (32,8),
-// thread x = row, y strides the depth, smem max-reduce.  Otherwise each row is
-// contiguous along l: one warp per row, lanes stride l, shuffle max-reduce.
-template <bool RCONTIG>
-__global__ void __launch_bounds__(256) k_exponent(const SplitParams p) {
-    const int64_t b = blockIdx.z;
-    const void *base = p.mode == SPLIT_REAL
-                           ? (const void *)(reinterpret_cast<const double *>(p.X) + b * p.bstride)
-                           : (const void *)(reinterpret_cast<const double2 *>(p.X) + b * p.bstride);
-    if constexpr (RCONTIG) {
-        __shared__ uint64_t smax[8][33];
-        __shared__ uint32_t snf[8][33];
-        const int64_t r = (int64_t)blockIdx.x * 32 + threadIdx.x;
-        uint64_t m = 0;
-        uint32_t nf = 0;
-        if (r < p.rows) {
-            for (int64_t l = threadIdx.y; l < p.k; l += 8) {
-                uint64_t u = mag_bits(p, base, r * p.rs + l * p.ls);
-                nf |= (u >= kExpInf);
-                m = (u < kExpInf && u > m) ? u : m;
-            }
-        }
-        smax[threadIdx.y][threadIdx.x] = m;
-        snf[threadIdx.y][threadIdx.x] = nf;
-        __syncthreads();
-        if (threadIdx.y == 0 && r < p.rows) {
-            for (int y = 1; y < 8; ++y) {
-                uint64_t o = smax[y][threadIdx.x];
-                m = o > m ? o : m;
-                nf |= snf[y][threadIdx.x];
-            }
-            reduce_and_store(p, b, r, m, nf);
-        }
-    } else {
-        const int warp = threadIdx.y, lane = threadIdx.x;
-        const int64_t r = (int64_t)blockIdx.x * 8 + warp;
-        if (r >= p.rows) return;
-        uint64_t m = 0;
-        uint32_t nf = 0;
-        for (int64_t l = lane; l < p.k; l += 32) {
-            uint64_t u = mag_bits(p, base, r * p.rs + l * p.ls);
-            nf |= (u >= kExpInf);
-            m = (u < kExpInf && u > m) ? u : m;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            uint64_t om = __shfl_xor_sync(0xffffffffu, m, o);
-            m = om > m ? om : m;
-            nf |= __shfl_xor_sync(0xffffffffu, nf, o);
-        }
-        if (lane == 0) reduce_and_store(p, b, r, m, nf);
-    }
-}
-
 // ------------------------------------------------------------------ digits
 // R4: X = RNE(x 2^(P-e)), P = 8s-1; balanced digits via the offset trick:
 // with Bofs = sum_{p=0}^{s-2} 128*256^p, Z = X + Bofs has plain base-256 bytes
 // (d_t + 128) at positions p = s-t for t >= 2 and d_1 = Z >> 8(s-1).
-template <int SMAX>
-struct DigitWords {
-    uint32_t w[SMAX][4];   // slice t (0 = most significant), 16 bytes
-};
-
-template <int SMAX>
-__device__ __forceinline__ void put_digits(DigitWords<SMAX> &dw, int i, double x, int32_t e,
-                                           int s) {
-    const int P = 8 * s - 1;
-    const int sh_i = 8 * (i & 3);
-    const int wi = i >> 2;
-    if constexpr (SMAX <= 8) {
-        double v = ldexp_rn(x, P - e);                 // |v| <= 127*2^(8s-8) < 2^63
-        long long X = __double2ll_rn(v);
-        long long bofs = (long long)(0x0080808080808080ull >> (8 * (8 - s)));   // s-1 bytes
-        long long Z = X + bofs;
+// 8 consecutive values of the split view at (r, l0..l0+7): comp 0 real,
+// 1 Re, 2 Im, 3 fl(Re + Im); `neg` flips the sign (the -Im block of 4M).
+// Conjugation applies to Im.
+__device__ __forceinline__ void load8(const SplitParams &p, const void *base, int64_t r, int64_t l0,
+                                      int comp, bool neg, bool live, double (&v)[8]) {
+    if (comp == 0) {
+        const double *x = reinterpret_cast<const double *>(base) + r * p.rs;
 #pragma unroll
-        for (int t = 0; t < SMAX; ++t) {
-            if (t < s) {
-                int p = s - 1 - t;
-                int d = (t == 0) ? (int)(Z >> (8 * p)) : (int)((Z >> (8 * p)) & 0xff) - 128;
-                dw.w[t][wi] |= ((uint32_t)d & 0xffu) << sh_i;
+        for (int i = 0; i < 8; ++i) {
+            const int64_t l = l0 + i;
+            v[i] = (live && l < p.k) ? __ldg(x + l * p.ls) : 0.0;
+        }
+        return;
+    }
+    const double2 *x = reinterpret_cast<const double2 *>(base) + r * p.rs;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t l = l0 + i;
+        double val = 0.0;
+        if (live && l < p.k) {
+            if (comp == 1) {
+                val = __ldg(&x[l * p.ls].x);
+            } else {
+                const double im0 = __ldg(&x[l * p.ls].y);
+                const double im = p.conj ? -im0 : im0;
+                val = (comp == 2) ? im : __dadd_rn(__ldg(&x[l * p.ls].x), im);
             }
+        }
+        v[i] = neg ? -val : val;
+    }
+}
+
+// 4x4 byte transpose: out[q] byte i = in[i] byte q.
+__device__ __forceinline__ void transpose4x4(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                             uint32_t &o0, uint32_t &o1, uint32_t &o2, uint32_t &o3) {
+    const uint32_t t0 = __byte_perm(a0, a1, 0x5140), t1 = __byte_perm(a2, a3, 0x5140);
+    const uint32_t t2 = __byte_perm(a0, a1, 0x7362), t3 = __byte_perm(a2, a3, 0x7362);
+    o0 = __byte_perm(t0, t1, 0x5410);
+    o1 = __byte_perm(t0, t1, 0x7632);
+    o2 = __byte_perm(t2, t3, 0x5410);
+    o3 = __byte_perm(t2, t3, 0x7632);
+}
+
+// R4 for 8 consecutive values and the s slices of their 8-byte output.
+// X = RNE(x 2^(P-e)); with B = 0x80 in each of the s-1 low bytes,
+// Y = (X + B) XOR B holds every balanced digit as a byte: byte q of Y is the
+// digit of slice t = s - q (q = s-1 is d_1, the most significant).  An 8x8
+// byte transpose (PRMT) turns the 8 values' Y into one 8-byte word per slice,
+// stored at up to two output locations (dst0, dst1; blk = bytes between slices).
+template <int SMAX>
+__device__ __forceinline__ void digits_store8(const double (&v)[8], int32_t e, int s, int8_t *dst0,
+                                              int8_t *dst1, int64_t blk) {
+    const int P = 8 * s - 1;
+    constexpr int NW = SMAX / 4;   // 32-bit words of Y per value
+    uint32_t w[NW][8];             // w[j][i] = bytes 4j..4j+3 of Y_i
+    if constexpr (SMAX <= 8) {
+        const unsigned long long B = 0x0080808080808080ull >> (8 * (8 - s));
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const long long X = __double2ll_rn(scale_pow2(v[i], P - e));   // |X| <= 127*2^(8s-8)
+            const unsigned long long Y = ((unsigned long long)X + B) ^ B;
+            w[0][i] = (uint32_t)Y;
+            w[1][i] = (uint32_t)(Y >> 32);
         }
     } else {
-        double v = ldexp_rn(x, P - e);                 // |v| < 2^127
-        __int128 X;
-        double av = fabs(v);
-        if (av < 9223372036854775808.0) {
-            X = (__int128)__double2ll_rn(v);
-        } else {                                       // integer >= 2^63: mant * 2^q
-            uint64_t bits = (uint64_t)__double_as_longlong(v);
-            int q = (int)((bits >> 52) & 0x7ff) - 1075;
-            __int128 mant = (__int128)((bits & kFracMask) | (1ull << 52));
-            X = mant << q;
-            if (bits >> 63) X = -X;
-        }
-        __int128 bofs = 0;
-        for (int p = 0; p < s - 1; ++p) bofs |= (__int128)0x80 << (8 * p);
-        __int128 Z = X + bofs;
+        unsigned __int128 B = 0;
+        for (int q = 0; q < s - 1; ++q) B |= (unsigned __int128)0x80 << (8 * q);
 #pragma unroll
-        for (int t = 0; t < SMAX; ++t) {
-            if (t < s) {
-                int p = s - 1 - t;
-                int d = (t == 0) ? (int)(Z >> (8 * p)) : (int)((Z >> (8 * p)) & 0xff) - 128;
-                dw.w[t][wi] |= ((uint32_t)d & 0xffu) << sh_i;
+        for (int i = 0; i < 8; ++i) {
+            const double x = scale_pow2(v[i], P - e);                          // |x| < 2^127
+            __int128 X;
+            if (fabs(x) < 9223372036854775808.0) {
+                X = (__int128)__double2ll_rn(x);
+            } else {                                                            // integer mant * 2^q
+                const uint64_t bits = (uint64_t)__double_as_longlong(x);
+                const int q = (int)((bits >> 52) & 0x7ff) - 1075;
+                X = (__int128)((bits & kFracMask) | (1ull << 52)) << q;
+                if (bits >> 63) X = -X;
+            }
+            const unsigned __int128 Y = ((unsigned __int128)X + B) ^ B;
+#pragma unroll
+            for (int j = 0; j < NW; ++j) w[j][i] = (uint32_t)(Y >> (32 * j));
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+        uint32_t lo[4], hi[4];   // slice word halves for byte positions q = 4j .. 4j+3
+        transpose4x4(w[j][0], w[j][1], w[j][2], w[j][3], lo[0], lo[1], lo[2], lo[3]);
+        transpose4x4(w[j][4], w[j][5], w[j][6], w[j][7], hi[0], hi[1], hi[2], hi[3]);
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+            const int q = 4 * j + qq;
+            if (q < s) {
+                const int64_t off = (int64_t)(s - 1 - q) * blk;
+                const uint2 val = make_uint2(lo[qq], hi[qq]);
+                *reinterpret_cast<uint2 *>(dst0 + off) = val;
+                if (dst1) *reinterpret_cast<uint2 *>(dst1 + off) = val;
             }
         }
     }
 }
 
-template <int SMAX>
-__device__ __forceinline__ void store_digits(const SplitParams &p, int64_t b, int64_t R,
-                                             int64_t Cchunk, const DigitWords<SMAX> &dw) {
-    const int64_t tile = R / p.tile_h;
-    const int64_t rr = R % p.tile_h;
-    const int64_t kb = Cchunk >> 1;
-    const int64_t cc = Cchunk & 1;
-    const int64_t blk = (int64_t)p.tile_h * 32;   // bytes of one (slice, k-block) block
-    int8_t *dst = p.out + (((b * p.tiles + tile) * p.KB + kb) * p.s) * blk + (rr >> 3) * 256 +
-                  cc * 128 + (rr & 7) * 16;
-#pragma unroll
-    for (int t = 0; t < SMAX; ++t) {
-        if (t < p.s) {
-            uint4 v = make_uint4(dw.w[t][0], dw.w[t][1], dw.w[t][2], dw.w[t][3]);
-            *reinterpret_cast<uint4 *>(dst + t * blk) = v;
+// address of the 8-byte half hh of 16-byte chunk C of output row R, slice 1
+__device__ __forceinline__ int8_t *slice_addr(const SplitParams &p, int64_t b, int64_t R, int64_t C, int hh) {
+    const int64_t tile = R / p.tile_h, rr = R % p.tile_h, kb = C >> 1, cc = C & 1;
+    const int64_t blk = (int64_t)p.tile_h * 32;
+    return p.out + (((b * p.tiles + tile) * p.KB + kb) * p.s) * blk + (rr >> 3) * 256 + cc * 128 +
+           (rr & 7) * 16 + hh * 8;
+}
+
+// Fused K1 (exponent scan + slicing).  One CTA owns 8 consecutive rows of the
+// split view (8 rows x 16 B = one canonical core matrix per chunk and slice):
+//   pass 1: per-row max |x| (IEEE bit patterns) -> exponent (R3), 127-rule;
+//   pass 2: re-read the (now L2-resident) 8-row slab; one work item = (row,
+//           8-value half chunk, target), digits (R4), 8-byte stores: 16
+//           consecutive threads write one whole 128-B core matrix per slice.
+// RCONTIG: consecutive rows are adjacent in memory (rs == 1), else each row
+// is contiguous along l.
+template <int SMAX, bool RCONTIG>
+__global__ void __launch_bounds__(256) k_split(const SplitParams p) {
+    __shared__ uint64_t s_max[8][33];
+    __shared__ uint32_t s_nf[8][33];
+    __shared__ int32_t s_e[8];
+    const int tid = threadIdx.x;
+    const int64_t b = blockIdx.y;
+    const int64_t r0 = (int64_t)blockIdx.x * 8;
+    const void *base = p.mode == SPLIT_REAL
+                           ? (const void *)(reinterpret_cast<const double *>(p.X) + b * p.bstride)
+                           : (const void *)(reinterpret_cast<const double2 *>(p.X) + b * p.bstride);
+    {   // ---------------- pass 1: exponents (4 independent loads in flight per thread)
+        const int row = RCONTIG ? (tid & 7) : (tid >> 5);
+        const int slot = RCONTIG ? (tid >> 3) : (tid & 31);
+        const int64_t r = r0 + row;
+        uint64_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+        uint32_t nf = 0;
+        if (r < p.rows) {
+            int64_t l = slot;
+            for (; l + 96 < p.k; l += 128) {
+                const uint64_t u0 = mag_bits(p, base, r * p.rs + l * p.ls);
+                const uint64_t u1 = mag_bits(p, base, r * p.rs + (l + 32) * p.ls);
+                const uint64_t u2 = mag_bits(p, base, r * p.rs + (l + 64) * p.ls);
+                const uint64_t u3 = mag_bits(p, base, r * p.rs + (l + 96) * p.ls);
+                nf |= (u0 >= kExpInf) | (u1 >= kExpInf) | (u2 >= kExpInf) | (u3 >= kExpInf);
+                m0 = (u0 < kExpInf && u0 > m0) ? u0 : m0;
+                m1 = (u1 < kExpInf && u1 > m1) ? u1 : m1;
+                m2 = (u2 < kExpInf && u2 > m2) ? u2 : m2;
+                m3 = (u3 < kExpInf && u3 > m3) ? u3 : m3;
+            }
+            for (; l < p.k; l += 32) {
+                const uint64_t u = mag_bits(p, base, r * p.rs + l * p.ls);
+                nf |= (u >= kExpInf);
+                m0 = (u < kExpInf && u > m0) ? u : m0;
+            }
         }
+        m0 = m0 > m1 ? m0 : m1;
+        m2 = m2 > m3 ? m2 : m3;
+        s_max[row][slot] = m0 > m2 ? m0 : m2;
+        s_nf[row][slot] = nf;
+        __syncthreads();
+        if (tid < 8) {
+            uint64_t mm = 0;
+            uint32_t nn = 0;
+            for (int q = 0; q < 32; ++q) {
+                const uint64_t o = s_max[tid][q];
+                mm = o > mm ? o : mm;
+                nn |= s_nf[tid][q];
+            }
+            int32_t e = 0;
+            if (r0 + tid < p.rows) {
+                reduce_and_store(p, b, r0 + tid, mm, nn);
+                e = nn ? kNonFinite : exponent_from_maxbits(mm);
+            }
+            s_e[tid] = e;
+        }
+        __syncthreads();
     }
-}
-
-template <int SMAX>
-__device__ __forceinline__ void zero_words(DigitWords<SMAX> &dw) {
-#pragma unroll
-    for (int t = 0; t < SMAX; ++t)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) dw.w[t][q] = 0;
-}
-
-// Phase 2.  Thread = (input row r, 16-wide chunk c of the input depth).
-// block (64, 4): x -> row (coalesced when rows are contiguous, and 8
-// consecutive rows write one contiguous 128-B core matrix), y -> chunk.
-template <int SMAX>
-__global__ void __launch_bounds__(256) k_slice(const SplitParams p) {
-    const int64_t b = blockIdx.z;
-    const int64_t r = (int64_t)blockIdx.x * 64 + threadIdx.x;
-    const int64_t c = (int64_t)blockIdx.y * 4 + threadIdx.y;
+    // ---------------- pass 2: digits
     const bool four_m = (p.mode == SPLIT_A4M || p.mode == SPLIT_B4M);
-    const int64_t nchunks = four_m ? (p.kh >> 4) : (p.KB * 2);
-    if (r >= p.rows_grid || c >= nchunks) return;
-
-    const bool row_ok = r < p.rows;
-    int32_t e = 0;
-    if (row_ok) e = p.exps[b * p.rows_out + (p.mode == SPLIT_B4M ? 2 * r : r)];
-    const bool live = row_ok && e != kNonFinite;
-    const int64_t l0 = c * 16;
-    DigitWords<SMAX> dw;
-
-    if (p.mode == SPLIT_REAL) {
-        const double *base = reinterpret_cast<const double *>(p.X) + b * p.bstride + r * p.rs;
-        double x[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            int64_t l = l0 + i;
-            x[i] = (live && l < p.k) ? __ldg(base + l * p.ls) : 0.0;
+    const int64_t nhalf = 2 * (four_m ? (p.kh >> 4) : (p.KB * 2));   // 8-value units per row
+    const int ntgt = p.mode == SPLIT_A4M ? 2 : (p.mode == SPLIT_B4M ? 3 : 1);
+    const int64_t c2off = p.kh >> 4;
+    for (int64_t item = tid; item < 8 * nhalf * ntgt; item += blockDim.x) {
+        const int row = (int)(item & 7);
+        const int64_t rest = item >> 3;
+        const int64_t h = rest % nhalf;
+        const int tgt = (int)(rest / nhalf);
+        const int64_t c = h >> 1;
+        const int hh = (int)(h & 1);
+        const int64_t r = r0 + row;
+        const int32_t e = s_e[row];
+        const bool live = (r < p.rows) && (e != kNonFinite);
+        const int64_t l0 = c * 16 + hh * 8;
+        double v[8];
+        int comp = 0;
+        bool neg = false;
+        switch (p.mode) {
+            case SPLIT_REAL: comp = 0; break;
+            case SPLIT_RE: comp = 1; break;
+            case SPLIT_IM: comp = 2; break;
+            case SPLIT_SUM: comp = 3; break;
+            case SPLIT_A4M: comp = tgt == 0 ? 1 : 2; break;
+            default: comp = tgt == 0 ? 1 : 2; neg = (tgt == 2); break;
         }
-        zero_words(dw);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) put_digits<SMAX>(dw, i, x[i], e, p.s);
-        store_digits<SMAX>(p, b, r, c, dw);
-        return;
-    }
-
-    const double2 *base = reinterpret_cast<const double2 *>(p.X) + b * p.bstride + r * p.rs;
-    double re[16], im[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        int64_t l = l0 + i;
-        double2 v = (live && l < p.k) ? __ldg(base + l * p.ls) : make_double2(0.0, 0.0);
-        re[i] = v.x;
-        im[i] = p.conj ? -v.y : v.y;
-    }
-    if (p.mode == SPLIT_RE || p.mode == SPLIT_IM || p.mode == SPLIT_SUM) {
-        zero_words(dw);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            double x = p.mode == SPLIT_RE ? re[i] : (p.mode == SPLIT_IM ? im[i] : __dadd_rn(re[i], im[i]));
-            put_digits<SMAX>(dw, i, x, e, p.s);
+        load8(p, base, r, l0, comp, neg, live, v);
+        int8_t *d0, *d1 = nullptr;
+        if (p.mode == SPLIT_B4M) {            // 2r = [Re | -Im], 2r+1 = [Im | Re] (R9)
+            if (tgt == 0) {
+                d0 = slice_addr(p, b, 2 * r, c, hh);
+                d1 = slice_addr(p, b, 2 * r + 1, c + c2off, hh);
+            } else if (tgt == 1) {
+                d0 = slice_addr(p, b, 2 * r + 1, c, hh);
+            } else {
+                d0 = slice_addr(p, b, 2 * r, c + c2off, hh);
+            }
+        } else if (p.mode == SPLIT_A4M) {     // row r = [Re | Im]
+            d0 = slice_addr(p, b, r, tgt == 0 ? c : c + c2off, hh);
+        } else {
+            d0 = slice_addr(p, b, r, c, hh);
         }
-        store_digits<SMAX>(p, b, r, c, dw);
-        return;
+        digits_store8<SMAX>(v, e, p.s, d0, d1, (int64_t)p.tile_h * 32);
     }
-    const int64_t c2 = (p.kh >> 4) + c;   // chunk index in the second half
-    if (p.mode == SPLIT_A4M) {            // row r = [Re | Im]
-        zero_words(dw);
+}
+
+// ------------------------------------------------------------------
+// Shared-memory staged variant (the production K1): the 8-row slab is copied
+// into SMEM with cp.async (deep memory-level parallelism, no registers), both
+// passes read SMEM.  Rows longer than one window (KW elements) are streamed in
+// windows: pass 1 scans all windows, pass 2 reloads them (second read hits L2).
+__device__ __forceinline__ void cp_async8(void *smem, const void *g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32_split(smem)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void *smem, const void *g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32_split(smem)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+template <int SMAX, bool RCONTIG, bool CPLX>
+__global__ void __launch_bounds__(256) k_split_sm(const SplitParams p, int KW) {
+    extern __shared__ __align__(16) uint8_t sbuf[];
+    __shared__ uint64_t s_max[8][33];
+    __shared__ uint32_t s_nf[8][33];
+    __shared__ int32_t s_e[8];
+    using Elem = typename std::conditional<CPLX, double2, double>::type;
+    constexpr int ES = sizeof(Elem);
+    const int ld = KW + (16 / ES);                 // padded row stride (elements) against bank conflicts
+    Elem *slab = reinterpret_cast<Elem *>(sbuf);
+    const int tid = threadIdx.x;
+    const int64_t b = blockIdx.y;
+    const int64_t r0 = (int64_t)blockIdx.x * 8;
+    const Elem *X = reinterpret_cast<const Elem *>(p.X) + b * p.bstride;
+    const bool four_m = (p.mode == SPLIT_A4M || p.mode == SPLIT_B4M);
+    const int64_t kpad = four_m ? p.kh : p.KB * 32;  // input depth covered by output chunks
+    const int64_t nwin = (kpad + KW - 1) / KW;
+    const int nrows = (int)min((int64_t)8, max((int64_t)0, p.rows - r0));
+
+    auto load_window = [&](int64_t w0) {
+        const int64_t wlen = min((int64_t)KW, p.k - w0);   // valid elements in this window
+        if (wlen <= 0) return;
+        if (RCONTIG) {   // 8 rows adjacent in memory for each l
+            for (int64_t idx = tid; idx < 8 * wlen; idx += blockDim.x) {
+                const int row = (int)(idx & 7);
+                const int64_t l = idx >> 3;
+                if (row < nrows) {
+                    const Elem *g = X + (r0 + row) * p.rs + (w0 + l) * p.ls;
+                    if (CPLX) cp_async16(slab + row * ld + l, g);
+                    else cp_async8(slab + row * ld + l, g);
+                }
+            }
+        } else {         // each row contiguous along l
+            for (int64_t idx = tid; idx < 8 * wlen; idx += blockDim.x) {
+                const int row = (int)(idx / wlen);
+                const int64_t l = idx - row * wlen;
+                if (row < nrows) {
+                    const Elem *g = X + (r0 + row) * p.rs + (w0 + l) * p.ls;
+                    if (CPLX) cp_async16(slab + row * ld + l, g);
+                    else cp_async8(slab + row * ld + l, g);
+                }
+            }
+        }
+        cp_async_wait_all();
+    };
+    auto mag = [&](const Elem &x) -> uint64_t {
+        if constexpr (!CPLX) {
+            return (uint64_t)__double_as_longlong(x) & kAbsMask;
+        } else {
+            const double re = x.x, im = p.conj ? -x.y : x.y;
+            const uint64_t ur = (uint64_t)__double_as_longlong(re) & kAbsMask;
+            const uint64_t ui = (uint64_t)__double_as_longlong(im) & kAbsMask;
+            switch (p.mode) {
+                case SPLIT_RE: return ur;
+                case SPLIT_IM: return ui;
+                case SPLIT_SUM: return (uint64_t)__double_as_longlong(__dadd_rn(re, im)) & kAbsMask;
+                default: return ur > ui ? ur : ui;
+            }
+        }
+    };
+
+    // ---------------- pass 1: exponents
+    {
+        const int row = tid >> 5, lane = tid & 31;
+        uint64_t m = 0;
+        uint32_t nf = 0;
+        for (int64_t w = 0; w < nwin; ++w) {
+            const int64_t w0 = w * KW;
+            load_window(w0);
+            __syncthreads();
+            const int64_t wlen = min((int64_t)KW, p.k - w0);
+            if (row < nrows)
+                for (int64_t l = lane; l < wlen; l += 32) {
+                    const uint64_t u = mag(slab[row * ld + l]);
+                    nf |= (u >= kExpInf);
+                    m = (u < kExpInf && u > m) ? u : m;
+                }
+            __syncthreads();
+        }
 #pragma unroll
-        for (int i = 0; i < 16; ++i) put_digits<SMAX>(dw, i, re[i], e, p.s);
-        store_digits<SMAX>(p, b, r, c, dw);
-        zero_words(dw);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) put_digits<SMAX>(dw, i, im[i], e, p.s);
-        store_digits<SMAX>(p, b, r, c2, dw);
-        return;
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t om = __shfl_xor_sync(0xffffffffu, m, o);
+            m = om > m ? om : m;
+            nf |= __shfl_xor_sync(0xffffffffu, nf, o);
+        }
+        if (lane == 0) {
+            int32_t e = 0;
+            if (row < nrows) {
+                reduce_and_store(p, b, r0 + row, m, nf);
+                e = nf ? kNonFinite : exponent_from_maxbits(m);
+            }
+            s_e[row] = e;
+        }
+        __syncthreads();
     }
-    // SPLIT_B4M: column 2r = [Re ; -Im], column 2r+1 = [Im ; Re]; -Im is split
-    // from the negated FP64 value (balanced digits are not sign-symmetric, R9).
-    zero_words(dw);
+    // ---------------- pass 2: digits (window already resident when nwin == 1)
+    const int ntgt = p.mode == SPLIT_A4M ? 2 : (p.mode == SPLIT_B4M ? 3 : 1);
+    const int64_t c2off = p.kh >> 4;
+    const int64_t blk = (int64_t)p.tile_h * 32;
+    for (int64_t w = 0; w < nwin; ++w) {
+        const int64_t w0 = w * KW;
+        if (nwin > 1) {
+            __syncthreads();
+            load_window(w0);
+            __syncthreads();
+        }
+        const int64_t wh = (min((int64_t)KW, kpad - w0) + 7) / 8;   // 8-value units in window
+        for (int64_t item = tid; item < 8 * wh * ntgt; item += blockDim.x) {
+            const int row = (int)(item & 7);
+            const int64_t rest = item >> 3;
+            const int64_t h = rest % wh;
+            const int tgt = (int)(rest / wh);
+            const int64_t lw = h * 8;                  // offset in window
+            const int64_t l0 = w0 + lw;                // input depth index
+            const int64_t c = l0 >> 4;
+            const int hh = (int)((l0 >> 3) & 1);
+            const int32_t e = s_e[row];
+            const bool live = (row < nrows) && (e != kNonFinite);
+            double v[8];
+            int comp = 0;
+            bool neg = false;
+            switch (p.mode) {
+                case SPLIT_REAL: comp = 0; break;
+                case SPLIT_RE: comp = 1; break;
+                case SPLIT_IM: comp = 2; break;
+                case SPLIT_SUM: comp = 3; break;
+                case SPLIT_A4M: comp = tgt == 0 ? 1 : 2; break;
+                default: comp = tgt == 0 ? 1 : 2; neg = (tgt == 2); break;
+            }
 #pragma unroll
-    for (int i = 0; i < 16; ++i) put_digits<SMAX>(dw, i, re[i], e, p.s);
-    store_digits<SMAX>(p, b, 2 * r, c, dw);
-    store_digits<SMAX>(p, b, 2 * r + 1, c2, dw);
-    zero_words(dw);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) put_digits<SMAX>(dw, i, im[i], e, p.s);
-    store_digits<SMAX>(p, b, 2 * r + 1, c, dw);
-    zero_words(dw);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) put_digits<SMAX>(dw, i, -im[i], e, p.s);
-    store_digits<SMAX>(p, b, 2 * r, c2, dw);
+            for (int i = 0; i < 8; ++i) {
+                double val = 0.0;
+                if (live && l0 + i < p.k) {
+                    const Elem x = slab[row * ld + lw + i];
+                    if constexpr (!CPLX) {
+                        val = x;
+                    } else {
+                        const double im = p.conj ? -x.y : x.y;
+                        val = comp == 1 ? x.x : (comp == 2 ? im : __dadd_rn(x.x, im));
+                    }
+                }
+                v[i] = neg ? -val : val;
+            }
+            const int64_t r = r0 + row;
+            int8_t *d0, *d1 = nullptr;
+            if (p.mode == SPLIT_B4M) {            // 2r = [Re | -Im], 2r+1 = [Im | Re] (R9)
+                if (tgt == 0) {
+                    d0 = slice_addr(p, b, 2 * r, c, hh);
+                    d1 = slice_addr(p, b, 2 * r + 1, c + c2off, hh);
+                } else if (tgt == 1) {
+                    d0 = slice_addr(p, b, 2 * r + 1, c, hh);
+                } else {
+                    d0 = slice_addr(p, b, 2 * r, c + c2off, hh);
+                }
+            } else if (p.mode == SPLIT_A4M) {     // row r = [Re | Im]
+                d0 = slice_addr(p, b, r, tgt == 0 ? c : c + c2off, hh);
+            } else {
+                d0 = slice_addr(p, b, r, c, hh);
+            }
+            digits_store8<SMAX>(v, e, p.s, d0, d1, blk);
+        }
+    }
 }
 
 }  // namespace ozk

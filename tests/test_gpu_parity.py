@@ -283,4 +283,4 @@ def test_stats_closed_forms():
     # s(s+1)/2 per real product, x4 (4M), x3 (3M)
     assert st["int8_gemm_equiv"] == 15 + 4 * 15 + 3 * 15
     assert st["dgemm_calls"] == 1 and st["zgemm_calls"] == 1 and st["zgemm3m_calls"] == 1
-    assert st["kernel_launches"] == 5 + 5 + (3 * 5 + 1)
+    assert st["kernel_launches"] == 3 + 3 + (3 * 3 + 1)
