@@ -428,6 +428,7 @@ __global__ void __launch_bounds__(256) k_split_sm(const SplitParams p, int KW) {
     const int ntgt = p.mode == SPLIT_A4M ? 2 : (p.mode == SPLIT_B4M ? 3 : 1);
     const int64_t c2off = p.kh >> 4;
     const int64_t blk = (int64_t)p.tile_h * 32;
+    const int64_t kb_stride = (int64_t)p.s * blk;          // bytes between k-blocks of one row tile
     for (int64_t w = 0; w < nwin; ++w) {
         const int64_t w0 = w * KW;
         if (nwin > 1) {
@@ -435,62 +436,76 @@ __global__ void __launch_bounds__(256) k_split_sm(const SplitParams p, int KW) {
             load_window(w0);
             __syncthreads();
         }
-        const int64_t wh = (min((int64_t)KW, kpad - w0) + 7) / 8;   // 8-value units in window
-        for (int64_t item = tid; item < 8 * wh * ntgt; item += blockDim.x) {
-            const int row = (int)(item & 7);
-            const int64_t rest = item >> 3;
-            const int64_t h = rest % wh;
-            const int tgt = (int)(rest / wh);
-            const int64_t lw = h * 8;                  // offset in window
-            const int64_t l0 = w0 + lw;                // input depth index
-            const int64_t c = l0 >> 4;
-            const int hh = (int)((l0 >> 3) & 1);
-            const int32_t e = s_e[row];
-            const bool live = (row < nrows) && (e != kNonFinite);
-            double v[8];
+        const int wh = (int)((min((int64_t)KW, kpad - w0) + 7) / 8);   // 8-value units in window
+        for (int tgt = 0; tgt < ntgt; ++tgt) {
+            // uniform per target: value component, sign, output rows and chunk offset
             int comp = 0;
             bool neg = false;
+            int rmul = 1, radd = 0;            // output row = rmul * r + radd
+            int64_t cadd = 0;                  // output chunk offset
+            int rmul1 = 0, radd1 = 0;          // second destination (B4M Re -> 2r+1, second half)
+            bool two = false;
             switch (p.mode) {
                 case SPLIT_REAL: comp = 0; break;
                 case SPLIT_RE: comp = 1; break;
                 case SPLIT_IM: comp = 2; break;
                 case SPLIT_SUM: comp = 3; break;
-                case SPLIT_A4M: comp = tgt == 0 ? 1 : 2; break;
-                default: comp = tgt == 0 ? 1 : 2; neg = (tgt == 2); break;
+                case SPLIT_A4M: comp = tgt == 0 ? 1 : 2; cadd = tgt == 0 ? 0 : c2off; break;
+                default:   // SPLIT_B4M: 2r = [Re | -Im], 2r+1 = [Im | Re] (R9)
+                    rmul = 2;
+                    if (tgt == 0) { comp = 1; radd = 0; two = true; rmul1 = 2; radd1 = 1; }
+                    else if (tgt == 1) { comp = 2; radd = 1; }
+                    else { comp = 2; neg = true; radd = 0; cadd = c2off; }
+                    break;
             }
+            for (int item = tid; item < 8 * wh; item += blockDim.x) {
+                const int row = item & 7;
+                const int h = item >> 3;
+                const int lw = h * 8;                      // offset in window
+                const int64_t l0 = w0 + lw;                // input depth index
+                const int32_t e = s_e[row];
+                const bool live = (row < nrows) && (e != kNonFinite);
+                double v[8];
+                const Elem *src = slab + row * ld + lw;
+                if (live && l0 + 8 <= p.k) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                double val = 0.0;
-                if (live && l0 + i < p.k) {
-                    const Elem x = slab[row * ld + lw + i];
-                    if constexpr (!CPLX) {
-                        val = x;
-                    } else {
-                        const double im = p.conj ? -x.y : x.y;
-                        val = comp == 1 ? x.x : (comp == 2 ? im : __dadd_rn(x.x, im));
+                    for (int i = 0; i < 8; ++i) {
+                        const Elem x = src[i];
+                        double val;
+                        if constexpr (!CPLX) {
+                            val = x;
+                        } else {
+                            const double im = p.conj ? -x.y : x.y;
+                            val = comp == 1 ? x.x : (comp == 2 ? im : __dadd_rn(x.x, im));
+                        }
+                        v[i] = neg ? -val : val;
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        double val = 0.0;
+                        if (live && l0 + i < p.k) {
+                            const Elem x = src[i];
+                            if constexpr (!CPLX) {
+                                val = x;
+                            } else {
+                                const double im = p.conj ? -x.y : x.y;
+                                val = comp == 1 ? x.x : (comp == 2 ? im : __dadd_rn(x.x, im));
+                            }
+                        }
+                        v[i] = neg ? -val : val;
                     }
                 }
-                v[i] = neg ? -val : val;
+                const int64_t r = r0 + row;
+                const int64_t c = (l0 >> 4) + cadd;
+                const int hh = (int)((l0 >> 3) & 1);
+                int8_t *d0 = slice_addr(p, b, rmul * r + radd, c, hh);
+                int8_t *d1 = two ? slice_addr(p, b, rmul1 * r + radd1, (l0 >> 4) + c2off, hh) : nullptr;
+                digits_store8<SMAX>(v, e, p.s, d0, d1, blk);
             }
-            const int64_t r = r0 + row;
-            int8_t *d0, *d1 = nullptr;
-            if (p.mode == SPLIT_B4M) {            // 2r = [Re | -Im], 2r+1 = [Im | Re] (R9)
-                if (tgt == 0) {
-                    d0 = slice_addr(p, b, 2 * r, c, hh);
-                    d1 = slice_addr(p, b, 2 * r + 1, c + c2off, hh);
-                } else if (tgt == 1) {
-                    d0 = slice_addr(p, b, 2 * r + 1, c, hh);
-                } else {
-                    d0 = slice_addr(p, b, 2 * r, c + c2off, hh);
-                }
-            } else if (p.mode == SPLIT_A4M) {     // row r = [Re | Im]
-                d0 = slice_addr(p, b, r, tgt == 0 ? c : c + c2off, hh);
-            } else {
-                d0 = slice_addr(p, b, r, c, hh);
-            }
-            digits_store8<SMAX>(v, e, p.s, d0, d1, blk);
         }
     }
+    (void)kb_stride;
 }
 
 }  // namespace ozk
