@@ -50,6 +50,14 @@ struct GemmParams {
     int64_t ldc, strideC;   // in elements (complex elements for EPI_CPLX4M)
     double alpha_r, alpha_i, beta_r, beta_i;
     int32_t *S_out;         // EPI_LEVELS
+    // K-chunking (reading R8): this launch covers k-blocks [kb_begin, kb_end);
+    // chunk_mode 0 = whole K, 1 = first chunk (W = S), 2 = middle (W += S),
+    // 3 = last (level sum = W + S, then the FP64 combine).  W holds the exact
+    // integer partial level sums in FP64 (< 2^53): W[(L-2)*w_lvl + col*Mp + row].
+    int64_t kb_begin, kb_end;
+    int32_t chunk_mode;
+    double *W;
+    int64_t w_lvl;
     unsigned long long *dbg;   // optional per-CTA role timers (ozaki_debug_timing), null = off
 };
 

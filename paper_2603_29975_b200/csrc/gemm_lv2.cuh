@@ -51,8 +51,9 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
             const int hi = PP.hi[ps], lo = PP.lo[ps], tlo = PP.tlo[ps], n = PP.n[ps];
             const uint32_t abytes = (uint32_t)n * kBlk, bbytes = (uint32_t)n * (kBlk / 2);
             const int kpp = lp.pass[ps].kpp;
-            for (int64_t kb0 = 0; kb0 < p.KB; kb0 += kpp) {
-                const int nk = (int)min((int64_t)kpp, p.KB - kb0);
+            for (int64_t kb0 = p.kb_begin; kb0 < p.kb_end; kb0 += kpp) {
+                const int nk = (int)min((int64_t)kpp, p.kb_end - kb0);
+                const bool kfirst = (kb0 == p.kb_begin);
                 long long w0 = p.dbg ? clock64() : 0;
                 mbar_wait(&full[stage], phase);
                 if (p.dbg) t_full += clock64() - w0;
@@ -62,7 +63,7 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
                     const uint32_t abase = sbase + (uint32_t)kk * (abytes + bbytes);
                     const uint64_t ad0 = dA + (abase >> 4);
                     const uint64_t bd0 = dB + ((abase + abytes) >> 4);
-                    if (kb0 == 0 && kk == 0) {
+                    if (kfirst && kk == 0) {
 #pragma unroll
                         for (int j = 0; j < hi - lo + 1; ++j) {
                             w0 = p.dbg ? clock64() : 0;
@@ -81,7 +82,7 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
                             const int t = t0 + r;
                             if (t <= t1) {
                                 const int u = L - t;
-                                const uint32_t acc = (r == 0) ? (uint32_t)(kb0 != 0 || kk != 0) : 1u;
+                                const uint32_t acc = (r == 0) ? (uint32_t)(!kfirst || kk != 0) : 1u;
                                 mma_i8_pair_elect(tbase + (uint32_t)(j * kLvBN),
                                                   ad0 + (uint64_t)(((t - tlo) * kBlk) >> 4),
                                                   bd0 + (uint64_t)(((u - tlo) * (kBlk / 2)) >> 4), idesc, acc);
@@ -155,8 +156,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 for (int ps = 0; ps < lp.npass; ++ps) {
                     const LvPass pa = lp.pass[ps];
                     const uint32_t abytes = (uint32_t)pa.n * kBlk, bbytes = (uint32_t)pa.n * (kBlk / 2);
-                    for (int64_t kb0 = 0; kb0 < p.KB; kb0 += pa.kpp) {
-                        const int nk = (int)min((int64_t)pa.kpp, p.KB - kb0);
+                    for (int64_t kb0 = p.kb_begin; kb0 < p.kb_end; kb0 += pa.kpp) {
+                        const int nk = (int)min((int64_t)pa.kpp, p.kb_end - kb0);
                         const long long w0 = p.dbg ? clock64() : 0;
                         mbar_wait(&empty[stage], phase ^ 1);
                         if (p.dbg) t_wait += clock64() - w0;
@@ -237,10 +238,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                             }
                             continue;
                         }
+                        if (p.chunk_mode == 0) {
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            acc[g * 32 + i] = __fma_rn(i32_to_f64(v0[i]), sc, acc[g * 32 + i]);
-                            acc[g * 32 + 16 + i] = __fma_rn(i32_to_f64(v1[i]), sc, acc[g * 32 + 16 + i]);
+                            for (int i = 0; i < 16; ++i) {
+                                acc[g * 32 + i] = __fma_rn(i32_to_f64(v0[i]), sc, acc[g * 32 + i]);
+                                acc[g * 32 + 16 + i] = __fma_rn(i32_to_f64(v1[i]), sc, acc[g * 32 + 16 + i]);
+                            }
+                        } else {
+                            // exact partial level sums in FP64 (R8): W (+)= S; last chunk combines W + S
+                            const int64_t c0 = tn * kLvBN + half * 64 + g * 32;
+                            const bool rok = grow < p.Mp;
+                            double *wp = p.W + (int64_t)(L - 2) * p.w_lvl + c0 * p.Mp + grow;
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) {
+                                const double part = i32_to_f64(i < 16 ? v0[i] : v1[i - 16]);
+                                const bool ok = rok && (c0 + i < p.N);
+                                double *q = wp + (int64_t)i * p.Mp;
+                                if (p.chunk_mode == 1) {
+                                    if (ok) *q = part;
+                                } else if (p.chunk_mode == 2) {
+                                    if (ok) *q = __dadd_rn(*q, part);
+                                } else {
+                                    const double lvl = ok ? __dadd_rn(*q, part) : part;   // exact
+                                    acc[g * 32 + i] = __fma_rn(lvl, sc, acc[g * 32 + i]);
+                                }
+                            }
                         }
                     }
                     tc_fence_before();
@@ -250,7 +272,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 if (p.dbg) t_d += clock64() - w1;
             }
             const long long s0 = p.dbg ? clock64() : 0;
-            if constexpr (EPI != EPI_LEVELS) lv_store<EPI>(p, b, grow, e, tn * kLvBN + half * 64, acc);
+            if constexpr (EPI != EPI_LEVELS)
+                if (p.chunk_mode == 0 || p.chunk_mode == 3) lv_store<EPI>(p, b, grow, e, tn * kLvBN + half * 64, acc);
             if (p.dbg) t_s += clock64() - s0;
         }
         if (p.dbg && warp == 2 && lane == 0) {

@@ -168,6 +168,7 @@ struct Plan {
     size_t a_bytes, b_bytes, ea_bytes, fb_bytes;   // per whole batch, 256-B aligned
     int kps, stages;
     size_t smem;
+    bool kchunk_needed;      // s * k_eff > 131071 (reading R8)
     bool lv;                 // level-pass kernels (BN = 128)
     bool pair;               // ... on CTA pairs (k_gemm_lv2, M = 256 per pair)
     int a_tile_h, b_tile_h;  // operand row tiles of the split layout
@@ -229,17 +230,20 @@ int make_plan(Kind kind, int64_t m, int64_t n, int64_t k, int64_t batch, int s, 
         P.kh = 0;
         P.Kp = rup(k, 32);
     }
-    // R8: a level sums (L-1) * k_eff products of magnitude <= 2^14 in INT32.
+    // R8: a level sums (L-1) * k_eff products of magnitude <= 2^14 in INT32; the
+    // pair kernel splits K into chunks that respect this (exact FP64 partials),
+    // the other kernels need the whole K in one INT32 accumulation.
     const int64_t keff = (kind == KIND_4M) ? 2 * k : k;
-    if ((int64_t)s * keff > 131071)
-        return fail(OZAKI_ERR_UNSUPPORTED,
-                    "s*k_eff = %lld exceeds the INT32 level-sum bound 131071 (K-chunking not in "
-                    "this build)",
-                    (long long)((int64_t)s * keff));
+    P.kchunk_needed = (int64_t)s * keff > 131071;
     P.KB = P.Kp / 32;
     const int kc = kernel_choice();
     P.lv = (s <= 12) && kc >= 1;
     P.pair = P.lv && kc == 2;
+    if (P.kchunk_needed && !P.pair)
+        return fail(OZAKI_ERR_UNSUPPORTED,
+                    "s*k_eff = %lld exceeds the INT32 level-sum bound 131071 and K-chunking needs the "
+                    "CTA-pair kernel (s <= 12)",
+                    (long long)((int64_t)s * keff));
     if (P.lv) P.BN = kLvBN;
     P.a_tile_h = kBM;
     P.b_tile_h = P.pair ? kLvBN / 2 : P.BN;
@@ -456,7 +460,8 @@ int rows_map(CUtensorMap *m, const void *base, size_t bytes, uint32_t box_rows) 
 }
 
 template <int EPI>
-int launch_gemm_lv2(const Plan &P, const GemmParams &gp, DevState *dev, cudaStream_t st) {
+int launch_gemm_lv2(const Plan &P, const GemmParams &gp, size_t a_avail, size_t b_avail, DevState *dev,
+                    cudaStream_t st) {
     static std::atomic<size_t> done{0};
     if (done.load() < P.smem) {
         CUDA_TRY(cudaFuncSetAttribute(k_gemm_lv2<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -470,10 +475,10 @@ int launch_gemm_lv2(const Plan &P, const GemmParams &gp, DevState *dev, cudaStre
     P2.lv.stage_bytes = P.stage_bytes;
     for (int q = 0; q < P.npass; ++q) {
         P2.lv.pass[q] = P.pass[q];
-        if (int rc = rows_map(&P2.tmA[q], gp.A, P.a_bytes, (uint32_t)P.pass[q].n * (kBlk / 256))) return rc;
-        if (int rc = rows_map(&P2.tmB[q], gp.B, P.b_bytes, (uint32_t)P.pass[q].n * (kBlk / 512))) return rc;
+        if (int rc = rows_map(&P2.tmA[q], gp.A, a_avail, (uint32_t)P.pass[q].n * (kBlk / 256))) return rc;
+        if (int rc = rows_map(&P2.tmB[q], gp.B, b_avail, (uint32_t)P.pass[q].n * (kBlk / 512))) return rc;
     }
-    const int64_t tiles = P.batch * P.tiles_m * P.tiles_n;
+    const int64_t tiles = gp.batch * gp.tiles_m * gp.tiles_n;
     const unsigned pairs = (unsigned)std::min<int64_t>(tiles, dev->sms / 2);
     {
         ProfScope ps(st, PH_GEMM);
@@ -496,6 +501,61 @@ int launch_gemm_t(const Plan &P, const GemmParams &gp, DevState *dev, cudaStream
     CUDA_TRY(cudaGetLastError());
     g_stats.launches += 1;
     return 0;
+}
+
+// K-chunked GEMM (reading R8): per batch entry, per column panel (W <= 2 GiB),
+// per K chunk (s * chunk_K' <= 131071): chunk 1 writes the exact INT32 partial
+// level sums into W (FP64, exact), middle chunks add, the last chunk adds its
+// own partial in the epilogue and runs the normal FP64 combine + alpha/beta.
+int launch_gemm_chunked(const Plan &P, const GemmParams &g0, int epi, int64_t kc_env, DevState *dev,
+                        cudaStream_t st) {
+    const int s = P.s;
+    int64_t kbc = 131071 / (32 * (int64_t)s);          // k-blocks per chunk
+    if (kc_env > 0) kbc = std::min<int64_t>(kbc, kc_env);
+    if (kbc < 1) return fail(OZAKI_ERR_UNSUPPORTED, "K chunk too small");
+    const int64_t nchunk = (P.KB + kbc - 1) / kbc;
+    const int64_t Np = P.Np, Mp = P.Mp;
+    int64_t panel = ((int64_t)2 << 30) / ((int64_t)s * Mp * 8);
+    panel = std::max<int64_t>(kLvBN, panel / kLvBN * kLvBN);
+    panel = std::min<int64_t>(panel, P.tiles_n * kLvBN);
+    if (const char *pe = getenv("OZAKI_PANEL_COLS"))     // test hook: force narrow panels
+        panel = std::max<int64_t>(kLvBN, std::min<int64_t>(panel, atoll(pe) / kLvBN * kLvBN));
+    double *W = nullptr;
+    const size_t wbytes = (size_t)s * Mp * panel * sizeof(double);
+    cudaError_t e = cudaMallocAsync((void **)&W, wbytes, st);
+    if (e != cudaSuccess) return fail(OZAKI_ERR_ALLOC, "K-chunk workspace (%zu B): %s", wbytes, cudaGetErrorString(e));
+    const size_t a_tile_bytes = (size_t)P.KB * s * kBlk;            // one 128-row A tile
+    const size_t b_tile_bytes = (size_t)P.KB * s * (kBlk / 2);      // one 64-row B tile
+    int rc = 0;
+    for (int64_t b = 0; b < P.batch && !rc; ++b) {
+        for (int64_t j0 = 0; j0 < Np && !rc; j0 += panel) {
+            const int64_t nw = std::min<int64_t>(panel, Np - j0);
+            GemmParams gp = g0;
+            gp.batch = 1;
+            gp.A = g0.A + (size_t)b * (2 * P.tiles_m) * a_tile_bytes;
+            gp.B = g0.B + ((size_t)b * (2 * P.tiles_n) + 2 * (j0 / kLvBN)) * b_tile_bytes;
+            gp.ea = g0.ea + b * Mp;
+            gp.fb = g0.fb + b * Np + j0;
+            gp.N = nw;
+            gp.tiles_n = (nw + kLvBN - 1) / kLvBN;
+            gp.C = (epi == EPI_CPLX4M) ? g0.C + 2 * (b * g0.strideC + (j0 / 2) * g0.ldc)
+                                       : g0.C + b * g0.strideC + j0 * g0.ldc;
+            gp.W = W;
+            gp.w_lvl = Mp * nw;
+            const size_t a_avail = (size_t)P.a_bytes - (size_t)(gp.A - g0.A);
+            const size_t b_avail = (size_t)P.b_bytes - (size_t)(gp.B - g0.B);
+            for (int64_t c = 0; c < nchunk && !rc; ++c) {
+                gp.kb_begin = c * kbc;
+                gp.kb_end = std::min<int64_t>(P.KB, (c + 1) * kbc);
+                gp.chunk_mode = (nchunk == 1) ? 0 : (c == 0 ? 1 : (c + 1 == nchunk ? 3 : 2));
+                rc = (epi == EPI_REAL) ? launch_gemm_lv2<EPI_REAL>(P, gp, a_avail, b_avail, dev, st)
+                                       : launch_gemm_lv2<EPI_CPLX4M>(P, gp, a_avail, b_avail, dev, st);
+                if (!rc && nchunk > 1) g_stats.chunks += 1;
+            }
+        }
+    }
+    cudaFreeAsync(W, st);
+    return rc;
 }
 
 int launch_gemm(const Plan &P, int epi, const int8_t *sa, const int8_t *sb, const int32_t *ea,
@@ -525,6 +585,11 @@ int launch_gemm(const Plan &P, int epi, const int8_t *sa, const int8_t *sb, cons
     gp.beta_r = be[0];
     gp.beta_i = be[1];
     gp.S_out = S_out;
+    gp.kb_begin = 0;
+    gp.kb_end = P.KB;
+    gp.chunk_mode = 0;
+    gp.W = nullptr;
+    gp.w_lvl = 0;
     if (g_dbg_on.load()) {
         if (!g_dbg) {
             CUDA_TRY(cudaMalloc(&g_dbg, sizeof(unsigned long long) * DBG_NSLOT));
@@ -533,9 +598,13 @@ int launch_gemm(const Plan &P, int epi, const int8_t *sa, const int8_t *sb, cons
         gp.dbg = g_dbg;
     }
     if (P.pair) {
-        if (epi == EPI_REAL) return launch_gemm_lv2<EPI_REAL>(P, gp, dev, st);
-        if (epi == EPI_CPLX4M) return launch_gemm_lv2<EPI_CPLX4M>(P, gp, dev, st);
-        return launch_gemm_lv2<EPI_LEVELS>(P, gp, dev, st);
+        const char *ev = getenv("OZAKI_KCHUNK_KB");   // test hook: force a small K chunk
+        const int64_t kc_env = ev ? atoll(ev) : 0;
+        if ((P.kchunk_needed || kc_env > 0) && epi != EPI_LEVELS)
+            return launch_gemm_chunked(P, gp, epi, kc_env, dev, st);
+        if (epi == EPI_REAL) return launch_gemm_lv2<EPI_REAL>(P, gp, P.a_bytes, P.b_bytes, dev, st);
+        if (epi == EPI_CPLX4M) return launch_gemm_lv2<EPI_CPLX4M>(P, gp, P.a_bytes, P.b_bytes, dev, st);
+        return launch_gemm_lv2<EPI_LEVELS>(P, gp, P.a_bytes, P.b_bytes, dev, st);
     }
     if (P.lv) {
         if (epi == EPI_REAL) return launch_gemm_lv<EPI_REAL>(P, gp, dev, st);

@@ -210,13 +210,54 @@ def test_dgemm_edge_cases(orc):
         assert same(host(Cd), want)
 
 
-def test_dgemm_rejects_kchunk_overflow():
-    A = dev(np.zeros((8, 20000)))
-    B = dev(np.zeros((20000, 8)))
-    C = dev(np.zeros((8, 8)))
-    with pytest.raises(oz.OzakiError) as ei:
-        oz.dgemm("N", "N", 1.0, A, B, 0.0, C, 8)
-    assert ei.value.code == 4
+def test_dgemm_large_k_chunked(orc):
+    """s * k > 131071 (reading R8): K is chunked with exact partial level sums."""
+    s = 8
+    A = synth.uniform(40, 17000, seed=11)
+    B = synth.spread(17000, 36, seed=12, phi=1.0)
+    want = orc.dgemm("N", "N", 1.0, A, B, 0.0, None, s)
+    C = dev(np.zeros((40, 36)))
+    oz.reset_stats()
+    oz.dgemm("N", "N", 1.0, dev(A), dev(B), 0.0, C, s)
+    assert same(host(C), want)
+    assert oz.get_stats()["k_chunks"] == 2
+
+
+@pytest.fixture
+def force_chunks(monkeypatch):
+    monkeypatch.setenv("OZAKI_KCHUNK_KB", "3")
+    monkeypatch.setenv("OZAKI_PANEL_COLS", "128")
+    yield
+
+
+@pytest.mark.parametrize("s", [3, 7, 9])
+def test_forced_kchunks_and_panels_bitexact(orc, force_chunks, s):
+    """Multi-chunk (first / middle / last) and multi-panel paths on small shapes."""
+    m, n, k = 150, 300, 260          # KB = 9 -> 3 chunks; 3 panels of 128 columns
+    A = synth.spread(m, k, seed=s, phi=1.5)
+    B = synth.uniform(k, n, seed=s + 1)
+    C = synth.uniform(m, n, seed=s + 2)
+    want = orc.dgemm("N", "N", -0.75, A, B, 0.5, C, s)
+    Cd = dev(C)
+    oz.dgemm("N", "N", -0.75, dev(A), dev(B), 0.5, Cd, s)
+    assert same(host(Cd), want)
+    Z = synth.kkr(70, 90, seed=s, gamma=1.0)
+    W = synth.kkr(90, 130, seed=s + 5, gamma=1.0)
+    for method, fn in (("4m", oz.zgemm), ("3m", oz.zgemm3m)):
+        Zc = dev(np.zeros((70, 130), np.complex128))
+        fn("N", "C", 1.0 + 0.5j, dev(Z), dev(np.conj(W.T).copy()), 0.0, Zc, s)
+        assert same(host(Zc), orc.zgemm("N", "N", 1.0 + 0.5j, Z, W, 0.0, None, s, method))
+    # batched entries through the chunked driver
+    batch = 3
+    As = [synth.uniform(m, k, seed=20 + i) for i in range(batch)]
+    Bs = [synth.uniform(k, n, seed=30 + i) for i in range(batch)]
+    tA = torch.stack([dev(a) for a in As]).transpose(1, 2).contiguous().transpose(1, 2)
+    tB = torch.stack([dev(b) for b in Bs]).transpose(1, 2).contiguous().transpose(1, 2)
+    tC = torch.zeros((batch, n, m), dtype=torch.float64, device="cuda").transpose(1, 2)
+    oz.dgemm_strided_batched("N", "N", 1.0, tA, tB, 0.0, tC, s)
+    got = host(tC)
+    for i in range(batch):
+        assert same(got[i], orc.dgemm("N", "N", 1.0, As[i], Bs[i], 0.0, None, s))
 
 
 # ---------------------------------------------------------------- ZGEMM
@@ -284,3 +325,37 @@ def test_stats_closed_forms():
     assert st["int8_gemm_equiv"] == 15 + 4 * 15 + 3 * 15
     assert st["dgemm_calls"] == 1 and st["zgemm_calls"] == 1 and st["zgemm3m_calls"] == 1
     assert st["kernel_launches"] == 3 + 3 + (3 * 3 + 1)
+
+
+_VARIANT_SNIPPET = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import oracle, synth, paper_2603_29975_b200 as oz
+def dev(x): return oz.colmajor(torch.from_numpy(np.asfortranarray(x)).cuda())
+bad = 0
+for s in {slices}:
+    A = synth.spread(130, 75, seed=s, phi=1.5); B = synth.uniform(75, 140, seed=s + 1)
+    C = synth.uniform(130, 140, seed=s + 2)
+    Cd = dev(C); oz.dgemm("N", "T", 1.5, dev(A), dev(B.T.copy()), -0.5, Cd, s)
+    bad += int(not (Cd.cpu().numpy() == oracle.dgemm("N", "T", 1.5, A, B.T.copy(), -0.5, C, s)).all())
+    Z = synth.kkr(66, 50, seed=s); Wm = synth.kkr(50, 70, seed=s + 3)
+    for method, fn in (("4m", oz.zgemm), ("3m", oz.zgemm3m)):
+        Zc = dev(np.zeros((66, 70), np.complex128)); fn("N", "N", 1j, dev(Z), dev(Wm), 0.0, Zc, s)
+        w = oracle.zgemm("N", "N", 1j, Z, Wm, 0.0, None, s, method); g = Zc.cpu().numpy()
+        bad += int(not ((g.real == w.real).all() and (g.imag == w.imag).all()))
+print("BAD", bad)
+"""
+
+
+@pytest.mark.parametrize("variant,slices", [("lv1", [2, 7, 12]), ("flat", [1, 6, 13, 16])])
+def test_kernel_variants_bitexact(variant, slices):
+    """The 1-CTA level-pass kernel and the flat kernel (OZAKI_KERNEL) are bit-exact too."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, OZAKI_KERNEL=variant)
+    res = subprocess.run([sys.executable, "-c", _VARIANT_SNIPPET.format(root=root, slices=slices)],
+                         env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    assert "BAD 0" in res.stdout, res.stdout + res.stderr[-2000:]
