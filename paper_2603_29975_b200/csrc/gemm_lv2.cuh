@@ -103,7 +103,10 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
     }
 }
 
-template <int EPI>
+// CHUNK (compile time, reading R8): 0 = whole K in one INT32 accumulation;
+// 1 = first/middle K chunk (W = S or W += S, nothing stored to C);
+// 2 = last K chunk (level sum = W + S, then the FP64 combine and store).
+template <int EPI, int CHUNK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     k_gemm_lv2(const __grid_constant__ Lv2Params P2) {
     const LvParams &lp = P2.lv;
@@ -238,30 +241,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                             }
                             continue;
                         }
-                        if (p.chunk_mode == 0) {
+                        if constexpr (CHUNK == 0) {
 #pragma unroll
                             for (int i = 0; i < 16; ++i) {
                                 acc[g * 32 + i] = __fma_rn(i32_to_f64(v0[i]), sc, acc[g * 32 + i]);
                                 acc[g * 32 + 16 + i] = __fma_rn(i32_to_f64(v1[i]), sc, acc[g * 32 + 16 + i]);
                             }
+                        } else if constexpr (CHUNK == 1) {
+                            // first/middle K chunk (R8): exact partial level sums W (+)= S
+                            const int64_t c0 = tn * kLvBN + half * 64 + g * 32;
+                            if (grow < p.Mp) {
+                                double *wp = p.W + (int64_t)(L - 2) * p.w_lvl + c0 * p.Mp + grow;
+#pragma unroll 4
+                                for (int i = 0; i < 32; ++i) {
+                                    if (c0 + i >= p.N) break;
+                                    const double part = i32_to_f64(i < 16 ? v0[i] : v1[i - 16]);
+                                    double *q = wp + (int64_t)i * p.Mp;
+                                    *q = (p.chunk_mode == 1) ? part : __dadd_rn(*q, part);
+                                }
+                            }
                         } else {
-                            // exact partial level sums in FP64 (R8): W (+)= S; last chunk combines W + S
+                            // last K chunk: level sum = W + S (exact), then the FP64 combine
                             const int64_t c0 = tn * kLvBN + half * 64 + g * 32;
                             const bool rok = grow < p.Mp;
-                            double *wp = p.W + (int64_t)(L - 2) * p.w_lvl + c0 * p.Mp + grow;
+                            const double *wp = p.W + (int64_t)(L - 2) * p.w_lvl + c0 * p.Mp + grow;
 #pragma unroll
                             for (int i = 0; i < 32; ++i) {
-                                const double part = i32_to_f64(i < 16 ? v0[i] : v1[i - 16]);
-                                const bool ok = rok && (c0 + i < p.N);
-                                double *q = wp + (int64_t)i * p.Mp;
-                                if (p.chunk_mode == 1) {
-                                    if (ok) *q = part;
-                                } else if (p.chunk_mode == 2) {
-                                    if (ok) *q = __dadd_rn(*q, part);
-                                } else {
-                                    const double lvl = ok ? __dadd_rn(*q, part) : part;   // exact
-                                    acc[g * 32 + i] = __fma_rn(lvl, sc, acc[g * 32 + i]);
-                                }
+                                double lvl = i32_to_f64(i < 16 ? v0[i] : v1[i - 16]);
+                                if (rok && c0 + i < p.N) lvl = __dadd_rn(wp[(int64_t)i * p.Mp], lvl);
+                                acc[g * 32 + i] = __fma_rn(lvl, sc, acc[g * 32 + i]);
                             }
                         }
                     }
@@ -272,8 +280,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 if (p.dbg) t_d += clock64() - w1;
             }
             const long long s0 = p.dbg ? clock64() : 0;
-            if constexpr (EPI != EPI_LEVELS)
-                if (p.chunk_mode == 0 || p.chunk_mode == 3) lv_store<EPI>(p, b, grow, e, tn * kLvBN + half * 64, acc);
+            if constexpr (EPI != EPI_LEVELS && CHUNK != 1) lv_store<EPI>(p, b, grow, e, tn * kLvBN + half * 64, acc);
             if (p.dbg) t_s += clock64() - s0;
         }
         if (p.dbg && warp == 2 && lane == 0) {

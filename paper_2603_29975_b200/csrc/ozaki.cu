@@ -459,12 +459,12 @@ int rows_map(CUtensorMap *m, const void *base, size_t bytes, uint32_t box_rows) 
     return 0;
 }
 
-template <int EPI>
+template <int EPI, int CHUNK = 0>
 int launch_gemm_lv2(const Plan &P, const GemmParams &gp, size_t a_avail, size_t b_avail, DevState *dev,
                     cudaStream_t st) {
     static std::atomic<size_t> done{0};
     if (done.load() < P.smem) {
-        CUDA_TRY(cudaFuncSetAttribute(k_gemm_lv2<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CUDA_TRY(cudaFuncSetAttribute(k_gemm_lv2<EPI, CHUNK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)P.smem));
         done.store(P.smem);
     }
@@ -482,7 +482,7 @@ int launch_gemm_lv2(const Plan &P, const GemmParams &gp, size_t a_avail, size_t 
     const unsigned pairs = (unsigned)std::min<int64_t>(tiles, dev->sms / 2);
     {
         ProfScope ps(st, PH_GEMM);
-        k_gemm_lv2<EPI><<<2 * pairs, kGemmThreads, P.smem, st>>>(P2);
+        k_gemm_lv2<EPI, CHUNK><<<2 * pairs, kGemmThreads, P.smem, st>>>(P2);
     }
     CUDA_TRY(cudaGetLastError());
     g_stats.launches += 1;
@@ -548,8 +548,14 @@ int launch_gemm_chunked(const Plan &P, const GemmParams &g0, int epi, int64_t kc
                 gp.kb_begin = c * kbc;
                 gp.kb_end = std::min<int64_t>(P.KB, (c + 1) * kbc);
                 gp.chunk_mode = (nchunk == 1) ? 0 : (c == 0 ? 1 : (c + 1 == nchunk ? 3 : 2));
-                rc = (epi == EPI_REAL) ? launch_gemm_lv2<EPI_REAL>(P, gp, a_avail, b_avail, dev, st)
-                                       : launch_gemm_lv2<EPI_CPLX4M>(P, gp, a_avail, b_avail, dev, st);
+                if (gp.chunk_mode == 0)
+                    rc = (epi == EPI_REAL) ? launch_gemm_lv2<EPI_REAL, 0>(P, gp, a_avail, b_avail, dev, st)
+                                           : launch_gemm_lv2<EPI_CPLX4M, 0>(P, gp, a_avail, b_avail, dev, st);
+                else if (gp.chunk_mode != 3)   // partial chunks store nothing to C: one kernel
+                    rc = launch_gemm_lv2<EPI_REAL, 1>(P, gp, a_avail, b_avail, dev, st);
+                else
+                    rc = (epi == EPI_REAL) ? launch_gemm_lv2<EPI_REAL, 2>(P, gp, a_avail, b_avail, dev, st)
+                                           : launch_gemm_lv2<EPI_CPLX4M, 2>(P, gp, a_avail, b_avail, dev, st);
                 if (!rc && nchunk > 1) g_stats.chunks += 1;
             }
         }
