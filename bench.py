@@ -279,20 +279,16 @@ def run_ours(args):
 
 
 def e2e_leg(torch, oz, fn, A_h, B_h, batch, n, s, device, args, world):
+    """End to end through the public API with HOST (pinned) buffers: the library's
+    offload path pipelines H2D copies, the emulated ZGEMM and D2H copies."""
     import torch.distributed as dist
     stream = torch.cuda.current_stream()
     Ap = torch.from_numpy(np.ascontiguousarray(np.transpose(A_h, (0, 2, 1)))).pin_memory()
     Bp = torch.from_numpy(np.ascontiguousarray(np.transpose(B_h, (0, 2, 1)))).pin_memory()
     Cp = torch.empty((batch, n, n), dtype=torch.complex128).pin_memory()
-    Ad = torch.empty_like(Ap, device=device)
-    Bd = torch.empty_like(Bp, device=device)
-    Cd = torch.empty((batch, n, n), dtype=torch.complex128, device=device)
 
     def step():
-        Ad.copy_(Ap, non_blocking=True)
-        Bd.copy_(Bp, non_blocking=True)
-        fn("N", "N", 1.0, Ad.transpose(1, 2), Bd.transpose(1, 2), 0.0, Cd.transpose(1, 2), s)
-        Cp.copy_(Cd, non_blocking=True)
+        fn("N", "N", 1.0, Ap.transpose(1, 2), Bp.transpose(1, 2), 0.0, Cp.transpose(1, 2), s)
 
     for _ in range(2):
         step()
@@ -314,7 +310,8 @@ def e2e_leg(torch, oz, fn, A_h, B_h, batch, n, s, device, args, world):
     return {"value": round(val, 3), "unit": "TFLOP/s (FP64-equivalent)", "ms_per_step": round(ms, 3),
             "h2d_bytes_per_step": int(Ap.numel() * 16 + Bp.numel() * 16),
             "d2h_bytes_per_step": int(Cp.numel() * 16),
-            "path": "pinned host -> device copy, ozaki_zgemm_strided_batched, device -> pinned host"}
+            "path": "ozaki_zgemm_strided_batched on pinned HOST tensors (library offload: chunked, "
+                    "H2D / GEMM / D2H overlapped on 3 streams)"}
 
 
 def accuracy_leg(torch, oz, A_h, B_h, C, s, method):

@@ -26,6 +26,11 @@
  *   - A, B, C (and strided-batched bases) are DEVICE pointers owned by the
  *     caller (e.g. torch tensors).  A and B are read-only; C must not alias A
  *     or B.  When beta == 0, C is never read (NaN-safe).
+ *   - Offload: if A, B and C are all HOST pointers (pinned or pageable), the
+ *     call stages batch chunks through device memory on internal streams with
+ *     H2D copy / GEMM / D2H copy overlapped, and returns once C is written
+ *     back (synchronous for the host; the caller's stream is ordered after it).
+ *     Mixed host/device operands return OZAKI_ERR_UNSUPPORTED.
  *   - transa/transb in {'N','n','T','t','C','c'}; for real routines 'C' == 'T'.
  *   - num_slices in [1, 16].
  *   - Calls enqueue work on the calling thread's stream (ozaki_set_stream,

@@ -137,9 +137,10 @@ def _ld(x) -> int:
 
 
 def _cuda(x, dtype, name):
+    """Operands are CUDA tensors, or CPU tensors (host offload: all of A, B, C)."""
     import torch
-    if not isinstance(x, torch.Tensor) or not x.is_cuda:
-        raise TypeError(f"{name} must be a CUDA torch tensor")
+    if not isinstance(x, torch.Tensor):
+        raise TypeError(f"{name} must be a torch tensor")
     if x.dtype != dtype:
         raise TypeError(f"{name} must be {dtype}, got {x.dtype}")
     return x
@@ -147,6 +148,8 @@ def _cuda(x, dtype, name):
 
 def _bind_stream(stream=None):
     import torch
+    if stream is None and not torch.cuda.is_available():
+        raise RuntimeError("no CUDA device: the Ozaki library has no CPU path")
     s = stream if stream is not None else torch.cuda.current_stream()
     lib().ozaki_set_stream(ctypes.c_void_p(s.cuda_stream))
 

@@ -711,6 +711,137 @@ int validate(const Call &c) {
     return 0;
 }
 
+int run(const Call &c0);
+
+// ------------------------------------------------------------ host offload
+// A, B, C in host memory (pinned or pageable): the library stages batch
+// chunks through device buffers on three internal streams so H2D copies,
+// the emulated GEMM and D2H copies overlap (chunk i+1 in, i computing, i-1
+// out), and returns when C is back in host memory.  This is the analogue of
+// the automatic BLAS offload the paper relies on.
+enum PtrKind { PTR_DEVICE = 0, PTR_HOST = 1, PTR_BAD = 2 };
+
+PtrKind ptr_kind(const void *p) {
+    if (!p) return PTR_DEVICE;   // only reached for empty operands
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return PTR_HOST;
+    }
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return PTR_DEVICE;
+    return PTR_HOST;   // cudaMemoryTypeHost (pinned) or cudaMemoryTypeUnregistered (pageable)
+}
+
+struct OffloadCtx {
+    bool init = false;
+    cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+    cudaEvent_t in_done[2] = {}, comp_done[2] = {}, out_done[2] = {}, start = nullptr;
+    char *buf[2] = {nullptr, nullptr};   // staging buffer sets, cached across calls
+    size_t cap = 0;
+};
+thread_local OffloadCtx t_off[kMaxDev];
+
+int offload_ctx(OffloadCtx **out) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    OffloadCtx &o = t_off[dev];
+    if (!o.init) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&o.h2d, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&o.comp, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&o.d2h, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            CUDA_TRY(cudaEventCreateWithFlags(&o.in_done[i], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&o.comp_done[i], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&o.out_done[i], cudaEventDisableTiming));
+        }
+        CUDA_TRY(cudaEventCreateWithFlags(&o.start, cudaEventDisableTiming));
+        o.init = true;
+    }
+    *out = &o;
+    return 0;
+}
+
+int run_offload(const Call &c) {
+    const size_t es = (c.kind == KIND_REAL) ? 8 : 16;
+    const int64_t ar = c.ta == 'N' ? c.m : c.k, ac = c.ta == 'N' ? c.k : c.m;
+    const int64_t br = c.tb == 'N' ? c.k : c.n, bc = c.tb == 'N' ? c.n : c.k;
+    // element span of one entry (leading dimensions kept as given)
+    const int64_t spanA = (ac - 1) * c.lda + ar, spanB = (bc - 1) * c.ldb + br, spanC = (c.n - 1) * c.ldc + c.m;
+    const bool readC = !(c.be[0] == 0.0 && c.be[1] == 0.0);
+    const size_t per_entry = (size_t)(spanA + spanB + spanC) * es;
+    int64_t cb = (int64_t)((64ull << 20) / std::max<size_t>(per_entry, 1));   // ~64 MB per chunk
+    cb = std::max<int64_t>(1, std::min<int64_t>(cb, (c.batch + 1) / 2 > 0 ? (c.batch + 1) / 2 : 1));
+    const int64_t nchunk = (c.batch + cb - 1) / cb;
+    OffloadCtx *o = nullptr;
+    if (int rc = offload_ctx(&o)) return rc;
+    cudaStream_t user = t_stream;
+    const size_t set_bytes = (size_t)cb * per_entry;
+    if (o->cap < set_bytes) {   // grow the cached staging sets (never freed per call: cudaFree syncs)
+        CUDA_TRY(cudaStreamSynchronize(o->d2h));
+        for (int i = 0; i < 2; ++i) {
+            if (o->buf[i]) cudaFree(o->buf[i]);
+            o->buf[i] = nullptr;
+        }
+        o->cap = 0;
+        for (int i = 0; i < 2; ++i) {
+            cudaError_t e = cudaMalloc(&o->buf[i], set_bytes);
+            if (e != cudaSuccess) return fail(OZAKI_ERR_ALLOC, "offload staging (%zu B): %s", set_bytes, cudaGetErrorString(e));
+        }
+        o->cap = set_bytes;
+    }
+    char *buf[2] = {o->buf[0], o->buf[1]};
+    CUDA_TRY(cudaEventRecord(o->start, user));
+    CUDA_TRY(cudaStreamWaitEvent(o->h2d, o->start, 0));
+    int rc = 0;
+    const char *hA = (const char *)c.A, *hB = (const char *)c.B;
+    char *hC = (char *)c.C;
+    for (int64_t ch = 0; ch < nchunk && !rc; ++ch) {
+        const int set = (int)(ch & 1);
+        const int64_t b0 = ch * cb, nb = std::min<int64_t>(cb, c.batch - b0);
+        double *dA = (double *)buf[set];
+        double *dB = (double *)(buf[set] + (size_t)cb * spanA * es);
+        double *dC = (double *)(buf[set] + (size_t)cb * (spanA + spanB) * es);
+        if (ch >= 2) CUDA_TRY(cudaStreamWaitEvent(o->h2d, o->out_done[set], 0));   // buffer set reuse
+        for (int64_t i = 0; i < nb; ++i) {
+            CUDA_TRY(cudaMemcpyAsync((char *)dA + (size_t)i * spanA * es, hA + (size_t)(b0 + i) * c.sA * es,
+                                     (size_t)spanA * es, cudaMemcpyHostToDevice, o->h2d));
+            CUDA_TRY(cudaMemcpyAsync((char *)dB + (size_t)i * spanB * es, hB + (size_t)(b0 + i) * c.sB * es,
+                                     (size_t)spanB * es, cudaMemcpyHostToDevice, o->h2d));
+            if (readC)
+                CUDA_TRY(cudaMemcpyAsync((char *)dC + (size_t)i * spanC * es, hC + (size_t)(b0 + i) * c.sC * es,
+                                         (size_t)spanC * es, cudaMemcpyHostToDevice, o->h2d));
+        }
+        CUDA_TRY(cudaEventRecord(o->in_done[set], o->h2d));
+        CUDA_TRY(cudaStreamWaitEvent(o->comp, o->in_done[set], 0));
+        Call d = c;
+        d.A = dA;
+        d.B = dB;
+        d.C = dC;
+        d.sA = spanA;
+        d.sB = spanB;
+        d.sC = spanC;
+        d.batch = nb;
+        d.batched = true;
+        t_stream = o->comp;
+        rc = run(d);
+        t_stream = user;
+        if (rc) break;
+        CUDA_TRY(cudaEventRecord(o->comp_done[set], o->comp));
+        CUDA_TRY(cudaStreamWaitEvent(o->d2h, o->comp_done[set], 0));
+        for (int64_t i = 0; i < nb; ++i)
+            CUDA_TRY(cudaMemcpyAsync(hC + (size_t)(b0 + i) * c.sC * es, (char *)dC + (size_t)i * spanC * es,
+                                     (size_t)spanC * es, cudaMemcpyDeviceToHost, o->d2h));
+        CUDA_TRY(cudaEventRecord(o->out_done[set], o->d2h));
+    }
+    // the caller's stream observes completion; host memory is final on return
+    cudaEventRecord(o->start, o->d2h);
+    cudaStreamWaitEvent(user, o->start, 0);
+    cudaError_t e = cudaStreamSynchronize(o->d2h);
+    if (!rc && e != cudaSuccess) rc = fail(OZAKI_ERR_CUDA, "offload: %s", cudaGetErrorString(e));
+    return rc;
+}
+
 int run(const Call &c0) {
     t_err.clear();
     if (int rc = validate(c0)) return rc;
@@ -724,6 +855,17 @@ int run(const Call &c0) {
     if (c.m == 0 || c.n == 0 || c.batch == 0) return 0;
     DevState *dev = nullptr;
     if (int rc = device_state(&dev)) return rc;
+    if (!c.S_out) {   // host operands -> pipelined offload (all three must be host)
+        const bool readsAB = !(c.al[0] == 0.0 && c.al[1] == 0.0) && c.k > 0;
+        const PtrKind kc = ptr_kind(c.C);
+        const PtrKind ka = readsAB ? ptr_kind(c.A) : kc, kb = readsAB ? ptr_kind(c.B) : kc;
+        if (ka == PTR_HOST || kb == PTR_HOST || kc == PTR_HOST) {
+            if (!(ka == PTR_HOST && kb == PTR_HOST && kc == PTR_HOST))
+                return fail(OZAKI_ERR_UNSUPPORTED, "A, B, C must all be device or all be host pointers");
+            if (!readsAB) return fail(OZAKI_ERR_UNSUPPORTED, "host-pointer quick return not supported");
+            return run_offload(c);
+        }
+    }
     cudaStream_t st = t_stream;
     const size_t es = (c.kind == KIND_REAL) ? 8 : 16;
     const bool cplx = c.kind != KIND_REAL;

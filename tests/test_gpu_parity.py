@@ -359,3 +359,34 @@ def test_kernel_variants_bitexact(variant, slices):
                          env=env, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stderr[-2000:]
     assert "BAD 0" in res.stdout, res.stdout + res.stderr[-2000:]
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_offload_bitexact(orc, pinned):
+    """Host operands: pipelined H2D / GEMM / D2H inside the library, bit-exact."""
+    batch, m, n, k, s = 7, 90, 70, 60, 7
+    zA = [synth.kkr(m, k, seed=60 + i) for i in range(batch)]
+    zB = [synth.kkr(k, n, seed=70 + i) for i in range(batch)]
+    zC = [synth.uniform(m, n, seed=80 + i, complex_=True) for i in range(batch)]
+
+    def host3(lst):
+        t = torch.from_numpy(np.stack([np.asfortranarray(x).T for x in lst])).contiguous()
+        t = t.pin_memory() if pinned else t
+        return t.transpose(1, 2)      # (batch, rows, cols) column-major per entry, CPU
+
+    for method, fn in (("4m", oz.zgemm_strided_batched), ("3m", oz.zgemm3m_strided_batched)):
+        tC = host3(zC)
+        fn("N", "N", 0.5 - 1j, host3(zA), host3(zB), -0.25, tC, s)
+        got = tC.numpy()
+        for i in range(batch):
+            assert same(got[i], orc.zgemm("N", "N", 0.5 - 1j, zA[i], zB[i], -0.25, zC[i], s, method))
+    # real, non-batched
+    A = synth.uniform(64, 50, seed=1)
+    B = synth.uniform(50, 40, seed=2)
+    C = torch.zeros((40, 64), dtype=torch.float64).t()
+    oz.dgemm("N", "N", 1.0, torch.from_numpy(np.asfortranarray(A)), torch.from_numpy(np.asfortranarray(B)),
+             0.0, C, s)
+    assert same(C.numpy(), orc.dgemm("N", "N", 1.0, A, B, 0.0, None, s))
+    # mixed host/device operands are refused
+    with pytest.raises(oz.OzakiError):
+        oz.dgemm("N", "N", 1.0, dev(A), torch.from_numpy(np.asfortranarray(B)), 0.0, C, s)
