@@ -50,21 +50,21 @@ struct LvParams {
 // columns col0 .. col0+63 held in acc[].  Complex (4M, R9 N-side embedding):
 // columns 2c / 2c+1 are Re / Im of complex column col0/2 + c, so each thread
 // owns whole complex numbers: one 16-byte store, no lane exchange.
-template <int EPI>
+template <int EPI, int NC = 64>
 __device__ __forceinline__ void lv_store(const GemmParams &p, int64_t b, int64_t grow, int32_t e,
                                          int64_t col0, const double *acc) {
     const int lane = threadIdx.x & 31;
-    const int ncol = (grow < p.Mp) ? (int)min((int64_t)64, p.N - col0) : 0;
+    const int ncol = (grow < p.Mp) ? (int)min((int64_t)NC, p.N - col0) : 0;
     // column exponents: lane j holds f of columns col0 + j and col0 + 32 + j
     const int32_t f_lo = (col0 + lane < p.N) ? __ldg(p.fb + b * p.N + col0 + lane) : 0;
-    const int32_t f_hi = (col0 + 32 + lane < p.N) ? __ldg(p.fb + b * p.N + col0 + 32 + lane) : 0;
+    const int32_t f_hi = (NC > 32 && col0 + 32 + lane < p.N) ? __ldg(p.fb + b * p.N + col0 + 32 + lane) : 0;
     const bool beta0 = (p.beta_r == 0.0 && p.beta_i == 0.0);
     const bool enan = (e == kNonFinite);
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);
     if constexpr (EPI == EPI_REAL) {
         double *cp = p.C + b * p.strideC + grow + col0 * p.ldc;
 #pragma unroll
-        for (int j = 0; j < 64; ++j) {
+        for (int j = 0; j < NC; ++j) {
             const int32_t f = __shfl_sync(0xffffffffu, j < 32 ? f_lo : f_hi, j & 31);
             const double P = (enan || f == kNonFinite) ? qnan : scale_pow2(acc[j], e + f - 14);
             if (j < ncol) *cp = beta0 ? __dmul_rn(p.alpha_r, P) : __fma_rn(p.alpha_r, P, __dmul_rn(p.beta_r, *cp));
@@ -73,7 +73,7 @@ __device__ __forceinline__ void lv_store(const GemmParams &p, int64_t b, int64_t
     } else {
         double2 *cp = reinterpret_cast<double2 *>(p.C) + b * p.strideC + grow + (col0 >> 1) * p.ldc;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
+        for (int c = 0; c < NC / 2; ++c) {
             const int32_t f = __shfl_sync(0xffffffffu, c < 16 ? f_lo : f_hi, (2 * c) & 31);
             const bool nan = enan || f == kNonFinite;
             const double Pr = nan ? qnan : scale_pow2(acc[2 * c], e + f - 14);

@@ -22,6 +22,9 @@
 namespace ozk {
 
 constexpr int kMaxPassMaps = 4;
+constexpr int kEpi2 = 16;                       // epilogue warps per CTA (4 per TMEM lane quarter)
+constexpr int kThreads2 = 64 + 32 * kEpi2;      // 576
+constexpr int kNC2 = kLvBN / (kEpi2 / 4);       // 32 columns per epilogue thread
 
 struct Lv2Params {
     LvParams lv;                          // operands / epilogue / pass plan
@@ -107,7 +110,7 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
 // 1 = first/middle K chunk (W = S or W += S, nothing stored to C);
 // 2 = last K chunk (level sum = W + S, then the FP64 combine and store).
 template <int EPI, int CHUNK>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     k_gemm_lv2(const __grid_constant__ Lv2Params P2) {
     const LvParams &lp = P2.lv;
     const GemmParams &p = lp.g;
@@ -132,7 +135,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             mbar_init(&empty[i], 1);
         }
         mbar_init(pass_full, 1);
-        for (int j = 0; j < kSlots; ++j) mbar_init(&slot_empty[j], 2 * kNumEpiWarps);
+        for (int j = 0; j < kSlots; ++j) mbar_init(&slot_empty[j], 2 * kEpi2);
         fence_mbar_init();
         for (int q = 0; q < lp.npass; ++q) {
             tma_prefetch_desc(&P2.tmA[q]);
@@ -197,8 +200,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         // ========================= epilogue (8 warps per CTA, own 128 rows)
         const int ew = warp - 2;
         const int q = warp & 3;
-        const int half = ew >> 2;
-        const uint32_t tl = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(half * 64);
+        const int half = ew >> 2;                    // column group: [half * kNC2, +kNC2)
+        const uint32_t tl = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(half * kNC2);
         uint32_t pphase = 0;
         long long t_w = 0, t_d = 0, t_s = 0;
         uint32_t slot_remote[kSlots];
@@ -209,9 +212,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             decode_tile(p, tile, b, tm, tn);
             const int64_t grow = (2 * tm + rank) * kBM + q * 32 + lane;
             const int32_t e = (grow < p.Mp) ? __ldg(p.ea + b * p.Mp + grow) : 0;
-            double acc[64];
+            double acc[kNC2];
 #pragma unroll
-            for (int j = 0; j < 64; ++j) acc[j] = 0.0;
+            for (int j = 0; j < kNC2; ++j) acc[j] = 0.0;
             for (int ps = 0; ps < lp.npass; ++ps) {
                 const LvPass pa = lp.pass[ps];
                 long long w0 = p.dbg ? clock64() : 0;
@@ -223,53 +226,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 for (int L = pa.hi; L >= pa.lo; --L) {          // ascending significance (R6)
                     const int j = pa.hi - L;
                     const double sc = pow2(-8 * (L - 2));
-#pragma unroll
-                    for (int g = 0; g < 2; ++g) {
-                        uint32_t v0[16], v1[16];
-                        tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + g * 32), v0);
-                        tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + g * 32 + 16), v1);
+                    if constexpr (CHUNK == 0 && EPI != EPI_LEVELS) {
+                        // software-pipelined drain: load 16 columns ahead of the FP64 work
+                        uint32_t va[16], vb[16];
+                        tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN), va);
                         tmem_wait_ld();
-                        if constexpr (EPI == EPI_LEVELS) {
-                            if (b == 0 && grow < p.Mp) {
 #pragma unroll
-                                for (int i = 0; i < 32; ++i) {
-                                    const int64_t gcol = tn * kLvBN + half * 64 + g * 32 + i;
-                                    if (gcol < p.N)
-                                        p.S_out[(int64_t)(L - 2) * p.Mp * p.N + gcol * p.Mp + grow] =
-                                            (int32_t)(i < 16 ? v0[i] : v1[i - 16]);
-                                }
-                            }
-                            continue;
+                        for (int g = 0; g < kNC2 / 16; ++g) {
+                            uint32_t (&cur)[16] = (g & 1) ? vb : va;
+                            uint32_t (&nxt)[16] = (g & 1) ? va : vb;
+                            if (g + 1 < kNC2 / 16) tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + (g + 1) * 16), nxt);
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                acc[g * 16 + i] = __fma_rn(i32_to_f64(cur[i]), sc, acc[g * 16 + i]);
+                            if (g + 1 < kNC2 / 16) tmem_wait_ld();
                         }
-                        if constexpr (CHUNK == 0) {
+                    } else {
 #pragma unroll
-                            for (int i = 0; i < 16; ++i) {
-                                acc[g * 32 + i] = __fma_rn(i32_to_f64(v0[i]), sc, acc[g * 32 + i]);
-                                acc[g * 32 + 16 + i] = __fma_rn(i32_to_f64(v1[i]), sc, acc[g * 32 + 16 + i]);
-                            }
-                        } else if constexpr (CHUNK == 1) {
-                            // first/middle K chunk (R8): exact partial level sums W (+)= S
-                            const int64_t c0 = tn * kLvBN + half * 64 + g * 32;
-                            if (grow < p.Mp) {
-                                double *wp = p.W + (int64_t)(L - 2) * p.w_lvl + c0 * p.Mp + grow;
-#pragma unroll 4
-                                for (int i = 0; i < 32; ++i) {
-                                    if (c0 + i >= p.N) break;
-                                    const double part = i32_to_f64(i < 16 ? v0[i] : v1[i - 16]);
-                                    double *q = wp + (int64_t)i * p.Mp;
-                                    *q = (p.chunk_mode == 1) ? part : __dadd_rn(*q, part);
+                        for (int g = 0; g < kNC2 / 32; ++g) {
+                            uint32_t v0[16], v1[16];
+                            tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + g * 32), v0);
+                            tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + g * 32 + 16), v1);
+                            tmem_wait_ld();
+                            if constexpr (EPI == EPI_LEVELS) {
+                                if (b == 0 && grow < p.Mp) {
+    #pragma unroll
+                                    for (int i = 0; i < 32; ++i) {
+                                        const int64_t gcol = tn * kLvBN + half * kNC2 + g * 32 + i;
+                                        if (gcol < p.N)
+                                            p.S_out[(int64_t)(L - 2) * p.Mp * p.N + gcol * p.Mp + grow] =
+                                                (int32_t)(i < 16 ? v0[i] : v1[i - 16]);
+                                    }
                                 }
+                                continue;
                             }
-                        } else {
-                            // last K chunk: level sum = W + S (exact), then the FP64 combine
-                            const int64_t c0 = tn * kLvBN + half * 64 + g * 32;
-                            const bool rok = grow < p.Mp;
-                            const double *wp = p.W + (int64_t)(L - 2) * p.w_lvl + c0 * p.Mp + grow;
-#pragma unroll
-                            for (int i = 0; i < 32; ++i) {
-                                double lvl = i32_to_f64(i < 16 ? v0[i] : v1[i - 16]);
-                                if (rok && c0 + i < p.N) lvl = __dadd_rn(wp[(int64_t)i * p.Mp], lvl);
-                                acc[g * 32 + i] = __fma_rn(lvl, sc, acc[g * 32 + i]);
+                            if constexpr (CHUNK == 0) {
+    #pragma unroll
+                                for (int i = 0; i < 16; ++i) {
+                                    acc[g * 32 + i] = __fma_rn(i32_to_f64(v0[i]), sc, acc[g * 32 + i]);
+                                    acc[g * 32 + 16 + i] = __fma_rn(i32_to_f64(v1[i]), sc, acc[g * 32 + 16 + i]);
+                                }
+                            } else if constexpr (CHUNK == 1) {
+                                // first/middle K chunk (R8): exact partial level sums W (+)= S
+                                const int64_t c0 = tn * kLvBN + half * kNC2 + g * 32;
+                                if (grow < p.Mp) {
+                                    double *wp = p.W + (int64_t)(L - 2) * p.w_lvl + c0 * p.Mp + grow;
+    #pragma unroll 4
+                                    for (int i = 0; i < 32; ++i) {
+                                        if (c0 + i >= p.N) break;
+                                        const double part = i32_to_f64(i < 16 ? v0[i] : v1[i - 16]);
+                                        double *q = wp + (int64_t)i * p.Mp;
+                                        *q = (p.chunk_mode == 1) ? part : __dadd_rn(*q, part);
+                                    }
+                                }
+                            } else {
+                                // last K chunk: level sum = W + S (exact), then the FP64 combine
+                                const int64_t c0 = tn * kLvBN + half * kNC2 + g * 32;
+                                const bool rok = grow < p.Mp;
+                                const double *wp = p.W + (int64_t)(L - 2) * p.w_lvl + c0 * p.Mp + grow;
+    #pragma unroll
+                                for (int i = 0; i < 32; ++i) {
+                                    double lvl = i32_to_f64(i < 16 ? v0[i] : v1[i - 16]);
+                                    if (rok && c0 + i < p.N) lvl = __dadd_rn(wp[(int64_t)i * p.Mp], lvl);
+                                    acc[g * 32 + i] = __fma_rn(lvl, sc, acc[g * 32 + i]);
+                                }
                             }
                         }
                     }
@@ -280,7 +300,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 if (p.dbg) t_d += clock64() - w1;
             }
             const long long s0 = p.dbg ? clock64() : 0;
-            if constexpr (EPI != EPI_LEVELS && CHUNK != 1) lv_store<EPI>(p, b, grow, e, tn * kLvBN + half * 64, acc);
+            if constexpr (EPI != EPI_LEVELS && CHUNK != 1) lv_store<EPI, kNC2>(p, b, grow, e, tn * kLvBN + half * kNC2, acc);
             if (p.dbg) t_s += clock64() - s0;
         }
         if (p.dbg && warp == 2 && lane == 0) {

@@ -482,7 +482,7 @@ int launch_gemm_lv2(const Plan &P, const GemmParams &gp, size_t a_avail, size_t 
     const unsigned pairs = (unsigned)std::min<int64_t>(tiles, dev->sms / 2);
     {
         ProfScope ps(st, PH_GEMM);
-        k_gemm_lv2<EPI, CHUNK><<<2 * pairs, kGemmThreads, P.smem, st>>>(P2);
+        k_gemm_lv2<EPI, CHUNK><<<2 * pairs, kThreads2, P.smem, st>>>(P2);
     }
     CUDA_TRY(cudaGetLastError());
     g_stats.launches += 1;
