@@ -48,7 +48,138 @@ def parse():
     ap.add_argument("--gamma", type=float, default=3.0)
     ap.add_argument("--no-extras", action="store_true", help="skip sweep / e2e / cpu baseline")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--workload", default="c2x30", choices=["c2x30", "c1", "c2", "c3", "c4", "c5"],
+                    help="c2x30 (default, the headline) or another BASELINE config (see CONFIGS)")
     return ap.parse_args()
+
+
+# The other BASELINE.json configs (parity cases / secondary measurements).
+CONFIGS = {
+    "c1": dict(kind="d", m=64, n=64, k=64, batch=1, fam="uniform", shard="replica",
+               desc="configs[0]: DGEMM 64^3, uniform"),
+    "c2": dict(kind="z", m=512, n=512, k=512, batch=1, fam="kkr", gamma=3.0, shard="replica",
+               desc="configs[1] single block: ZGEMM 512^3 KKR (gamma=3)"),
+    "c3": dict(kind="d", m=8192, n=8192, k=8192, batch=1, fam="uniform", shard="replica",
+               desc="configs[2]: DGEMM 8192^3, uniform"),
+    "c4": dict(kind="z", m=1024, n=1024, k=1024, batch=256, fam="kkr", gamma=1.0, shard="batch",
+               desc="configs[3]: 256 x ZGEMM 1024^3 KKR (gamma=1), batch-sharded across ranks"),
+    "c5": dict(kind="d", m=32768, n=32768, k=4096, batch=1, fam="spread", phi=4.0, shard="columns",
+               desc="configs[4]: DGEMM 32768x32768x4096 spread(phi=4), column slabs + all-gather of C"),
+}
+
+
+def run_config(args):
+    """Secondary workloads: one timed step = the whole GEMM (or this rank's shard of it)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2603_29975_b200 as oz
+    from paper_2603_29975_b200 import dist as zd
+
+    cfg = CONFIGS[args.workload]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    s = args.slices
+    m, n, k, kind = cfg["m"], cfg["n"], cfg["k"], cfg["kind"]
+    batch = args.batch if (cfg["shard"] == "batch" and args.batch != 30) else cfg["batch"]
+    cplx = kind == "z"
+    kw = {x: cfg[x] for x in ("gamma", "phi") if x in cfg}
+
+    def gen(r, c, seed):
+        return synth.make(cfg["fam"], r, c, seed, complex_=cplx, **kw)
+
+    def colmajor_dev(X):
+        return oz.colmajor(torch.from_numpy(np.asfortranarray(X)).to(device))
+
+    if cfg["shard"] == "batch":
+        b0, b1 = zd.batch_shard(batch, rank, world)
+        nb = b1 - b0
+        distinct = 8   # distinct blocks, tiled over the batch (identical GEMM work per entry)
+        As = [colmajor_dev(gen(m, k, 10 + i)) for i in range(distinct)]
+        Bs = [colmajor_dev(gen(k, n, 50 + i)) for i in range(distinct)]
+        A = torch.stack([As[(b0 + i) % distinct] for i in range(nb)]).transpose(1, 2).contiguous().transpose(1, 2)
+        B = torch.stack([Bs[(b0 + i) % distinct] for i in range(nb)]).transpose(1, 2).contiguous().transpose(1, 2)
+        C = torch.zeros((nb, n, m), dtype=A.dtype, device=device).transpose(1, 2)
+        fn = oz.zgemm_strided_batched if cplx else oz.dgemm_strided_batched
+        step = lambda: fn("N", "N", 1.0, A, B, 0.0, C, s)   # noqa: E731
+        units = batch
+    else:
+        A = colmajor_dev(gen(m, k, 1))
+        B = colmajor_dev(gen(k, n, 2))
+        C = torch.zeros((n, m), dtype=A.dtype, device=device).t()
+        fn = oz.zgemm if cplx else oz.dgemm
+        if cfg["shard"] == "columns":
+            gemm = lambda a, b, c: fn("N", "N", 1.0, a, b, 0.0, c, s)   # noqa: E731
+            step = lambda: zd.sharded_gemm_columns(gemm, A, B, C, rank, world)   # noqa: E731
+            units = 1
+        else:
+            step = lambda: fn("N", "N", 1.0, A, B, 0.0, C, s)   # noqa: E731
+            units = world   # replicas
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    oz.profile_enable(True)
+    oz.profile_read()
+    st0 = oz.get_stats()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    clocks.stop()
+    prof = oz.profile_read()
+    oz.profile_enable(False)
+    st1 = oz.get_stats()
+    ms = zd.max_over_ranks(e0.elapsed_time(e1), device) / args.steps
+    flop_unit = (8 if cplx else 2) * m * n * k
+    value = flop_unit * units / (ms * 1e-3) / 1e12
+    gemm = prof["k2_gemm"]
+    gemm_ms = gemm["ms"] / max(1, gemm["launches"])
+    pairs = s * (s + 1) // 2
+    per_launch_units = (nb if cfg["shard"] == "batch" else 1)
+    if cfg["shard"] == "columns":
+        j0, j1 = zd.column_slab(n, rank, world)
+        frac_cols = (j1 - j0) / n
+    else:
+        frac_cols = 1.0
+    alg_ops = 2 * pairs * (4 if cplx else 1) * m * n * k * per_launch_units * frac_cols
+    bf16_burst, _, peak_src = peaks()
+    peak_int8 = bf16_burst * INT8_OVER_BF16
+    achieved = alg_ops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    out = {
+        "metric": "FP64-equiv TFLOP/s (ZGEMM/DGEMM) vs slice count; INT8 pipe util; max rel err",
+        "value": round(value, 3), "unit": f"TFLOP/s (FP64-equivalent, {'8' if cplx else '2'}mnk)",
+        "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "strong" if cfg["shard"] in ("batch", "columns") else "weak",
+        "vs_baseline": None, "dtype": "f64 in/out; int8 tensor-core products; f64 epilogue",
+        "data": f"synthetic (synth.{cfg['fam']}, seeded)",
+        "config": {"workload": cfg["desc"], "slices": s, "m": m, "n": n, "k": k, "batch": batch,
+                   "parallelism": f"{cfg['shard']} x{world}"},
+        "roofline": {"bound": "tensor", "kernel": "slice GEMM (K2+K3)",
+                     "achieved": round(achieved, 2) if achieved else None, "peak": round(peak_int8, 1),
+                     "unit": "TOPS (INT8 dense)", "frac": round(achieved / peak_int8, 4) if achieved else None,
+                     "peak_source": f"{peak_src} bf16 burst x 2", "kernel_ms_per_launch": round(gemm_ms, 5),
+                     "traffic": None},
+        "phase_ms_per_step": {k2: round(v["ms"] / args.steps, 5) for k2, v in prof.items()},
+        "gpu_launches": int(st1["kernel_launches"] - st0["kernel_launches"]),
+        "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def traffic_from_profile(s, method, n, batch, gamma):
@@ -270,6 +401,7 @@ def run_ours(args):
         out["e2e"] = e2e_leg(torch, oz, fn, A_h, B_h, batch, n, s, device, args, world)
         out["accuracy"] = accuracy_leg(torch, oz, A_h, B_h, C, s, args.method)
         out["sweep"] = sweep_leg(torch, oz, A, B, C, batch, n)
+        out["native_fp64"] = native_leg(torch, A, B, batch, n)
     if rank == 0 and not args.no_extras and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(A_h, B_h, s, args.method, n)
     if rank == 0:
@@ -355,6 +487,25 @@ def sweep_leg(torch, oz, A, B, C, batch, n):
     return res
 
 
+def native_leg(torch, A, B, batch, n):
+    """Context only (PAPER.md:119 'native FP64 GEMM'): cuBLAS complex128 batched matmul on the same
+    inputs, TFLOP/s (8mnk per ZGEMM)."""
+    for _ in range(2):
+        torch.bmm(A, B)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    reps = 5
+    e0.record()
+    for _ in range(reps):
+        torch.bmm(A, B)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    return {"value": round(fp64_equiv_flops(batch, n) / (ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
+            "path": "torch.bmm complex128 (cuBLAS native FP64), context only"}
+
+
 def cpu_baseline(A_h, B_h, s, method, n, budget_s=10.0):
     """The oracle on the host cores: whole n^3 ZGEMM entries of the same batch,
     as many as fit in ~budget_s seconds (at least one)."""
@@ -421,6 +572,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload != "c2x30":
+        run_config(args)
     else:
         run_ours(args)
 
