@@ -1,0 +1,25 @@
+"""Small invocations of every kernel path, for compute-sanitizer runs."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import synth
+import paper_2603_29975_b200 as oz
+
+def dev(x):
+    return oz.colmajor(torch.from_numpy(np.asfortranarray(x)).cuda())
+
+A = synth.spread(200, 70, seed=1); B = synth.uniform(70, 150, seed=2)
+C = dev(np.zeros((200, 150)))
+for s in (3, 7, 13):
+    oz.dgemm("N", "T", 1.0, dev(A), dev(B.T.copy()), 0.0, C, s)
+Z = synth.kkr(100, 60, seed=3); W = synth.kkr(60, 90, seed=4)
+Zc = dev(np.zeros((100, 90), np.complex128))
+oz.zgemm("N", "N", 1.0, dev(Z), dev(W), 0.5, Zc, 7)
+oz.zgemm3m("C", "N", 1.0, dev(np.conj(Z.T).copy()), dev(W), 0.0, Zc, 5)
+os.environ["OZAKI_KCHUNK_KB"] = "1"
+oz.dgemm("N", "N", 1.0, dev(A), dev(synth.uniform(70, 150, seed=5)), 0.0, C, 6)
+del os.environ["OZAKI_KCHUNK_KB"]
+oz.debug_split("B", "z", "N", dev(W), 8)
+oz.debug_level_sums("N", "N", dev(A), dev(synth.uniform(70, 150, seed=5)), 4)
+torch.cuda.synchronize()
+print("sanitize_check done")
