@@ -91,38 +91,6 @@ __device__ __forceinline__ void reduce_and_store(const SplitParams &p, int64_t b
 // R4: X = RNE(x 2^(P-e)), P = 8s-1; balanced digits via the offset trick:
 // with Bofs = sum_{p=0}^{s-2} 128*256^p, Z = X + Bofs has plain base-256 bytes
 // (d_t + 128) at positions p = s-t for t >= 2 and d_1 = Z >> 8(s-1).
-// 8 consecutive values of the split view at (r, l0..l0+7): comp 0 real,
-// 1 Re, 2 Im, 3 fl(Re + Im); `neg` flips the sign (the -Im block of 4M).
-// Conjugation applies to Im.
-__device__ __forceinline__ void load8(const SplitParams &p, const void *base, int64_t r, int64_t l0,
-                                      int comp, bool neg, bool live, double (&v)[8]) {
-    if (comp == 0) {
-        const double *x = reinterpret_cast<const double *>(base) + r * p.rs;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int64_t l = l0 + i;
-            v[i] = (live && l < p.k) ? __ldg(x + l * p.ls) : 0.0;
-        }
-        return;
-    }
-    const double2 *x = reinterpret_cast<const double2 *>(base) + r * p.rs;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int64_t l = l0 + i;
-        double val = 0.0;
-        if (live && l < p.k) {
-            if (comp == 1) {
-                val = __ldg(&x[l * p.ls].x);
-            } else {
-                const double im0 = __ldg(&x[l * p.ls].y);
-                const double im = p.conj ? -im0 : im0;
-                val = (comp == 2) ? im : __dadd_rn(__ldg(&x[l * p.ls].x), im);
-            }
-        }
-        v[i] = neg ? -val : val;
-    }
-}
-
 // 4x4 byte transpose: out[q] byte i = in[i] byte q.
 __device__ __forceinline__ void transpose4x4(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                              uint32_t &o0, uint32_t &o1, uint32_t &o2, uint32_t &o3) {
@@ -134,47 +102,10 @@ __device__ __forceinline__ void transpose4x4(uint32_t a0, uint32_t a1, uint32_t 
     o3 = __byte_perm(t2, t3, 0x7632);
 }
 
-// R4 for 8 consecutive values and the s slices of their 8-byte output.
-// X = RNE(x 2^(P-e)); with B = 0x80 in each of the s-1 low bytes,
-// Y = (X + B) XOR B holds every balanced digit as a byte: byte q of Y is the
-// digit of slice t = s - q (q = s-1 is d_1, the most significant).  An 8x8
-// byte transpose (PRMT) turns the 8 values' Y into one 8-byte word per slice,
-// stored at up to two output locations (dst0, dst1; blk = bytes between slices).
-template <int SMAX>
-__device__ __forceinline__ void digits_store8(const double (&v)[8], int32_t e, int s, int8_t *dst0,
-                                              int8_t *dst1, int64_t blk) {
-    const int P = 8 * s - 1;
-    constexpr int NW = SMAX / 4;   // 32-bit words of Y per value
-    uint32_t w[NW][8];             // w[j][i] = bytes 4j..4j+3 of Y_i
-    if constexpr (SMAX <= 8) {
-        const unsigned long long B = 0x0080808080808080ull >> (8 * (8 - s));
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const long long X = __double2ll_rn(scale_pow2(v[i], P - e));   // |X| <= 127*2^(8s-8)
-            const unsigned long long Y = ((unsigned long long)X + B) ^ B;
-            w[0][i] = (uint32_t)Y;
-            w[1][i] = (uint32_t)(Y >> 32);
-        }
-    } else {
-        unsigned __int128 B = 0;
-        for (int q = 0; q < s - 1; ++q) B |= (unsigned __int128)0x80 << (8 * q);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const double x = scale_pow2(v[i], P - e);                          // |x| < 2^127
-            __int128 X;
-            if (fabs(x) < 9223372036854775808.0) {
-                X = (__int128)__double2ll_rn(x);
-            } else {                                                            // integer mant * 2^q
-                const uint64_t bits = (uint64_t)__double_as_longlong(x);
-                const int q = (int)((bits >> 52) & 0x7ff) - 1075;
-                X = (__int128)((bits & kFracMask) | (1ull << 52)) << q;
-                if (bits >> 63) X = -X;
-            }
-            const unsigned __int128 Y = ((unsigned __int128)X + B) ^ B;
-#pragma unroll
-            for (int j = 0; j < NW; ++j) w[j][i] = (uint32_t)(Y >> (32 * j));
-        }
-    }
+// transpose the 8 values' digit words w[j][i] and store one 8-byte word per slice
+template <int NW>
+__device__ __forceinline__ void store_planes(const uint32_t (&w)[NW][8], int s, int8_t *dst0, int8_t *dst1,
+                                             int64_t blk) {
 #pragma unroll
     for (int j = 0; j < NW; ++j) {
         uint32_t lo[4], hi[4];   // slice word halves for byte positions q = 4j .. 4j+3
@@ -193,125 +124,67 @@ __device__ __forceinline__ void digits_store8(const double (&v)[8], int32_t e, i
     }
 }
 
+// R4 for 8 consecutive values and the s slices of their 8-byte output.
+// X = RNE(x 2^(P-e)): x * scale with scale = 2^(P-e) (one exact-or-correctly-
+// rounded DMUL, identical to ldexp) when the power is representable, else
+// ldexp_rn.  With B = 0x80 in each of the s-1 low bytes, Y = (X + B) XOR B
+// holds every balanced digit as a byte (byte q = digit of slice t = s - q);
+// an 8x8 byte transpose (PRMT) gives one 8-byte word per slice.  dst0 / dst1
+// receive the digits of X, dstn (optional) the digits of -X (RNE is sign-
+// symmetric, so -X is exactly the integer of the negated values).
+template <int SMAX>
+__device__ __forceinline__ void digits_store8(const double (&v)[8], double scale, int32_t e, int s,
+                                              int8_t *dst0, int8_t *dst1, int8_t *dstn, int64_t blk) {
+    const int P = 8 * s - 1;
+    constexpr int NW = SMAX / 4;   // 32-bit words of Y per value
+    uint32_t w[NW][8], wn[NW][8];
+    if constexpr (SMAX <= 8) {
+        const unsigned long long B = 0x0080808080808080ull >> (8 * (8 - s));
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const double xs = (scale != 0.0) ? __dmul_rn(v[i], scale) : ldexp_rn(v[i], P - e);
+            const long long X = __double2ll_rn(xs);                     // |X| <= 127*2^(8s-8)
+            const unsigned long long Y = ((unsigned long long)X + B) ^ B;
+            const unsigned long long Yn = ((unsigned long long)(-X) + B) ^ B;
+            w[0][i] = (uint32_t)Y;
+            w[1][i] = (uint32_t)(Y >> 32);
+            wn[0][i] = (uint32_t)Yn;
+            wn[1][i] = (uint32_t)(Yn >> 32);
+        }
+    } else {
+        unsigned __int128 B = 0;
+        for (int q = 0; q < s - 1; ++q) B |= (unsigned __int128)0x80 << (8 * q);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const double x = (scale != 0.0) ? __dmul_rn(v[i], scale) : ldexp_rn(v[i], P - e);   // |x| < 2^127
+            __int128 X;
+            if (fabs(x) < 9223372036854775808.0) {
+                X = (__int128)__double2ll_rn(x);
+            } else {                                                         // integer mant * 2^q
+                const uint64_t bits = (uint64_t)__double_as_longlong(x);
+                const int q = (int)((bits >> 52) & 0x7ff) - 1075;
+                X = (__int128)((bits & kFracMask) | (1ull << 52)) << q;
+                if (bits >> 63) X = -X;
+            }
+            const unsigned __int128 Y = ((unsigned __int128)X + B) ^ B;
+            const unsigned __int128 Yn = ((unsigned __int128)(-X) + B) ^ B;
+#pragma unroll
+            for (int j = 0; j < NW; ++j) {
+                w[j][i] = (uint32_t)(Y >> (32 * j));
+                wn[j][i] = (uint32_t)(Yn >> (32 * j));
+            }
+        }
+    }
+    store_planes<NW>(w, s, dst0, dst1, blk);
+    if (dstn) store_planes<NW>(wn, s, dstn, nullptr, blk);
+}
+
 // address of the 8-byte half hh of 16-byte chunk C of output row R, slice 1
 __device__ __forceinline__ int8_t *slice_addr(const SplitParams &p, int64_t b, int64_t R, int64_t C, int hh) {
     const int64_t tile = R / p.tile_h, rr = R % p.tile_h, kb = C >> 1, cc = C & 1;
     const int64_t blk = (int64_t)p.tile_h * 32;
     return p.out + (((b * p.tiles + tile) * p.KB + kb) * p.s) * blk + (rr >> 3) * 256 + cc * 128 +
            (rr & 7) * 16 + hh * 8;
-}
-
-// Fused K1 (exponent scan + slicing).  One CTA owns 8 consecutive rows of the
-// split view (8 rows x 16 B = one canonical core matrix per chunk and slice):
-//   pass 1: per-row max |x| (IEEE bit patterns) -> exponent (R3), 127-rule;
-//   pass 2: re-read the (now L2-resident) 8-row slab; one work item = (row,
-//           8-value half chunk, target), digits (R4), 8-byte stores: 16
-//           consecutive threads write one whole 128-B core matrix per slice.
-// RCONTIG: consecutive rows are adjacent in memory (rs == 1), else each row
-// is contiguous along l.
-template <int SMAX, bool RCONTIG>
-__global__ void __launch_bounds__(256) k_split(const SplitParams p) {
-    __shared__ uint64_t s_max[8][33];
-    __shared__ uint32_t s_nf[8][33];
-    __shared__ int32_t s_e[8];
-    const int tid = threadIdx.x;
-    const int64_t b = blockIdx.y;
-    const int64_t r0 = (int64_t)blockIdx.x * 8;
-    const void *base = p.mode == SPLIT_REAL
-                           ? (const void *)(reinterpret_cast<const double *>(p.X) + b * p.bstride)
-                           : (const void *)(reinterpret_cast<const double2 *>(p.X) + b * p.bstride);
-    {   // ---------------- pass 1: exponents (4 independent loads in flight per thread)
-        const int row = RCONTIG ? (tid & 7) : (tid >> 5);
-        const int slot = RCONTIG ? (tid >> 3) : (tid & 31);
-        const int64_t r = r0 + row;
-        uint64_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
-        uint32_t nf = 0;
-        if (r < p.rows) {
-            int64_t l = slot;
-            for (; l + 96 < p.k; l += 128) {
-                const uint64_t u0 = mag_bits(p, base, r * p.rs + l * p.ls);
-                const uint64_t u1 = mag_bits(p, base, r * p.rs + (l + 32) * p.ls);
-                const uint64_t u2 = mag_bits(p, base, r * p.rs + (l + 64) * p.ls);
-                const uint64_t u3 = mag_bits(p, base, r * p.rs + (l + 96) * p.ls);
-                nf |= (u0 >= kExpInf) | (u1 >= kExpInf) | (u2 >= kExpInf) | (u3 >= kExpInf);
-                m0 = (u0 < kExpInf && u0 > m0) ? u0 : m0;
-                m1 = (u1 < kExpInf && u1 > m1) ? u1 : m1;
-                m2 = (u2 < kExpInf && u2 > m2) ? u2 : m2;
-                m3 = (u3 < kExpInf && u3 > m3) ? u3 : m3;
-            }
-            for (; l < p.k; l += 32) {
-                const uint64_t u = mag_bits(p, base, r * p.rs + l * p.ls);
-                nf |= (u >= kExpInf);
-                m0 = (u < kExpInf && u > m0) ? u : m0;
-            }
-        }
-        m0 = m0 > m1 ? m0 : m1;
-        m2 = m2 > m3 ? m2 : m3;
-        s_max[row][slot] = m0 > m2 ? m0 : m2;
-        s_nf[row][slot] = nf;
-        __syncthreads();
-        if (tid < 8) {
-            uint64_t mm = 0;
-            uint32_t nn = 0;
-            for (int q = 0; q < 32; ++q) {
-                const uint64_t o = s_max[tid][q];
-                mm = o > mm ? o : mm;
-                nn |= s_nf[tid][q];
-            }
-            int32_t e = 0;
-            if (r0 + tid < p.rows) {
-                reduce_and_store(p, b, r0 + tid, mm, nn);
-                e = nn ? kNonFinite : exponent_from_maxbits(mm);
-            }
-            s_e[tid] = e;
-        }
-        __syncthreads();
-    }
-    // ---------------- pass 2: digits
-    const bool four_m = (p.mode == SPLIT_A4M || p.mode == SPLIT_B4M);
-    const int64_t nhalf = 2 * (four_m ? (p.kh >> 4) : (p.KB * 2));   // 8-value units per row
-    const int ntgt = p.mode == SPLIT_A4M ? 2 : (p.mode == SPLIT_B4M ? 3 : 1);
-    const int64_t c2off = p.kh >> 4;
-    for (int64_t item = tid; item < 8 * nhalf * ntgt; item += blockDim.x) {
-        const int row = (int)(item & 7);
-        const int64_t rest = item >> 3;
-        const int64_t h = rest % nhalf;
-        const int tgt = (int)(rest / nhalf);
-        const int64_t c = h >> 1;
-        const int hh = (int)(h & 1);
-        const int64_t r = r0 + row;
-        const int32_t e = s_e[row];
-        const bool live = (r < p.rows) && (e != kNonFinite);
-        const int64_t l0 = c * 16 + hh * 8;
-        double v[8];
-        int comp = 0;
-        bool neg = false;
-        switch (p.mode) {
-            case SPLIT_REAL: comp = 0; break;
-            case SPLIT_RE: comp = 1; break;
-            case SPLIT_IM: comp = 2; break;
-            case SPLIT_SUM: comp = 3; break;
-            case SPLIT_A4M: comp = tgt == 0 ? 1 : 2; break;
-            default: comp = tgt == 0 ? 1 : 2; neg = (tgt == 2); break;
-        }
-        load8(p, base, r, l0, comp, neg, live, v);
-        int8_t *d0, *d1 = nullptr;
-        if (p.mode == SPLIT_B4M) {            // 2r = [Re | -Im], 2r+1 = [Im | Re] (R9)
-            if (tgt == 0) {
-                d0 = slice_addr(p, b, 2 * r, c, hh);
-                d1 = slice_addr(p, b, 2 * r + 1, c + c2off, hh);
-            } else if (tgt == 1) {
-                d0 = slice_addr(p, b, 2 * r + 1, c, hh);
-            } else {
-                d0 = slice_addr(p, b, 2 * r, c + c2off, hh);
-            }
-        } else if (p.mode == SPLIT_A4M) {     // row r = [Re | Im]
-            d0 = slice_addr(p, b, r, tgt == 0 ? c : c + c2off, hh);
-        } else {
-            d0 = slice_addr(p, b, r, c, hh);
-        }
-        digits_store8<SMAX>(v, e, p.s, d0, d1, (int64_t)p.tile_h * 32);
-    }
 }
 
 // ------------------------------------------------------------------
@@ -335,6 +208,8 @@ __global__ void __launch_bounds__(256) k_split_sm(const SplitParams p, int KW) {
     __shared__ uint64_t s_max[8][33];
     __shared__ uint32_t s_nf[8][33];
     __shared__ int32_t s_e[8];
+    __shared__ double s_scale[8];
+    __shared__ int8_t *s_rowbase[16];      // output row base (tile, row-in-tile part of the address)
     using Elem = typename std::conditional<CPLX, double2, double>::type;
     constexpr int ES = sizeof(Elem);
     const int ld = KW + (16 / ES);                 // padded row stride (elements) against bank conflicts
@@ -347,47 +222,38 @@ __global__ void __launch_bounds__(256) k_split_sm(const SplitParams p, int KW) {
     const int64_t kpad = four_m ? p.kh : p.KB * 32;  // input depth covered by output chunks
     const int64_t nwin = (kpad + KW - 1) / KW;
     const int nrows = (int)min((int64_t)8, max((int64_t)0, p.rows - r0));
+    const int64_t blk = (int64_t)p.tile_h * 32;      // bytes between slices of one (tile, k-block)
+    const int64_t kbs = (int64_t)p.s * blk;          // bytes between k-blocks of one tile
+
+    if (tid < 16) {   // output rows of this block: r0..r0+7 (B4M: 2r0 .. 2r0+15)
+        const int64_t R = (p.mode == SPLIT_B4M ? 2 * r0 : r0) + tid;
+        const int64_t tile = R / p.tile_h, rr = R % p.tile_h;
+        s_rowbase[tid] = p.out + (b * p.tiles + tile) * p.KB * kbs + (rr >> 3) * 256 + (rr & 7) * 16;
+    }
 
     auto load_window = [&](int64_t w0) {
-        const int64_t wlen = min((int64_t)KW, p.k - w0);   // valid elements in this window
+        const int wlen = (int)min((int64_t)KW, p.k - w0);   // valid elements in this window
         if (wlen <= 0) return;
         if (RCONTIG) {   // 8 rows adjacent in memory for each l
-            for (int64_t idx = tid; idx < 8 * wlen; idx += blockDim.x) {
-                const int row = (int)(idx & 7);
-                const int64_t l = idx >> 3;
+            const Elem *g0 = X + r0 * p.rs + w0 * p.ls;
+            for (int idx = tid; idx < 8 * wlen; idx += blockDim.x) {
+                const int row = idx & 7, l = idx >> 3;
                 if (row < nrows) {
-                    const Elem *g = X + (r0 + row) * p.rs + (w0 + l) * p.ls;
+                    const Elem *g = g0 + row + (int64_t)l * p.ls;
                     if (CPLX) cp_async16(slab + row * ld + l, g);
                     else cp_async8(slab + row * ld + l, g);
                 }
             }
         } else {         // each row contiguous along l
-            for (int64_t idx = tid; idx < 8 * wlen; idx += blockDim.x) {
-                const int row = (int)(idx / wlen);
-                const int64_t l = idx - row * wlen;
-                if (row < nrows) {
-                    const Elem *g = X + (r0 + row) * p.rs + (w0 + l) * p.ls;
-                    if (CPLX) cp_async16(slab + row * ld + l, g);
-                    else cp_async8(slab + row * ld + l, g);
+            for (int row = 0; row < nrows; ++row) {
+                const Elem *g = X + (r0 + row) * p.rs + w0;
+                for (int l = tid; l < wlen; l += blockDim.x) {
+                    if (CPLX) cp_async16(slab + row * ld + l, g + l);
+                    else cp_async8(slab + row * ld + l, g + l);
                 }
             }
         }
         cp_async_wait_all();
-    };
-    auto mag = [&](const Elem &x) -> uint64_t {
-        if constexpr (!CPLX) {
-            return (uint64_t)__double_as_longlong(x) & kAbsMask;
-        } else {
-            const double re = x.x, im = p.conj ? -x.y : x.y;
-            const uint64_t ur = (uint64_t)__double_as_longlong(re) & kAbsMask;
-            const uint64_t ui = (uint64_t)__double_as_longlong(im) & kAbsMask;
-            switch (p.mode) {
-                case SPLIT_RE: return ur;
-                case SPLIT_IM: return ui;
-                case SPLIT_SUM: return (uint64_t)__double_as_longlong(__dadd_rn(re, im)) & kAbsMask;
-                default: return ur > ui ? ur : ui;
-            }
-        }
     };
 
     // ---------------- pass 1: exponents
@@ -399,13 +265,27 @@ __global__ void __launch_bounds__(256) k_split_sm(const SplitParams p, int KW) {
             const int64_t w0 = w * KW;
             load_window(w0);
             __syncthreads();
-            const int64_t wlen = min((int64_t)KW, p.k - w0);
-            if (row < nrows)
-                for (int64_t l = lane; l < wlen; l += 32) {
-                    const uint64_t u = mag(slab[row * ld + l]);
+            const int wlen = (int)min((int64_t)KW, p.k - w0);
+            if (row < nrows) {
+                const Elem *src = slab + row * ld;
+                for (int l = lane; l < wlen; l += 32) {
+                    const Elem x = src[l];
+                    uint64_t u;
+                    if constexpr (!CPLX) {
+                        u = (uint64_t)__double_as_longlong(x) & kAbsMask;
+                    } else {
+                        const uint64_t ur = (uint64_t)__double_as_longlong(x.x) & kAbsMask;
+                        const uint64_t ui = (uint64_t)__double_as_longlong(x.y) & kAbsMask;   // |conj| = |.|
+                        if (p.mode == SPLIT_RE) u = ur;
+                        else if (p.mode == SPLIT_IM) u = ui;
+                        else if (p.mode == SPLIT_SUM)
+                            u = (uint64_t)__double_as_longlong(__dadd_rn(x.x, p.conj ? -x.y : x.y)) & kAbsMask;
+                        else u = ur > ui ? ur : ui;
+                    }
                     nf |= (u >= kExpInf);
                     m = (u < kExpInf && u > m) ? u : m;
                 }
+            }
             __syncthreads();
         }
 #pragma unroll
@@ -421,14 +301,13 @@ __global__ void __launch_bounds__(256) k_split_sm(const SplitParams p, int KW) {
                 e = nf ? kNonFinite : exponent_from_maxbits(m);
             }
             s_e[row] = e;
+            const int sh = 8 * p.s - 1 - e;               // 2^(P-e) as one exact DMUL when representable
+            s_scale[row] = (sh >= -1022 && sh <= 1023) ? pow2(sh) : 0.0;
         }
         __syncthreads();
     }
-    // ---------------- pass 2: digits (window already resident when nwin == 1)
-    const int ntgt = p.mode == SPLIT_A4M ? 2 : (p.mode == SPLIT_B4M ? 3 : 1);
+    // ---------------- pass 2: digits; one item = (row, 8-value half chunk), all targets
     const int64_t c2off = p.kh >> 4;
-    const int64_t blk = (int64_t)p.tile_h * 32;
-    const int64_t kb_stride = (int64_t)p.s * blk;          // bytes between k-blocks of one row tile
     for (int64_t w = 0; w < nwin; ++w) {
         const int64_t w0 = w * KW;
         if (nwin > 1) {
@@ -437,75 +316,66 @@ __global__ void __launch_bounds__(256) k_split_sm(const SplitParams p, int KW) {
             __syncthreads();
         }
         const int wh = (int)((min((int64_t)KW, kpad - w0) + 7) / 8);   // 8-value units in window
-        for (int tgt = 0; tgt < ntgt; ++tgt) {
-            // uniform per target: value component, sign, output rows and chunk offset
-            int comp = 0;
-            bool neg = false;
-            int rmul = 1, radd = 0;            // output row = rmul * r + radd
-            int64_t cadd = 0;                  // output chunk offset
-            int rmul1 = 0, radd1 = 0;          // second destination (B4M Re -> 2r+1, second half)
-            bool two = false;
-            switch (p.mode) {
-                case SPLIT_REAL: comp = 0; break;
-                case SPLIT_RE: comp = 1; break;
-                case SPLIT_IM: comp = 2; break;
-                case SPLIT_SUM: comp = 3; break;
-                case SPLIT_A4M: comp = tgt == 0 ? 1 : 2; cadd = tgt == 0 ? 0 : c2off; break;
-                default:   // SPLIT_B4M: 2r = [Re | -Im], 2r+1 = [Im | Re] (R9)
-                    rmul = 2;
-                    if (tgt == 0) { comp = 1; radd = 0; two = true; rmul1 = 2; radd1 = 1; }
-                    else if (tgt == 1) { comp = 2; radd = 1; }
-                    else { comp = 2; neg = true; radd = 0; cadd = c2off; }
-                    break;
-            }
-            for (int item = tid; item < 8 * wh; item += blockDim.x) {
-                const int row = item & 7;
-                const int h = item >> 3;
-                const int lw = h * 8;                      // offset in window
-                const int64_t l0 = w0 + lw;                // input depth index
-                const int32_t e = s_e[row];
-                const bool live = (row < nrows) && (e != kNonFinite);
+        for (int item = tid; item < 8 * wh; item += blockDim.x) {
+            const int row = item & 7;
+            const int h = item >> 3;
+            const int lw = h * 8;                      // offset in window
+            const int64_t l0 = w0 + lw;                // input depth index
+            const int32_t e = s_e[row];
+            const double scale = s_scale[row];
+            const bool live = (row < nrows) && (e != kNonFinite);
+            const int nvalid = live ? (int)min((int64_t)8, max((int64_t)0, p.k - l0)) : 0;
+            const Elem *src = slab + row * ld + lw;
+            const int64_t c = l0 >> 4;
+            const int hh = (int)((l0 >> 3) & 1);
+            const int64_t coff = (c >> 1) * kbs + (c & 1) * 128 + hh * 8;            // first half
+            const int64_t coff2 = ((c + c2off) >> 1) * kbs + ((c + c2off) & 1) * 128 + hh * 8;   // second half
+            if constexpr (!CPLX) {
                 double v[8];
-                const Elem *src = slab + row * ld + lw;
-                if (live && l0 + 8 <= p.k) {
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const Elem x = src[i];
-                        double val;
-                        if constexpr (!CPLX) {
-                            val = x;
-                        } else {
-                            const double im = p.conj ? -x.y : x.y;
-                            val = comp == 1 ? x.x : (comp == 2 ? im : __dadd_rn(x.x, im));
-                        }
-                        v[i] = neg ? -val : val;
-                    }
-                } else {
+                for (int i = 0; i < 8; ++i) v[i] = (i < nvalid) ? src[i] : 0.0;
+                digits_store8<SMAX>(v, scale, e, p.s, s_rowbase[row] + coff, nullptr, nullptr, blk);
+            } else {
+                // one component at a time (8 live values): 0 = Re, 1 = Im (conj applied), 2 = Re + Im
+                auto comp8 = [&](int comp, double (&v)[8]) {
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         double val = 0.0;
-                        if (live && l0 + i < p.k) {
-                            const Elem x = src[i];
-                            if constexpr (!CPLX) {
-                                val = x;
-                            } else {
-                                const double im = p.conj ? -x.y : x.y;
-                                val = comp == 1 ? x.x : (comp == 2 ? im : __dadd_rn(x.x, im));
-                            }
+                        if (i < nvalid) {
+                            const double *xe = reinterpret_cast<const double *>(src + i);
+                            const double re = xe[0], im0 = xe[1];
+                            const double im = p.conj ? -im0 : im0;
+                            val = comp == 0 ? re : (comp == 1 ? im : __dadd_rn(re, im));
                         }
-                        v[i] = neg ? -val : val;
+                        v[i] = val;
                     }
+                };
+                double v[8];
+                switch (p.mode) {
+                    case SPLIT_RE:
+                    case SPLIT_IM:
+                    case SPLIT_SUM:
+                        comp8(p.mode == SPLIT_RE ? 0 : (p.mode == SPLIT_IM ? 1 : 2), v);
+                        digits_store8<SMAX>(v, scale, e, p.s, s_rowbase[row] + coff, nullptr, nullptr, blk);
+                        break;
+                    case SPLIT_A4M:   // row r = [Re | Im]
+                        comp8(0, v);
+                        digits_store8<SMAX>(v, scale, e, p.s, s_rowbase[row] + coff, nullptr, nullptr, blk);
+                        comp8(1, v);
+                        digits_store8<SMAX>(v, scale, e, p.s, s_rowbase[row] + coff2, nullptr, nullptr, blk);
+                        break;
+                    default:          // SPLIT_B4M: 2r = [Re | -Im], 2r+1 = [Im | Re] (R9)
+                        comp8(0, v);
+                        digits_store8<SMAX>(v, scale, e, p.s, s_rowbase[2 * row] + coff,
+                                            s_rowbase[2 * row + 1] + coff2, nullptr, blk);
+                        comp8(1, v);
+                        digits_store8<SMAX>(v, scale, e, p.s, s_rowbase[2 * row + 1] + coff, nullptr,
+                                            s_rowbase[2 * row] + coff2, blk);
+                        break;
                 }
-                const int64_t r = r0 + row;
-                const int64_t c = (l0 >> 4) + cadd;
-                const int hh = (int)((l0 >> 3) & 1);
-                int8_t *d0 = slice_addr(p, b, rmul * r + radd, c, hh);
-                int8_t *d1 = two ? slice_addr(p, b, rmul1 * r + radd1, (l0 >> 4) + c2off, hh) : nullptr;
-                digits_store8<SMAX>(v, e, p.s, d0, d1, blk);
             }
         }
     }
-    (void)kb_stride;
 }
 
 }  // namespace ozk
