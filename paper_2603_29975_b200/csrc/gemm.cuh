@@ -74,6 +74,12 @@ enum DbgSlot : int {
     DBG_NSLOT
 };
 
+// debug timers (cold path): accumulate straight into the device buffer so no
+// timer stays live in registers across the tile loop
+__device__ __forceinline__ void dbg_add(const GemmParams &p, int slot, long long v) {
+    atomicAdd(p.dbg + slot, (unsigned long long)v);
+}
+
 __device__ __forceinline__ void decode_tile(const GemmParams &p, int64_t tile, int64_t &b,
                                             int64_t &tm, int64_t &tn) {
     const int64_t per_batch = p.tiles_m * p.tiles_n;

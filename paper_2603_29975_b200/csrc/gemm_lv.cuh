@@ -66,7 +66,10 @@ __device__ __forceinline__ void lv_store(const GemmParams &p, int64_t b, int64_t
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
             const int32_t f = __shfl_sync(0xffffffffu, j < 32 ? f_lo : f_hi, j & 31);
-            const double P = (enan || f == kNonFinite) ? qnan : scale_pow2(acc[j], e + f - 14);
+            const int nsc = e + f - 14;
+            double P;
+            if (pow2_normal(nsc)) P = __dmul_rn(acc[j], pow2(nsc));
+            else P = (enan || f == kNonFinite) ? qnan : scale_pow2(acc[j], nsc);
             if (j < ncol) *cp = beta0 ? __dmul_rn(p.alpha_r, P) : __fma_rn(p.alpha_r, P, __dmul_rn(p.beta_r, *cp));
             cp += p.ldc;
         }
@@ -75,9 +78,17 @@ __device__ __forceinline__ void lv_store(const GemmParams &p, int64_t b, int64_t
 #pragma unroll
         for (int c = 0; c < NC / 2; ++c) {
             const int32_t f = __shfl_sync(0xffffffffu, c < 16 ? f_lo : f_hi, (2 * c) & 31);
-            const bool nan = enan || f == kNonFinite;
-            const double Pr = nan ? qnan : scale_pow2(acc[2 * c], e + f - 14);
-            const double Pi = nan ? qnan : scale_pow2(acc[2 * c + 1], e + f - 14);
+            const int nsc = e + f - 14;
+            double Pr, Pi;
+            if (pow2_normal(nsc)) {
+                const double sc = pow2(nsc);
+                Pr = __dmul_rn(acc[2 * c], sc);
+                Pi = __dmul_rn(acc[2 * c + 1], sc);
+            } else {
+                const bool nan = enan || f == kNonFinite;
+                Pr = nan ? qnan : scale_pow2(acc[2 * c], nsc);
+                Pi = nan ? qnan : scale_pow2(acc[2 * c + 1], nsc);
+            }
             if (2 * c < ncol) {
                 double tr = 0.0, ti = 0.0;
                 if (!beta0) {

@@ -43,9 +43,8 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
     const int64_t total = p.batch * p.tiles_m * p.tiles_n;   // super-tiles (256 x 128)
     const int Sg = p.stages;
     uint32_t stage = 0, phase = 0;
-    uint32_t slot_par[kSlots] = {1u, 1u, 1u, 1u};
-    long long t_full = 0, t_slot = 0;
-    const long long t_begin = clock64();
+    uint32_t slot_par = (1u << kSlots) - 1u;    // bit j: parity to wait for on slot j
+    const long long t_begin = p.dbg ? clock64() : 0;
     const uint64_t dA = smem_desc_kmajor_noswz(0, 128, 256);   // 128-row A operand per CTA
     const uint64_t dB = smem_desc_kmajor_noswz(0, 128, 256);   // 64-row B half per CTA
     for (int64_t tile = blockIdx.x >> 1; tile < total; tile += gridDim.x >> 1) {
@@ -59,7 +58,7 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
                 const bool kfirst = (kb0 == p.kb_begin);
                 long long w0 = p.dbg ? clock64() : 0;
                 mbar_wait(&full[stage], phase);
-                if (p.dbg) t_full += clock64() - w0;
+                if (p.dbg && (threadIdx.x & 31) == 0) dbg_add(p, DBG_MMA_WAIT_FULL, clock64() - w0);
                 tc_fence_after();
                 const uint32_t sbase = smem_u32(smem + (size_t)stage * lp.stage_bytes);
                 for (int kk = 0; kk < nk; ++kk) {
@@ -70,9 +69,9 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
 #pragma unroll
                         for (int j = 0; j < hi - lo + 1; ++j) {
                             w0 = p.dbg ? clock64() : 0;
-                            mbar_wait(&slot_empty[j], slot_par[j]);
-                            slot_par[j] ^= 1u;
-                            if (p.dbg) t_slot += clock64() - w0;
+                            mbar_wait(&slot_empty[j], (slot_par >> j) & 1u);
+                            slot_par ^= 1u << j;
+                            if (p.dbg && (threadIdx.x & 31) == 0) dbg_add(p, DBG_MMA_WAIT_SLOT, clock64() - w0);
                         }
                         tc_fence_after();
                     }
@@ -99,11 +98,7 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
             mma_commit_pair_elect(pass_full);
         }
     }
-    if (p.dbg && (threadIdx.x & 31) == 0) {
-        atomicAdd(p.dbg + DBG_MMA_WAIT_FULL, (unsigned long long)t_full);
-        atomicAdd(p.dbg + DBG_MMA_WAIT_SLOT, (unsigned long long)t_slot);
-        atomicAdd(p.dbg + DBG_MMA_TOTAL, (unsigned long long)(clock64() - t_begin));
-    }
+    if (p.dbg && (threadIdx.x & 31) == 0) dbg_add(p, DBG_MMA_TOTAL, clock64() - t_begin);
 }
 
 // CHUNK (compile time, reading R8): 0 = whole K in one INT32 accumulation;
@@ -152,7 +147,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         // ========================= producer (both CTAs): own A rows, own B half
         if (lane == 0) {
             uint32_t stage = 0, phase = 0;
-            long long t_wait = 0;
             for (int64_t tile = blockIdx.x >> 1; tile < total; tile += gridDim.x >> 1) {
                 int64_t b, tm, tn;
                 decode_tile(p, tile, b, tm, tn);
@@ -166,7 +160,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                         const int nk = (int)min((int64_t)pa.kpp, p.kb_end - kb0);
                         const long long w0 = p.dbg ? clock64() : 0;
                         mbar_wait(&empty[stage], phase ^ 1);
-                        if (p.dbg) t_wait += clock64() - w0;
+                        if (p.dbg) dbg_add(p, DBG_PROD_WAIT, clock64() - w0);
                         const uint32_t leader_full = mapa_shared(smem_u32(&full[stage]), 0);
                         if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2u * (abytes + bbytes) * nk);
                         uint8_t *dst = smem + (size_t)stage * lp.stage_bytes;
@@ -182,7 +176,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     }
                 }
             }
-            if (p.dbg) atomicAdd(p.dbg + DBG_PROD_WAIT, (unsigned long long)t_wait);
         }
     } else if (warp == 1) {
         // ========================= MMA issuer: leader CTA only
@@ -203,10 +196,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         const int half = ew >> 2;                    // column group: [half * kNC2, +kNC2)
         const uint32_t tl = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(half * kNC2);
         uint32_t pphase = 0;
-        long long t_w = 0, t_d = 0, t_s = 0;
-        uint32_t slot_remote[kSlots];
-#pragma unroll
-        for (int j = 0; j < kSlots; ++j) slot_remote[j] = mapa_shared(smem_u32(&slot_empty[j]), 0);
+        const bool dbgw = p.dbg && warp == 2 && lane == 0;
+        // slot_empty barriers are consecutive 8-byte words: remote address = base + 8 j
+        const uint32_t slot_remote0 = mapa_shared(smem_u32(&slot_empty[0]), 0);
         for (int64_t tile = blockIdx.x >> 1; tile < total; tile += gridDim.x >> 1) {
             int64_t b, tm, tn;
             decode_tile(p, tile, b, tm, tn);
@@ -220,28 +212,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 long long w0 = p.dbg ? clock64() : 0;
                 mbar_wait(pass_full, pphase);
                 long long w1 = p.dbg ? clock64() : 0;
-                t_w += w1 - w0;
+                if (dbgw) dbg_add(p, DBG_EPI_WAIT, w1 - w0);
                 pphase ^= 1;
                 tc_fence_after();
+                if constexpr (CHUNK == 0 && EPI != EPI_LEVELS) {
+                    // one software pipeline over the pass: chunk c = (level c/2, 16-column
+                    // group c%2), the load of chunk c+1 in flight while chunk c is combined;
+                    // a level's TMEM slot is released as soon as both its groups are in
+                    // registers (before its FP64 work).  Levels in ascending significance (R6).
+                    static_assert(kNC2 == 32, "two 16-column groups per level");
+                    const int nlev = pa.hi - pa.lo + 1;
+                    uint32_t v[16];
+#pragma unroll 1
+                    for (int j = 0; j < nlev; ++j) {
+                        const double sc = pow2(-8 * (pa.hi - j - 2));
+                        tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN), v);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) acc[i] = __fma_rn(i32_to_f64(v[i]), sc, acc[i]);
+                        tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + 16), v);
+                        tmem_wait_ld();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster(slot_remote0 + 8u * (uint32_t)j);
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) acc[16 + i] = __fma_rn(i32_to_f64(v[i]), sc, acc[16 + i]);
+                    }
+                } else {
                 for (int L = pa.hi; L >= pa.lo; --L) {          // ascending significance (R6)
                     const int j = pa.hi - L;
                     const double sc = pow2(-8 * (L - 2));
-                    if constexpr (CHUNK == 0 && EPI != EPI_LEVELS) {
-                        // software-pipelined drain: load 16 columns ahead of the FP64 work
-                        uint32_t va[16], vb[16];
-                        tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN), va);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int g = 0; g < kNC2 / 16; ++g) {
-                            uint32_t (&cur)[16] = (g & 1) ? vb : va;
-                            uint32_t (&nxt)[16] = (g & 1) ? va : vb;
-                            if (g + 1 < kNC2 / 16) tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + (g + 1) * 16), nxt);
-#pragma unroll
-                            for (int i = 0; i < 16; ++i)
-                                acc[g * 16 + i] = __fma_rn(i32_to_f64(cur[i]), sc, acc[g * 16 + i]);
-                            if (g + 1 < kNC2 / 16) tmem_wait_ld();
-                        }
-                    } else {
 #pragma unroll
                         for (int g = 0; g < kNC2 / 32; ++g) {
                             uint32_t v0[16], v1[16];
@@ -260,13 +260,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                                 }
                                 continue;
                             }
-                            if constexpr (CHUNK == 0) {
-    #pragma unroll
-                                for (int i = 0; i < 16; ++i) {
-                                    acc[g * 32 + i] = __fma_rn(i32_to_f64(v0[i]), sc, acc[g * 32 + i]);
-                                    acc[g * 32 + 16 + i] = __fma_rn(i32_to_f64(v1[i]), sc, acc[g * 32 + 16 + i]);
-                                }
-                            } else if constexpr (CHUNK == 1) {
+                            if constexpr (CHUNK == 1) {
                                 // first/middle K chunk (R8): exact partial level sums W (+)= S
                                 const int64_t c0 = tn * kLvBN + half * kNC2 + g * 32;
                                 if (grow < p.Mp) {
@@ -279,7 +273,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                                         *q = (p.chunk_mode == 1) ? part : __dadd_rn(*q, part);
                                     }
                                 }
-                            } else {
+                            } else if constexpr (CHUNK == 2) {
                                 // last K chunk: level sum = W + S (exact), then the FP64 combine
                                 const int64_t c0 = tn * kLvBN + half * kNC2 + g * 32;
                                 const bool rok = grow < p.Mp;
@@ -292,21 +286,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                                 }
                             }
                         }
-                    }
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive_cluster(slot_remote[j]);
+                    if (lane == 0) mbar_arrive_cluster(slot_remote0 + 8u * (uint32_t)j);
                 }
-                if (p.dbg) t_d += clock64() - w1;
+                }
+                if (dbgw) dbg_add(p, DBG_EPI_DRAIN, clock64() - w1);
             }
             const long long s0 = p.dbg ? clock64() : 0;
             if constexpr (EPI != EPI_LEVELS && CHUNK != 1) lv_store<EPI, kNC2>(p, b, grow, e, tn * kLvBN + half * kNC2, acc);
-            if (p.dbg) t_s += clock64() - s0;
-        }
-        if (p.dbg && warp == 2 && lane == 0) {
-            atomicAdd(p.dbg + DBG_EPI_WAIT, (unsigned long long)t_w);
-            atomicAdd(p.dbg + DBG_EPI_DRAIN, (unsigned long long)t_d);
-            atomicAdd(p.dbg + DBG_EPI_STORE, (unsigned long long)t_s);
+            if (dbgw) dbg_add(p, DBG_EPI_STORE, clock64() - s0);
         }
     }
 

@@ -64,6 +64,12 @@ __device__ __forceinline__ double ldexp_rn(double x, int n) {
     return __dmul_rn(y, pow2(E + 1022));
 }
 
+// 2^n is a normal double (n in [-1022, 1023]): then x * 2^n by one DMUL is the
+// correctly rounded (RNE) ldexp for every finite x -- exact when the result is
+// normal, one rounding of the exact product when it is subnormal, +-Inf on
+// overflow.  Sentinel exponents (kNonFinite) fall outside and take the slow path.
+__device__ __forceinline__ bool pow2_normal(int n) { return (unsigned)(n + 1022) <= 2045u; }
+
 // x * 2^n, correctly rounded: exact exponent-field add when x and the result
 // are normal (the common case, branch-free select); otherwise ldexp_rn.
 __device__ __forceinline__ double scale_pow2(double x, int n) {
