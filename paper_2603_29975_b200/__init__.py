@@ -309,7 +309,8 @@ def debug_split(side, kind, trans, X, num_slices, stream=None):
 
 
 TIMER_NAMES = ("prod_wait_empty", "mma_wait_full", "mma_wait_slot", "mma_total", "epi_wait_pass",
-               "epi_drain", "epi_store", "cta_total")
+               "epi_drain", "epi_store", "cta_total", "mma_wait_slot_pass0", "epi_prefix",
+               "epi_first_arrive")
 
 
 def debug_timing(enable: bool = True, read: bool = False) -> dict | None:

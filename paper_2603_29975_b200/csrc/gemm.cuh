@@ -49,6 +49,7 @@ struct GemmParams {
     double *C;              // real: double elements; complex: interleaved pairs
     int64_t ldc, strideC;   // in elements (complex elements for EPI_CPLX4M)
     double alpha_r, alpha_i, beta_r, beta_i;
+    int ab_unit;               // alpha == 1 (+0i) and beta == 0: C = P, no FP64 in the store
     int32_t *S_out;         // EPI_LEVELS
     // K-chunking (reading R8): this launch covers k-blocks [kb_begin, kb_end);
     // chunk_mode 0 = whole K, 1 = first chunk (W = S), 2 = middle (W += S),
@@ -71,6 +72,9 @@ enum DbgSlot : int {
     DBG_EPI_DRAIN,       // epilogue TMEM -> FP64 accumulate (warp 2)
     DBG_EPI_STORE,       // epilogue ldexp + alpha/beta + store (warp 2)
     DBG_TOTAL,           // CTA lifetime (warp 1)
+    DBG_MMA_WAIT_SLOT0,  // part of DBG_MMA_WAIT_SLOT spent before the first pass of a tile
+    DBG_EPI_PREFIX,      // part of DBG_EPI_DRAIN spent in the exact-prefix levels (warp 2)
+    DBG_EPI_FIRST_ARRIVE,// pass_full -> first slot released, first pass (warp 2)
     DBG_NSLOT
 };
 

@@ -52,7 +52,7 @@ struct LvParams {
 // owns whole complex numbers: one 16-byte store, no lane exchange.
 template <int EPI, int NC = 64>
 __device__ __forceinline__ void lv_store(const GemmParams &p, int64_t b, int64_t grow, int32_t e,
-                                         int64_t col0, const double *acc) {
+                                         int64_t col0, const double *acc, int nbias = 0) {
     const int lane = threadIdx.x & 31;
     const int ncol = (grow < p.Mp) ? (int)min((int64_t)NC, p.N - col0) : 0;
     // column exponents: lane j holds f of columns col0 + j and col0 + 32 + j
@@ -61,16 +61,22 @@ __device__ __forceinline__ void lv_store(const GemmParams &p, int64_t b, int64_t
     const bool beta0 = (p.beta_r == 0.0 && p.beta_i == 0.0);
     const bool enan = (e == kNonFinite);
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+    // P = ldexp(acc, e + f - 14) by an integer exponent-field add (scale_pow2: exact, no FP64
+    // instruction on the normal path).  Scalar FP64 shares the SM's tensor datapath on B200 and
+    // runs ~19x slower while the MMAs of the next tile stream (tools/fp64_vs_mma.cu), so the
+    // store avoids FP64 entirely when alpha = 1, beta = 0: then R7's formula reduces bitwise to
+    // C = P (real) and, complex, C_r = P_r + 0 (-0 -> +0; NaN if P_i is not finite, from
+    // -0 * Inf), C_i likewise.
     if constexpr (EPI == EPI_REAL) {
         double *cp = p.C + b * p.strideC + grow + col0 * p.ldc;
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
             const int32_t f = __shfl_sync(0xffffffffu, j < 32 ? f_lo : f_hi, j & 31);
-            const int nsc = e + f - 14;
-            double P;
-            if (pow2_normal(nsc)) P = __dmul_rn(acc[j], pow2(nsc));
-            else P = (enan || f == kNonFinite) ? qnan : scale_pow2(acc[j], nsc);
-            if (j < ncol) *cp = beta0 ? __dmul_rn(p.alpha_r, P) : __fma_rn(p.alpha_r, P, __dmul_rn(p.beta_r, *cp));
+            const double P = (enan || f == kNonFinite) ? qnan : scale_pow2(acc[j], e + f - 14 + nbias);
+            if (j < ncol) {
+                if (p.ab_unit) *cp = P;
+                else *cp = beta0 ? __dmul_rn(p.alpha_r, P) : __fma_rn(p.alpha_r, P, __dmul_rn(p.beta_r, *cp));
+            }
             cp += p.ldc;
         }
     } else {
@@ -78,26 +84,23 @@ __device__ __forceinline__ void lv_store(const GemmParams &p, int64_t b, int64_t
 #pragma unroll
         for (int c = 0; c < NC / 2; ++c) {
             const int32_t f = __shfl_sync(0xffffffffu, c < 16 ? f_lo : f_hi, (2 * c) & 31);
-            const int nsc = e + f - 14;
-            double Pr, Pi;
-            if (pow2_normal(nsc)) {
-                const double sc = pow2(nsc);
-                Pr = __dmul_rn(acc[2 * c], sc);
-                Pi = __dmul_rn(acc[2 * c + 1], sc);
-            } else {
-                const bool nan = enan || f == kNonFinite;
-                Pr = nan ? qnan : scale_pow2(acc[2 * c], nsc);
-                Pi = nan ? qnan : scale_pow2(acc[2 * c + 1], nsc);
-            }
+            const int nsc = e + f - 14 + nbias;
+            const bool nan = enan || f == kNonFinite;
+            const double Pr = nan ? qnan : scale_pow2(acc[2 * c], nsc);
+            const double Pi = nan ? qnan : scale_pow2(acc[2 * c + 1], nsc);
             if (2 * c < ncol) {
-                double tr = 0.0, ti = 0.0;
-                if (!beta0) {
-                    const double2 cv = *cp;
-                    tr = __fma_rn(p.beta_r, cv.x, -__dmul_rn(p.beta_i, cv.y));
-                    ti = __fma_rn(p.beta_r, cv.y, __dmul_rn(p.beta_i, cv.x));
+                if (p.ab_unit) {
+                    *cp = make_double2(plus_zero(Pr, Pi), plus_zero(Pi, Pr));
+                } else {
+                    double tr = 0.0, ti = 0.0;
+                    if (!beta0) {
+                        const double2 cv = *cp;
+                        tr = __fma_rn(p.beta_r, cv.x, -__dmul_rn(p.beta_i, cv.y));
+                        ti = __fma_rn(p.beta_r, cv.y, __dmul_rn(p.beta_i, cv.x));
+                    }
+                    *cp = make_double2(__fma_rn(p.alpha_r, Pr, __fma_rn(-p.alpha_i, Pi, tr)),
+                                       __fma_rn(p.alpha_r, Pi, __fma_rn(p.alpha_i, Pr, ti)));
                 }
-                *cp = make_double2(__fma_rn(p.alpha_r, Pr, __fma_rn(-p.alpha_i, Pi, tr)),
-                                   __fma_rn(p.alpha_r, Pi, __fma_rn(p.alpha_i, Pr, ti)));
             }
             cp += p.ldc;
         }

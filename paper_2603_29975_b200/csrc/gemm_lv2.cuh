@@ -71,7 +71,11 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
                             w0 = p.dbg ? clock64() : 0;
                             mbar_wait(&slot_empty[j], (slot_par >> j) & 1u);
                             slot_par ^= 1u << j;
-                            if (p.dbg && (threadIdx.x & 31) == 0) dbg_add(p, DBG_MMA_WAIT_SLOT, clock64() - w0);
+                            if (p.dbg && (threadIdx.x & 31) == 0) {
+                                const long long dw = clock64() - w0;
+                                dbg_add(p, DBG_MMA_WAIT_SLOT, dw);
+                                if (ps == 0) dbg_add(p, DBG_MMA_WAIT_SLOT0, dw);
+                            }
                         }
                         tc_fence_after();
                     }
@@ -221,11 +225,53 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     // a level's TMEM slot is released as soon as both its groups are in
                     // registers (before its FP64 work).  Levels in ascending significance (R6).
                     static_assert(kNC2 == 32, "two 16-column groups per level");
+                    // acc is carried scaled by 2^(8(s-1)) (exact: power-of-two scaling of
+                    // normal values leaves every RNE step unchanged); level L weighs 2^(8(s+1-L)).
                     const int nlev = pa.hi - pa.lo + 1;
                     uint32_t v[16];
+                    int j0 = 0;
+                    if (ps == 0) {
+                        // exact prefix: the first np <= 3 levels (L = s+1, s, s-1).  With
+                        // |S_L| < 2^31 their sum T = S_{s+1} + 2^8 S_s + 2^16 S_{s-1} < 2^48 is
+                        // an integer, so every FP64 step of R6 over them is exact and equals T;
+                        // build T in int64 (IMAD.WIDE) and convert once via the 1.5*2^52 bias.
+                        const int np = nlev < 3 ? nlev : 3;
+#pragma unroll
+                        for (int g = 0; g < 2; ++g) {
+                            long long t[16];
+                            tmem_ld_32x32b_x16(tl + (uint32_t)(g * 16), v);
+                            tmem_wait_ld();
+                            if (g == 1) {
+                                tc_fence_before();
+                                __syncwarp();
+                                if (lane == 0) mbar_arrive_cluster(slot_remote0);
+                                if (dbgw) dbg_add(p, DBG_EPI_FIRST_ARRIVE, clock64() - w1);
+                            }
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) t[i] = (long long)(int)v[i] + 0x4338000000000000ll;
 #pragma unroll 1
-                    for (int j = 0; j < nlev; ++j) {
-                        const double sc = pow2(-8 * (pa.hi - j - 2));
+                            for (int j = 1; j < np; ++j) {
+                                tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + g * 16), v);
+                                tmem_wait_ld();
+                                if (g == 1) {
+                                    tc_fence_before();
+                                    __syncwarp();
+                                    if (lane == 0) mbar_arrive_cluster(slot_remote0 + 8u * (uint32_t)j);
+                                }
+                                const long long w = 1ll << (8 * j);
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) t[i] += (long long)(int)v[i] * w;
+                            }
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                acc[g * 16 + i] = __dsub_rn(__longlong_as_double(t[i]), 6755399441055744.0);
+                        }
+                        j0 = np;
+                        if (dbgw) dbg_add(p, DBG_EPI_PREFIX, clock64() - w1);
+                    }
+#pragma unroll 1
+                    for (int j = j0; j < nlev; ++j) {
+                        const double sc = pow2(8 * (s + 1 - (pa.hi - j)));
                         tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN), v);
                         tmem_wait_ld();
 #pragma unroll
@@ -294,7 +340,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 if (dbgw) dbg_add(p, DBG_EPI_DRAIN, clock64() - w1);
             }
             const long long s0 = p.dbg ? clock64() : 0;
-            if constexpr (EPI != EPI_LEVELS && CHUNK != 1) lv_store<EPI, kNC2>(p, b, grow, e, tn * kLvBN + half * kNC2, acc);
+            if constexpr (EPI != EPI_LEVELS && CHUNK != 1)
+                lv_store<EPI, kNC2>(p, b, grow, e, tn * kLvBN + half * kNC2, acc, CHUNK == 0 ? -8 * (s - 1) : 0);
             if (dbgw) dbg_add(p, DBG_EPI_STORE, clock64() - s0);
         }
     }

@@ -81,6 +81,36 @@ __device__ __forceinline__ double scale_pow2(double x, int n) {
     return ldexp_rn(x, n);
 }
 
+// RNE(x) to a double for an integer |x| < 2^62, with integer operations only
+// (no FP64 instruction): round the magnitude to 53 significant bits, ties to
+// even, then assemble sign | exponent | fraction.
+__device__ __forceinline__ double i64_to_f64_rn(long long x) {
+    const unsigned long long sgn = (unsigned long long)x & 0x8000000000000000ull;
+    const unsigned long long a = x < 0 ? 0ull - (unsigned long long)x : (unsigned long long)x;
+    if (a == 0) return 0.0;
+    const int p = 63 - __clzll((long long)a);          // bit length - 1
+    unsigned long long m;
+    if (p > 52) {
+        const int k = p - 52;
+        const unsigned long long r = a >> k, rem = a & ((1ull << k) - 1), half = 1ull << (k - 1);
+        m = r + ((rem > half || (rem == half && (r & 1ull))) ? 1ull : 0ull);   // may reach 2^53
+    } else {
+        m = a << (52 - p);
+    }
+    // m's leading one (bit 52, or 53 after a carry) adds to the exponent field
+    return __longlong_as_double((long long)(sgn | (((unsigned long long)(p + 1022) << 52) + m)));
+}
+
+// fma(1, x, fma(+-0, y, +0)) of R7 with alpha = 1, beta = 0, in integer operations:
+// the inner term is +0 when y is finite and NaN when y is +-Inf / NaN; x + (+0) maps
+// -0 to +0 and keeps every other x (NaN stays NaN).
+__device__ __forceinline__ double plus_zero(double x, double y) {
+    const long long by = __double_as_longlong(y);
+    if ((by & (long long)kExpInf) == (long long)kExpInf) return __longlong_as_double(0x7ff8000000000000ll);
+    const long long bx = __double_as_longlong(x);
+    return __longlong_as_double(bx == (long long)0x8000000000000000ull ? 0ll : bx);
+}
+
 // Exact int32 -> double without the XU pipe: 2^52 + 2^31 + x is representable,
 // built from bits (hi word 0x43300000, lo word x + 2^31); one exact DADD
 // removes the offset.  Same value as __int2double_rn, on the FP64 pipe.

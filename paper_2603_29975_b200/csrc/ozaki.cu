@@ -590,6 +590,7 @@ int launch_gemm(const Plan &P, int epi, const int8_t *sa, const int8_t *sb, cons
     gp.alpha_i = al[1];
     gp.beta_r = be[0];
     gp.beta_i = be[1];
+    gp.ab_unit = (al[0] == 1.0 && al[1] == 0.0 && be[0] == 0.0 && be[1] == 0.0) ? 1 : 0;
     gp.S_out = S_out;
     gp.kb_begin = 0;
     gp.kb_end = P.KB;
