@@ -231,40 +231,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     uint32_t v[16];
                     int j0 = 0;
                     if (ps == 0) {
-                        // exact prefix: the first np <= 3 levels (L = s+1, s, s-1).  With
-                        // |S_L| < 2^31 their sum T = S_{s+1} + 2^8 S_s + 2^16 S_{s-1} < 2^48 is
-                        // an integer, so every FP64 step of R6 over them is exact and equals T;
-                        // build T in int64 (IMAD.WIDE) and convert once via the 1.5*2^52 bias.
-                        const int np = nlev < 3 ? nlev : 3;
+                        // Integer prefix: the first np <= 4 levels (L = s+1 .. s-2).  With
+                        // |S_L| < 2^31, X = sum_j S_j 2^(8j) (< 2^55.01) is exact in int64; R6's
+                        // steps over the first three are exact (< 2^53), so R6 rounds once, at the
+                        // fourth: acc = RNE53(X) = one I2F.F64.S64 (round-to-nearest-even).  No
+                        // FP64-pipe instruction: FP64 is starved while the tensor core streams the
+                        // next pass (tools/fp64_vs_mma.cu), I2F and IMAD are not.
+                        const int np = nlev < 4 ? nlev : 4;
+                        long long t0[16], t1[16];
+                        // columns 0..15 of every prefix level, then 16..31 (each slot released
+                        // right after its second load); conversions only after the last release
+                        tmem_ld_32x32b_x16(tl, v);
+                        tmem_wait_ld();
 #pragma unroll
-                        for (int g = 0; g < 2; ++g) {
-                            long long t[16];
-                            tmem_ld_32x32b_x16(tl + (uint32_t)(g * 16), v);
-                            tmem_wait_ld();
-                            if (g == 1) {
-                                tc_fence_before();
-                                __syncwarp();
-                                if (lane == 0) mbar_arrive_cluster(slot_remote0);
-                                if (dbgw) dbg_add(p, DBG_EPI_FIRST_ARRIVE, clock64() - w1);
-                            }
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) t[i] = (long long)(int)v[i] + 0x4338000000000000ll;
+                        for (int i = 0; i < 16; ++i) t0[i] = (long long)(int)v[i];
 #pragma unroll 1
-                            for (int j = 1; j < np; ++j) {
-                                tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + g * 16), v);
-                                tmem_wait_ld();
-                                if (g == 1) {
-                                    tc_fence_before();
-                                    __syncwarp();
-                                    if (lane == 0) mbar_arrive_cluster(slot_remote0 + 8u * (uint32_t)j);
-                                }
-                                const long long w = 1ll << (8 * j);
+                        for (int j = 1; j < np; ++j) {
+                            tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN), v);
+                            tmem_wait_ld();
+                            const int w = 1 << (8 * j);
 #pragma unroll
-                                for (int i = 0; i < 16; ++i) t[i] += (long long)(int)v[i] * w;
-                            }
+                            for (int i = 0; i < 16; ++i) t0[i] += (long long)(int)v[i] * w;
+                        }
+                        tmem_ld_32x32b_x16(tl + 16u, v);
+                        tmem_wait_ld();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster(slot_remote0);
+                        if (dbgw) dbg_add(p, DBG_EPI_FIRST_ARRIVE, clock64() - w1);
 #pragma unroll
-                            for (int i = 0; i < 16; ++i)
-                                acc[g * 16 + i] = __dsub_rn(__longlong_as_double(t[i]), 6755399441055744.0);
+                        for (int i = 0; i < 16; ++i) t1[i] = (long long)(int)v[i];
+#pragma unroll 1
+                        for (int j = 1; j < np; ++j) {
+                            tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + 16), v);
+                            tmem_wait_ld();
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_cluster(slot_remote0 + 8u * (uint32_t)j);
+                            const int w = 1 << (8 * j);
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) t1[i] += (long long)(int)v[i] * w;
+                        }
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            acc[i] = __ll2double_rn(t0[i]);
+                            acc[16 + i] = __ll2double_rn(t1[i]);
                         }
                         j0 = np;
                         if (dbgw) dbg_add(p, DBG_EPI_PREFIX, clock64() - w1);
