@@ -129,6 +129,9 @@ int ozaki_zgemm3m_strided_batched(char transa, char transb, int64_t m, int64_t n
  * thread-local; returns 0.                                                 */
 int ozaki_set_stream(void *stream);
 void *ozaki_get_stream(void);
+/* Blocks until all work enqueued on this thread's stream is done (used by the
+ * BLAS shim, whose calls are synchronous).  0, or OZAKI_ERR_CUDA.          */
+int ozaki_stream_synchronize(void);
 /* Synchronises the device once to read the non-finite counter.           */
 int ozaki_get_stats(ozaki_stats_t *out);
 int ozaki_reset_stats(void);

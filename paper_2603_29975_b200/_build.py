@@ -9,6 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libozaki.so")
+SHIM = os.path.join(PKG, "libozaki_blas.so")   # Fortran dgemm_/zgemm_ interposition (NEXT-2)
 SOURCES = ["ozaki.cu"]
 HEADERS = ["gemm_lv2.cuh", "passplan.cuh", "gemm_lv.cuh", "gemm.cuh", "split.cuh", "numerics.cuh", "ptx.cuh"]
 
@@ -37,8 +38,26 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def build_shim(force: bool = False) -> str:
+    """libozaki_blas.so: dgemm_/zgemm_ (Fortran ABI) -> libozaki.so, rpath $ORIGIN."""
+    src = os.path.join(CSRC, "blas_shim.cpp")
+    deps = [src, os.path.join(ROOT, "include", "ozaki.h"), LIB]
+    if not force and os.path.exists(SHIM) and all(os.path.getmtime(d) <= os.path.getmtime(SHIM) for d in deps):
+        return SHIM
+    tmp = SHIM + f".tmp{os.getpid()}"
+    cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-Wall", "-I", os.path.join(ROOT, "include"),
+           src, "-o", tmp, "-L", PKG, "-l:libozaki.so", "-Wl,-rpath,$ORIGIN"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("building libozaki_blas.so failed")
+    os.replace(tmp, SHIM)
+    return SHIM
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
+        build_shim()
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
@@ -53,6 +72,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         sys.stderr.write(res.stderr)
     os.replace(tmp, LIB)
+    build_shim(force=True)
     return LIB
 
 

@@ -1053,6 +1053,11 @@ int ozaki_set_stream(void *stream) {
 
 void *ozaki_get_stream(void) { return (void *)t_stream; }
 
+int ozaki_stream_synchronize(void) {
+    CUDA_TRY(cudaStreamSynchronize(t_stream));
+    return 0;
+}
+
 int ozaki_get_stats(ozaki_stats_t *out) {
     if (!out) return -1;
     std::memset(out, 0, sizeof *out);
