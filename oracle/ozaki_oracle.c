@@ -386,3 +386,88 @@ void orc_quick_complex(int64_t mn, double br, double bi, double *Cr, double *Ci)
         }
     }
 }
+
+/* ========================================================================= */
+/* Ozaki-II (CRT) -- NEXT-1.  PAPER.md:99 (§2.2): "converts floating-point     */
+/* matrices into integers, performs multiple matrix multiplications using     */
+/* smaller, pairwise coprime moduli and uses the CRT to reconstruct the final */
+/* result"; knob = the moduli count.  Steps follow        */
+/* SPEC.md [MODULE] ozaki2 (quantize / residue_gemm / crt_reconstruct) with    */
+/* DESIGN.md readings R16..R20.  The CRT itself and the final rounding live in */
+/* oracle/ozaki2.py (Python big integers / Fraction); these are the two loops  */
+/* that are too slow in Python.                                               */
+/* ========================================================================= */
+
+/* R17 quantize: row (A) / column (B) power-of-two scale e and integers
+ *   Q = RNE(x * 2^(nu - e)),  |Q| < 2^nu.
+ * e = frexp exponent of M = max|x| (M < 2^e); if RNE(M * 2^(nu-e)) reaches 2^nu
+ * then e += 1.  M == 0 -> e = 0, Q = 0.  Non-finite entry -> row flagged, Q = 0.
+ * nu <= 62.  Inputs row-major rows x k (row contiguous).                     */
+int orc2_quantize_rows(int64_t rows, int64_t k, const double *X, int nu, int64_t *Q, int *e_out,
+                       int *nonfinite)
+{
+    for (int64_t i = 0; i < rows; ++i) {
+        const double *x = X + i * k;
+        double M = 0.0;
+        int nf = 0;
+        for (int64_t j = 0; j < k; ++j) {
+            if (!isfinite(x[j])) nf = 1;
+            else if (fabs(x[j]) > M) M = fabs(x[j]);
+        }
+        nonfinite[i] = nf;
+        int e = 0;
+        if (M > 0.0) {
+            (void)frexp(M, &e);
+            if (nearbyint(ldexp(M, nu - e)) >= ldexp(1.0, nu)) e += 1;
+        }
+        e_out[i] = e;
+        for (int64_t j = 0; j < k; ++j)
+            Q[i * k + j] = (nf || M == 0.0) ? 0 : (int64_t)nearbyint(ldexp(x[j], nu - e));
+    }
+    return 0;
+}
+
+/* Exact integer product Z = QA @ QBt^T with |Q| < 2^62: split Q = h 2^32 + l
+ * (l = low 32 bits, unsigned) and accumulate three int128 sums
+ *   hh = sum h_a h_b,  mid = sum (h_a l_b + l_a h_b),  ll = sum l_a l_b
+ * so Z = hh 2^64 + mid 2^32 + ll (combined with big integers in Python).
+ * out[(i n + j) * 6 + {0..5}] = (hh, mid, ll) as (low64, high64) pairs.     */
+void orc2_int_gemm(int64_t m, int64_t n, int64_t k, const int64_t *QA, const int64_t *QBt, uint64_t *out)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < m; ++i)
+        for (int64_t j = 0; j < n; ++j) {
+            i128 hh = 0, mid = 0, ll = 0;
+            for (int64_t t = 0; t < k; ++t) {
+                const int64_t a = QA[i * k + t], b = QBt[j * k + t];
+                const i128 ah = a >> 32, bh = b >> 32;
+                const i128 al = (uint32_t)(a & 0xffffffff), bl = (uint32_t)(b & 0xffffffff);
+                hh += ah * bh;
+                mid += ah * bl + al * bh;
+                ll += al * bl;
+            }
+            uint64_t *o = out + (i * n + j) * 6;
+            const i128 v[3] = {hh, mid, ll};
+            for (int q = 0; q < 3; ++q) {
+                o[2 * q] = (uint64_t)v[q];
+                o[2 * q + 1] = (uint64_t)(v[q] >> 64);
+            }
+        }
+}
+
+/* R19 residue GEMM for one modulus p: C = (RA @ RBt^T) mod p, centered
+ * (p even: [-p/2, p/2-1]; odd: [-(p-1)/2, (p-1)/2]).  RA, RBt int8 residues.  */
+void orc2_residue_gemm(int64_t m, int64_t n, int64_t k, const int8_t *RA, const int8_t *RBt, int p,
+                       int32_t *C)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < m; ++i)
+        for (int64_t j = 0; j < n; ++j) {
+            int64_t acc = 0;
+            for (int64_t t = 0; t < k; ++t) acc += (int64_t)RA[i * k + t] * RBt[j * k + t];
+            int64_t r = acc % p;
+            if (r < 0) r += p;
+            if (r >= (p + 1) / 2) r -= p;
+            C[i * n + j] = (int32_t)r;
+        }
+}
