@@ -77,6 +77,7 @@ typedef struct ozaki_stats {
     uint64_t k_chunks;        /* extra INT32 K-chunks needed (R8)             */
     uint64_t nonfinite_rows;  /* rows/cols that contained Inf/NaN (synced)    */
     uint64_t kernel_launches; /* device kernels launched by the library      */
+    uint64_t crt_calls;       /* Ozaki-II calls (ozaki2_*)                   */
 } ozaki_stats_t;
 
 /* --- real: C = alpha op(A) op(B) + beta C,  op(A) m x k, op(B) k x n ---------
@@ -123,6 +124,42 @@ int ozaki_zgemm3m_strided_batched(char transa, char transb, int64_t m, int64_t n
                                   const double *B, int64_t ldb, int64_t strideB,
                                   const double *beta, double *C, int64_t ldc, int64_t strideC,
                                   int64_t batch, int num_slices);
+
+/* --- Ozaki-II (CRT), NEXT-1 of SURVEY.md §8(f) ------------------------------
+ * PAPER.md:99 (§2.2): Ozaki-II "converts floating-point matrices into
+ * integers, performs multiple matrix multiplications using smaller, pairwise
+ * coprime moduli and uses the CRT to reconstruct the final result"; the knob is
+ * the moduli count (10..18 in PAPER.md:119, :127).  Readings R16..R20:
+ *   moduli   256, 255, 253, 251, 247, ... (greedy pairwise coprime, <= 256)
+ *   nu       = min(62, floor((log2 M - ceil(log2 k_eff) - 1) / 2)), M = prod p
+ *   e_i, f_j power-of-two row / column exponents; Q = RNE(x 2^(nu - e)), |Q| < 2^nu
+ *   per modulus one INT8 GEMM of centred residues, reduced mod p (exact INT32)
+ *   Z        = CRT of the residues = the exact integer product Q_A Q_B
+ *   P        = RNE(Z 2^(e_i + f_j - 2 nu)) (one rounding); C = alpha P + beta C (R7)
+ * Complex: the 4M real embedding of R9 (k_eff = 2k).  Same conventions, error
+ * codes and host/device pointer rules as the Ozaki-I routines above;
+ * parameter 14 (18 batched) is num_moduli in [1, 20].  Limits:
+ * k_eff <= 131071 (INT32 residue sums) else OZAKI_ERR_UNSUPPORTED; nu >= 1
+ * (enough moduli for k) else OZAKI_ERR_UNSUPPORTED.  Bit-identical to
+ * oracle/ozaki2.py.                                                         */
+int ozaki2_dgemm(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                 double alpha, const double *A, int64_t lda,
+                 const double *B, int64_t ldb,
+                 double beta, double *C, int64_t ldc, int num_moduli);
+int ozaki2_zgemm(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                 const double *alpha, const double *A, int64_t lda,
+                 const double *B, int64_t ldb,
+                 const double *beta, double *C, int64_t ldc, int num_moduli);
+int ozaki2_dgemm_strided_batched(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                                 double alpha, const double *A, int64_t lda, int64_t strideA,
+                                 const double *B, int64_t ldb, int64_t strideB,
+                                 double beta, double *C, int64_t ldc, int64_t strideC,
+                                 int64_t batch, int num_moduli);
+int ozaki2_zgemm_strided_batched(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                                 const double *alpha, const double *A, int64_t lda, int64_t strideA,
+                                 const double *B, int64_t ldb, int64_t strideB,
+                                 const double *beta, double *C, int64_t ldc, int64_t strideC,
+                                 int64_t batch, int num_moduli);
 
 /* --- streams, stats, errors --------------------------------------------- */
 /* stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);

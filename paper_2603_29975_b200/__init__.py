@@ -44,7 +44,7 @@ PHASES = ("k1_exponent", "k1_slice", "k2_gemm", "other")
 class Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in (
         "dgemm_calls", "zgemm_calls", "zgemm3m_calls", "batch_entries", "int8_gemm_equiv",
-        "int8_macs", "k_chunks", "nonfinite_rows", "kernel_launches")]
+        "int8_macs", "k_chunks", "nonfinite_rows", "kernel_launches", "crt_calls")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
@@ -72,6 +72,12 @@ def lib():
     L.ozaki_zgemm_strided_batched.argtypes = [c, c, i64, i64, i64, dP, p, i64, i64, p, i64, i64,
                                               dP, p, i64, i64, i64, i32]
     L.ozaki_zgemm3m_strided_batched.argtypes = L.ozaki_zgemm_strided_batched.argtypes
+    L.ozaki2_dgemm.argtypes = L.ozaki_dgemm.argtypes
+    L.ozaki2_zgemm.argtypes = L.ozaki_zgemm.argtypes
+    L.ozaki2_dgemm_strided_batched.argtypes = L.ozaki_dgemm_strided_batched.argtypes
+    L.ozaki2_zgemm_strided_batched.argtypes = L.ozaki_zgemm_strided_batched.argtypes
+    for fn in (L.ozaki2_dgemm, L.ozaki2_zgemm, L.ozaki2_dgemm_strided_batched, L.ozaki2_zgemm_strided_batched):
+        fn.restype = i32
     for f in ("ozaki_dgemm", "ozaki_zgemm", "ozaki_zgemm3m", "ozaki_dgemm_strided_batched",
               "ozaki_zgemm_strided_batched", "ozaki_zgemm3m_strided_batched"):
         getattr(L, f).restype = i32
@@ -248,6 +254,39 @@ def zgemm3m_strided_batched(transa, transb, alpha, A, B, beta, C, num_slices, st
     import torch
     return _batched(lib().ozaki_zgemm3m_strided_batched, torch.complex128, transa, transb, alpha,
                     A, B, beta, C, num_slices, stream, True)
+
+
+# ------------------------------------------------- Ozaki-II (CRT), NEXT-1
+def ozaki2_dgemm(transa, transb, alpha, A, B, beta, C, num_moduli, stream=None):
+    """C <- alpha op(A) op(B) + beta C via Ozaki-II with ``num_moduli`` moduli (R16..R20)."""
+    import torch
+    for x, nm in ((A, "A"), (B, "B"), (C, "C")):
+        _cuda(x, torch.float64, nm)
+    m, n, k = _dims(transa, transb, A, B)
+    if tuple(C.shape) != (m, n):
+        raise ValueError(f"C must be {m}x{n}")
+    _bind_stream(stream)
+    rc = lib().ozaki2_dgemm(_ch(transa), _ch(transb), m, n, k, float(alpha), A.data_ptr(), _ld(A),
+                            B.data_ptr(), _ld(B), float(beta), C.data_ptr(), _ld(C), int(num_moduli))
+    _check(rc, "ozaki2_dgemm")
+    return C
+
+
+def ozaki2_zgemm(transa, transb, alpha, A, B, beta, C, num_moduli, stream=None):
+    """Complex Ozaki-II through the 4M real embedding (k_eff = 2k)."""
+    return _zgemm(lib().ozaki2_zgemm, transa, transb, alpha, A, B, beta, C, num_moduli, stream)
+
+
+def ozaki2_dgemm_strided_batched(transa, transb, alpha, A, B, beta, C, num_moduli, stream=None):
+    import torch
+    return _batched(lib().ozaki2_dgemm_strided_batched, torch.float64, transa, transb, alpha, A, B,
+                    beta, C, num_moduli, stream, False)
+
+
+def ozaki2_zgemm_strided_batched(transa, transb, alpha, A, B, beta, C, num_moduli, stream=None):
+    import torch
+    return _batched(lib().ozaki2_zgemm_strided_batched, torch.complex128, transa, transb, alpha, A,
+                    B, beta, C, num_moduli, stream, True)
 
 
 # ------------------------------------------------------------- utilities

@@ -1,0 +1,242 @@
+// crt_kernel.cuh -- Ozaki-II reconstruction (NEXT-1, reading R20; PAPER.md:99
+// "uses the CRT to reconstruct the final result").
+//
+// Per output element: the n centred residues z_q (plane q) determine the
+// unique Z in (-M/2, M/2] with Z = z_q mod p_q; by the choice of nu (R17) Z is
+// the exact integer product Q_A . Q_B.  Computed exactly in 32-bit limbs:
+//   S = sum_q u_q W_q   (u_q = z_q mod p_q in [0, p_q), W_q = (M/p_q) inv_q < M)
+//   Z = S mod M  (quotient from an FP64 estimate, corrected to be exact), centred
+// then P = RNE(Z 2^(e_i + f_j - 2 nu)) with ONE rounding at the bit position
+// of the (normal or subnormal) result, and C = alpha P + beta C as R7.
+#pragma once
+#include <cstdint>
+
+#include "crt.cuh"
+#include "numerics.cuh"
+
+namespace ozk {
+
+constexpr int kCrtLimbs = 5;   // M < 2^160 (kMaxModuli = 20)
+
+struct CrtParams {
+    const int8_t *R;
+    int64_t plane_bytes, batch_bytes, rows_pad, groups;   // groups = padded columns / 16
+    const int32_t *ea, *fb;
+    int64_t Mp, Np, batch;
+    double *C;
+    int64_t ldc, strideC;
+    int32_t cplx, ab_unit, nu, n;
+    double alpha_r, alpha_i, beta_r, beta_i;
+    uint32_t p[kMaxModuli];
+    uint32_t W[kMaxModuli][kCrtLimbs];
+    uint32_t M[kCrtLimbs + 1];
+    uint32_t Mhalf[kCrtLimbs];
+    double Minv;                                            // ~1/M (quotient estimate)
+};
+
+// RNE(mag * 2^sh) for a non-negative integer mag of L 32-bit limbs, one rounding
+// at the precision of the result (53 bits, fewer when subnormal).
+template <int L>
+__device__ __forceinline__ double round_scaled(const uint32_t (&mag)[L], int sh) {
+    int top = -1;
+#pragma unroll
+    for (int l = 0; l < L; ++l)
+        if (mag[l]) top = l;
+    if (top < 0) return 0.0;
+    // T = the 64 bits below and including the leading one; sticky = anything lower
+    uint64_t hi = mag[top];
+    uint64_t T;
+    bool sticky = false;
+    const int lz = __clz(mag[top]);
+    const int BL = 32 * top + 32 - lz;                       // bit length of mag
+    {
+        const uint32_t m1 = top >= 1 ? mag[top - 1] : 0u, m2 = top >= 2 ? mag[top - 2] : 0u;
+        const uint64_t w96hi = (hi << 32) | m1;              // bits [32 top - 32, 32 top + 32)
+        // T = top 64 bits of (mag[top], m1, m2) left-aligned
+        T = lz ? ((w96hi << lz) | ((uint64_t)m2 >> (32 - lz))) : w96hi;
+        if (lz && (m2 << lz)) sticky = true;
+        if (!lz && m2) sticky = true;
+#pragma unroll
+        for (int l = 0; l < L; ++l)
+            if (l < top - 2 && mag[l]) sticky = true;
+    }
+    // T carries bits [BL-64, BL) of mag (zeros below when BL < 64); value = T 2^(BL-64+sh)
+    const int E = BL - 1 + sh;                               // binary exponent of the exact value
+    int prec = 53;
+    if (E < -1022) prec = 53 - (-1022 - E);                  // subnormal: fewer significant bits
+    if (prec < 0) return 0.0;                                // below half the smallest subnormal
+    const int d = 64 - prec;                                 // bits to drop from T (11..64)
+    uint64_t Rq;
+    if (d >= 64) {
+        Rq = 0;                                              // prec == 0: round(T 2^-64) in {0, 1}
+        const bool up = (T > (1ull << 63)) || (T == (1ull << 63) && sticky);
+        Rq = up ? 1 : 0;
+    } else {
+        Rq = T >> d;
+        const uint64_t rem = T & ((1ull << d) - 1), half = 1ull << (d - 1);
+        const bool up = rem > half || (rem == half && (sticky || (Rq & 1ull)));
+        Rq += up ? 1 : 0;
+    }
+    if (Rq == 0) return 0.0;
+    // exact: Rq < 2^54, and Rq 2^(BL-64+d+sh) is representable (normal or subnormal)
+    return ldexp_rn((double)Rq, BL - 64 + d + sh);
+}
+
+template <int L>
+__global__ void __launch_bounds__(256) k_crt(const __grid_constant__ CrtParams P) {
+    const int64_t per_b = P.rows_pad * P.groups;
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t b = blockIdx.y;
+    if (idx >= per_b) return;
+    const int64_t G = idx / P.rows_pad, row = idx - G * P.rows_pad;   // consecutive threads: consecutive rows
+    if (row >= P.Mp || G * 16 >= P.Np) return;
+    const int n = P.n;
+    const int8_t *src = P.R + b * P.batch_bytes + (G * P.rows_pad + row) * 16;
+    uint4 z[kMaxModuli];
+#pragma unroll
+    for (int q = 0; q < kMaxModuli; ++q)
+        if (q < n) z[q] = __ldg(reinterpret_cast<const uint4 *>(src + (int64_t)q * P.plane_bytes));
+    const int32_t e = __ldg(P.ea + b * P.Mp + row);
+    double Pv[16];
+#pragma unroll 1
+    for (int x = 0; x < 16; ++x) {
+        const int64_t col = G * 16 + x;
+        if (col >= P.Np) {
+            Pv[x] = 0.0;
+            continue;
+        }
+        // S = sum u_q W_q in 64-bit per-limb accumulators
+        unsigned long long acc[L];
+#pragma unroll
+        for (int l = 0; l < L; ++l) acc[l] = 0;
+#pragma unroll
+        for (int q = 0; q < kMaxModuli; ++q) {
+            if (q < n) {
+                const uint32_t word = (x < 4) ? z[q].x : (x < 8) ? z[q].y : (x < 12) ? z[q].z : z[q].w;
+                const int32_t zc = (int32_t)(int8_t)(word >> (8 * (x & 3)));
+                const uint32_t u = (uint32_t)(zc < 0 ? zc + (int32_t)P.p[q] : zc);
+#pragma unroll
+                for (int l = 0; l < L; ++l) acc[l] += (unsigned long long)u * P.W[q][l];
+            }
+        }
+        uint32_t s[L + 1];
+        unsigned long long c = 0;
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+            const unsigned long long t = acc[l] + c;
+            s[l] = (uint32_t)t;
+            c = t >> 32;
+        }
+        s[L] = (uint32_t)c;
+        // quotient estimate q = floor(S / M) (< 2^13), then S - q M exactly, corrected
+        double Sd = 0.0;
+#pragma unroll
+        for (int l = L; l >= 0; --l) Sd = Sd * 4294967296.0 + (double)s[l];
+        long long qe = (long long)(Sd * P.Minv);
+        if (qe < 0) qe = 0;
+        {
+            unsigned long long br = 0, cm = 0;
+#pragma unroll
+            for (int l = 0; l <= L; ++l) {
+                const unsigned long long prod = (unsigned long long)P.M[l] * (unsigned long long)qe + cm;
+                cm = prod >> 32;
+                const unsigned long long diff = (unsigned long long)s[l] - (uint32_t)prod - br;
+                s[l] = (uint32_t)diff;
+                br = (diff >> 63) & 1ull;
+            }
+            // s = S - qe M (two's complement over L+1 limbs); fix up by +-M
+            for (int it = 0; it < 2; ++it) {
+                if ((int32_t)s[L] < 0) {            // negative: add M
+                    unsigned long long cc = 0;
+#pragma unroll
+                    for (int l = 0; l <= L; ++l) {
+                        const unsigned long long t = (unsigned long long)s[l] + P.M[l] + cc;
+                        s[l] = (uint32_t)t;
+                        cc = t >> 32;
+                    }
+                } else {                             // s >= M ? subtract M
+                    bool ge = true;
+#pragma unroll
+                    for (int l = L; l >= 0; --l) {
+                        if (s[l] != P.M[l]) {
+                            ge = s[l] > P.M[l];
+                            break;
+                        }
+                    }
+                    if (ge) {
+                        unsigned long long bb = 0;
+#pragma unroll
+                        for (int l = 0; l <= L; ++l) {
+                            const unsigned long long t = (unsigned long long)s[l] - P.M[l] - bb;
+                            s[l] = (uint32_t)t;
+                            bb = (t >> 63) & 1ull;
+                        }
+                    }
+                }
+            }
+        }
+        // now 0 <= s < M; centre: s > M/2 -> Z = s - M < 0
+        bool neg = false;
+#pragma unroll
+        for (int l = L - 1; l >= 0; --l) {
+            if (s[l] != P.Mhalf[l]) {
+                neg = s[l] > P.Mhalf[l];
+                break;
+            }
+        }
+        uint32_t mag[L];
+        if (neg) {                                   // |Z| = M - s
+            unsigned long long bb = 0;
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
+                const unsigned long long t = (unsigned long long)P.M[l] - s[l] - bb;
+                mag[l] = (uint32_t)t;
+                bb = (t >> 63) & 1ull;
+            }
+        } else {
+#pragma unroll
+            for (int l = 0; l < L; ++l) mag[l] = s[l];
+        }
+        const int32_t f = __ldg(P.fb + b * P.Np + col);
+        double v;
+        if (e == kNonFinite || f == kNonFinite) v = __longlong_as_double(0x7ff8000000000000ll);
+        else {
+            v = round_scaled<L>(mag, e + f - 2 * P.nu);
+            if (neg) v = -v;
+        }
+        Pv[x] = v;
+    }
+    // C = alpha P + beta C (R7); complex: columns 2j / 2j+1 are Re / Im (R9)
+    if (!P.cplx) {
+        double *cp = P.C + b * P.strideC + row + G * 16 * P.ldc;
+        const bool beta0 = P.beta_r == 0.0;
+        for (int x = 0; x < 16; ++x) {
+            if (G * 16 + x >= P.Np) break;
+            if (P.ab_unit) *cp = Pv[x];
+            else *cp = beta0 ? __dmul_rn(P.alpha_r, Pv[x]) : __fma_rn(P.alpha_r, Pv[x], __dmul_rn(P.beta_r, *cp));
+            cp += P.ldc;
+        }
+    } else {
+        double2 *cp = reinterpret_cast<double2 *>(P.C) + b * P.strideC + row + G * 8 * P.ldc;
+        const bool beta0 = P.beta_r == 0.0 && P.beta_i == 0.0;
+        for (int c = 0; c < 8; ++c) {
+            if (G * 16 + 2 * c >= P.Np) break;
+            const double Pr = Pv[2 * c], Pi = Pv[2 * c + 1];
+            if (P.ab_unit) {
+                *cp = make_double2(plus_zero(Pr, Pi), plus_zero(Pi, Pr));
+            } else {
+                double tr = 0.0, ti = 0.0;
+                if (!beta0) {
+                    const double2 cv = *cp;
+                    tr = __fma_rn(P.beta_r, cv.x, -__dmul_rn(P.beta_i, cv.y));
+                    ti = __fma_rn(P.beta_r, cv.y, __dmul_rn(P.beta_i, cv.x));
+                }
+                *cp = make_double2(__fma_rn(P.alpha_r, Pr, __fma_rn(-P.alpha_i, Pi, tr)),
+                                   __fma_rn(P.alpha_r, Pi, __fma_rn(P.alpha_i, Pr, ti)));
+            }
+            cp += P.ldc;
+        }
+    }
+}
+
+}  // namespace ozk

@@ -19,7 +19,9 @@
 #include <string>
 #include <vector>
 
+#include "crt_kernel.cuh"
 #include "gemm.cuh"
+#include "gemm_crt.cuh"
 #include "gemm_lv.cuh"
 #include "gemm_lv2.cuh"
 #include "ozaki.h"
@@ -34,7 +36,7 @@ thread_local std::string t_err;
 
 struct Stats {
     std::atomic<uint64_t> dgemm{0}, zgemm{0}, zgemm3m{0}, entries{0}, equiv{0}, macs{0},
-        chunks{0}, launches{0};
+        chunks{0}, launches{0}, crt{0};
 } g_stats;
 
 // ------------------------------------------------------------ profiler
@@ -372,6 +374,8 @@ int launch_split(const Plan &P, const Operand &op, bool sideA, int8_t *slices, i
     sp.conj = op.conj;
     sp.s = P.s;
     sp.tile_h = sideA ? P.a_tile_h : P.b_tile_h;
+    sp.kbs_bytes = (int64_t)P.s * sp.tile_h * 32;   // layout [tile][kb][slice][block]
+    sp.ss_bytes = (int64_t)sp.tile_h * 32;
     sp.tiles = (sideA ? P.tiles_m : P.tiles_n) * (P.pair ? 2 : 1);
     sp.KB = P.KB;
     sp.kh = P.kh;
@@ -688,9 +692,10 @@ struct Call {
     int64_t ldb, sB;
     double *C;
     int64_t ldc, sC, batch;
-    int s;
+    int s;            // Ozaki-I: slices; Ozaki-II (crt): moduli count
     bool batched;
     int32_t *S_out;   // debug level dump (real only)
+    bool crt;         // Ozaki-II (NEXT-1)
 };
 
 int validate(const Call &c) {
@@ -708,7 +713,8 @@ int validate(const Call &c) {
     if (c.ldc < std::max<int64_t>(1, c.m)) return fail(b ? -15 : -13, "ldc too small");
     if (b && c.sC < 0) return fail(-16, "strideC < 0");
     if (b && c.batch < 0) return fail(-17, "batch < 0");
-    if (c.s < 1 || c.s > 16) return fail(b ? -18 : -14, "num_slices not in [1,16]");
+    if (!c.crt && (c.s < 1 || c.s > 16)) return fail(b ? -18 : -14, "num_slices not in [1,16]");
+    if (c.crt && (c.s < 1 || c.s > kMaxModuli)) return fail(b ? -18 : -14, "num_moduli not in [1,20]");
     return 0;
 }
 
@@ -843,6 +849,293 @@ int run_offload(const Call &c) {
     return rc;
 }
 
+// ============================================================ Ozaki-II (NEXT-1)
+// Host tables of reading R16..R20: the greedy moduli, the per-modulus
+// reduction constants of crt.cuh and the CRT weights W_q = (M/p_q) inv_q as
+// 32-bit limbs (exact multi-limb arithmetic on the host).
+struct CrtHost {
+    bool ready = false;
+    int n = 0, L = 0, bitlen = 0;
+    CrtTab tab{};
+    uint32_t W[kMaxModuli][kCrtLimbs]{};
+    uint32_t M[kCrtLimbs + 1]{};
+    uint32_t Mhalf[kCrtLimbs]{};
+    double Minv = 0.0;
+};
+CrtHost g_crt[kMaxModuli + 1];
+std::mutex g_crt_mu;
+
+int gcd_i(int a, int b) {
+    while (b) {
+        const int t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+const CrtHost &crt_tables(int n) {
+    std::lock_guard<std::mutex> lk(g_crt_mu);
+    CrtHost &h = g_crt[n];
+    if (h.ready) return h;
+    // R16: 256, then the largest integers coprime to all chosen
+    std::vector<int> mods{256};
+    for (int c = 255; (int)mods.size() < n && c >= 2; --c) {
+        bool ok = true;
+        for (int q : mods) ok = ok && gcd_i(c, q) == 1;
+        if (ok) mods.push_back(c);
+    }
+    h.n = n;
+    h.tab.n = n;
+    // M = prod p_q, little-endian 32-bit limbs
+    uint32_t M[kCrtLimbs + 1] = {1};
+    for (int q = 0; q < n; ++q) {
+        uint64_t carry = 0;
+        for (int l = 0; l <= kCrtLimbs; ++l) {
+            const uint64_t t = (uint64_t)M[l] * (uint32_t)mods[q] + carry;
+            M[l] = (uint32_t)t;
+            carry = t >> 32;
+        }
+    }
+    int top = kCrtLimbs;
+    while (top > 0 && M[top] == 0) --top;
+    h.bitlen = 32 * top + (32 - __builtin_clz(M[top]));
+    h.L = (h.bitlen + 31) / 32;
+    std::memcpy(h.M, M, sizeof M);
+    for (int l = 0; l < kCrtLimbs; ++l) h.Mhalf[l] = (M[l] >> 1) | (l + 1 <= kCrtLimbs ? (M[l + 1] << 31) : 0u);
+    double md = 0.0;
+    for (int l = kCrtLimbs; l >= 0; --l) md = md * 4294967296.0 + (double)M[l];
+    h.Minv = 1.0 / md;
+    for (int q = 0; q < n; ++q) {
+        const uint32_t p = (uint32_t)mods[q];
+        // Mq = M / p (exact), r = Mq mod p, inv = r^-1 mod p, W = Mq * inv (< M)
+        uint32_t Mq[kCrtLimbs + 1];
+        uint64_t rem = 0;
+        for (int l = kCrtLimbs; l >= 0; --l) {
+            const uint64_t cur = (rem << 32) | M[l];
+            Mq[l] = (uint32_t)(cur / p);
+            rem = cur % p;
+        }
+        uint64_t r = 0;
+        for (int l = kCrtLimbs; l >= 0; --l) r = ((r << 32) | Mq[l]) % p;
+        uint32_t inv = 0;
+        for (uint32_t x = 1; x < p; ++x)
+            if ((r * x) % p == 1) {
+                inv = x;
+                break;
+            }
+        if (p == 1) inv = 0;
+        uint64_t carry = 0;
+        for (int l = 0; l < kCrtLimbs; ++l) {
+            const uint64_t t = (uint64_t)Mq[l] * inv + carry;
+            h.W[q][l] = (uint32_t)t;
+            carry = t >> 32;
+        }
+        h.tab.p[q] = p;
+        h.tab.c21[q] = (uint32_t)((1ull << 21) % p);
+        h.tab.c42[q] = (uint32_t)((1ull << 42) % p);
+        h.tab.c16[q] = (uint32_t)((1ull << 16) % p);
+        h.tab.bias28[q] = (uint32_t)(((1ull << 28) + p - 1) / p * p);
+        h.tab.bias23[q] = (uint32_t)(((1ull << 23) + p - 1) / p * p);
+        h.tab.m40[q] = ((1ull << 40) + p - 1) / p;
+    }
+    h.ready = true;
+    return h;
+}
+
+// R17: nu = min(62, largest nu with 2^(2 nu + ceil(log2 k_eff) + 1) <= M), and
+// 2^x <= M  <=>  x <= bitlen(M) - 1.
+int crt_nu(const CrtHost &h, int64_t keff) {
+    int c = 0;
+    while ((1ll << c) < keff) ++c;
+    int nu = 0;
+    while (2 * (nu + 1) + c + 1 <= h.bitlen - 1) ++nu;
+    return std::min(nu, 62);
+}
+
+int run_crt(const Call &c, DevState *dev, cudaStream_t st) {
+    const int n = c.s;
+    const CrtHost &h = crt_tables(n);
+    const bool cplx = c.kind == KIND_4M;
+    const int64_t keff = cplx ? 2 * c.k : c.k;
+    if (keff > 131071)
+        return fail(OZAKI_ERR_UNSUPPORTED, "Ozaki-II: k_eff = %lld exceeds the INT32 residue-GEMM bound 131071",
+                    (long long)keff);
+    const int nu = crt_nu(h, keff);
+    if (nu < 1) return fail(OZAKI_ERR_UNSUPPORTED, "Ozaki-II: moduli budget too small for k (nu < 1)");
+    const int64_t Mp = c.m, Np = cplx ? 2 * c.n : c.n;
+    const int64_t kh = cplx ? rup(c.k, 32) : 0;
+    const int64_t Kp = cplx ? 2 * kh : rup(c.k, 32);
+    const int64_t KB = Kp / 32;
+    const int64_t tiles_m = (Mp + 255) / 256, tiles_n = (Np + 255) / 256;
+    const size_t a_bytes = al256((size_t)n * kCrtBlk * KB * 2 * tiles_m * c.batch);
+    const size_t b_bytes = al256((size_t)n * kCrtBlk * KB * 2 * tiles_n * c.batch);
+    const size_t ea_bytes = al256(sizeof(int32_t) * Mp * c.batch), fb_bytes = al256(sizeof(int32_t) * Np * c.batch);
+    const int64_t rows_pad = 256 * tiles_m, groups = 16 * tiles_n;
+    const int64_t batch_bytes = rows_pad * groups * 16;
+    const size_t plane_bytes = (size_t)batch_bytes * c.batch;
+    const size_t ws = a_bytes + b_bytes + ea_bytes + fb_bytes + al256(plane_bytes * n);
+    void *base = nullptr;
+    {
+        cudaError_t e = cudaMallocAsync(&base, ws, st);
+        if (e != cudaSuccess) return fail(OZAKI_ERR_ALLOC, "cudaMallocAsync(%zu): %s", ws, cudaGetErrorString(e));
+    }
+    int8_t *sa = (int8_t *)base;
+    int8_t *sb = sa + a_bytes;
+    int32_t *ea = (int32_t *)(sb + b_bytes);
+    int32_t *fb = (int32_t *)((char *)ea + ea_bytes);
+    int8_t *planes = (int8_t *)((char *)fb + fb_bytes);
+    int rc = 0;
+
+    // ---- K1': R17 quantisation + R18 residues (modulus-major slices, 128-row tiles)
+    auto split = [&](const Operand &op, bool sideA, int8_t *out, int32_t *exps) -> int {
+        SplitParams sp{};
+        sp.X = op.X;
+        sp.rs = op.rs;
+        sp.ls = op.ls;
+        sp.bstride = op.bstride;
+        sp.rows = op.rows;
+        sp.k = op.k;
+        sp.mode = op.mode;
+        sp.conj = op.conj;
+        sp.s = n;
+        sp.tile_h = 128;
+        sp.tiles = 2 * (sideA ? tiles_m : tiles_n);
+        sp.KB = KB;
+        sp.kh = kh;
+        sp.rows_out = (op.mode == SPLIT_B4M) ? 2 * op.rows : op.rows;
+        sp.rows_grid = (op.mode == SPLIT_B4M) ? sp.tiles * sp.tile_h / 2 : sp.tiles * sp.tile_h;
+        sp.out = out;
+        sp.exps = exps;
+        sp.nonfinite = dev->nonfinite;
+        sp.kbs_bytes = kCrtBlk;
+        sp.ss_bytes = (int64_t)KB * kCrtBlk;
+        sp.crt = h.tab;
+        sp.crt.nu = nu;
+        if (op.rows == 0) return 0;
+        const bool rcontig = (op.rs == 1);
+        const bool cx = op.mode != SPLIT_REAL;
+        dim3 grid((unsigned)((sp.rows_grid + 7) / 8), (unsigned)c.batch);
+        const int KW = cx ? 512 : 1024;
+        const size_t smem = (size_t)8 * (KW + (cx ? 1 : 2)) * (cx ? 16 : 8);
+        ProfScope ps(st, PH_SLICE);
+#define OZK_SPLIT2(RC, CX)                                                                           \
+        {                                                                                            \
+            static bool attr = false;                                                                \
+            if (!attr) {                                                                             \
+                cudaFuncSetAttribute(k_split_sm<8, RC, CX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     (int)smem);                                                     \
+                attr = true;                                                                         \
+            }                                                                                        \
+            k_split_sm<8, RC, CX, true><<<grid, 256, smem, st>>>(sp, KW);                           \
+        }
+        if (rcontig) { if (cx) OZK_SPLIT2(true, true) else OZK_SPLIT2(true, false) }
+        else { if (cx) OZK_SPLIT2(false, true) else OZK_SPLIT2(false, false) }
+#undef OZK_SPLIT2
+        CUDA_TRY(cudaGetLastError());
+        g_stats.launches += 1;
+        return 0;
+    };
+    const int ma = cplx ? SPLIT_A4M : SPLIT_REAL, mb = cplx ? SPLIT_B4M : SPLIT_REAL;
+    rc = split(view_A(c.A, c.ta, c.m, c.k, c.lda, c.sA, ma), true, sa, ea);
+    if (!rc) rc = split(view_B(c.B, c.tb, c.n, c.k, c.ldb, c.sB, mb), false, sb, fb);
+
+    // ---- K2': one INT8 GEMM per modulus, residues of the products (R19)
+    if (!rc) {
+        CrtGemmParams G;
+        std::memset(&G, 0, sizeof G);
+        int kpp = 4;
+        while (KB % kpp) kpp >>= 1;
+        G.kpp = kpp;
+        G.stage_bytes = (uint32_t)kpp * 2 * kCrtBlk;
+        G.stages = (int)std::min<int64_t>(8, (int64_t)(224 * 1024) / G.stage_bytes);
+        const size_t smem = (size_t)G.stages * G.stage_bytes + 1024 + 512;
+        G.batch = c.batch;
+        G.tiles_m = tiles_m;
+        G.tiles_n = tiles_n;
+        G.KB = KB;
+        G.R = planes;
+        G.plane_bytes = (int64_t)plane_bytes;
+        G.batch_bytes = batch_bytes;
+        G.rows_pad = rows_pad;
+        G.crt = h.tab;
+        G.crt.nu = nu;
+        rc = rows_map(&G.tmA, sa, a_bytes, (uint32_t)kpp * (kCrtBlk / 256));
+        if (!rc) rc = rows_map(&G.tmB, sb, b_bytes, (uint32_t)kpp * (kCrtBlk / 256));
+        if (!rc) {
+            static std::atomic<size_t> done{0};
+            if (done.load() < smem) {
+                CUDA_TRY(cudaFuncSetAttribute(k_gemm_crt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                done.store(smem);
+            }
+            const int64_t tiles = c.batch * tiles_m * tiles_n;
+            const unsigned pairs = (unsigned)std::min<int64_t>(tiles, dev->sms / 2);
+            {
+                ProfScope ps(st, PH_GEMM);
+                k_gemm_crt<<<2 * pairs, kCrtThreads, smem, st>>>(G);
+            }
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) rc = fail(OZAKI_ERR_CUDA, "k_gemm_crt: %s", cudaGetErrorString(e));
+            g_stats.launches += 1;
+        }
+    }
+    // ---- K3': CRT reconstruction + one rounding + alpha/beta (R20, R7)
+    if (!rc) {
+        CrtParams Q;
+        std::memset(&Q, 0, sizeof Q);
+        Q.R = planes;
+        Q.plane_bytes = (int64_t)plane_bytes;
+        Q.batch_bytes = batch_bytes;
+        Q.rows_pad = rows_pad;
+        Q.groups = groups;
+        Q.ea = ea;
+        Q.fb = fb;
+        Q.Mp = Mp;
+        Q.Np = Np;
+        Q.batch = c.batch;
+        Q.C = c.C;
+        Q.ldc = c.ldc;
+        Q.strideC = c.sC;
+        Q.cplx = cplx ? 1 : 0;
+        Q.ab_unit = (c.al[0] == 1.0 && c.al[1] == 0.0 && c.be[0] == 0.0 && c.be[1] == 0.0) ? 1 : 0;
+        Q.nu = nu;
+        Q.n = n;
+        Q.alpha_r = c.al[0];
+        Q.alpha_i = c.al[1];
+        Q.beta_r = c.be[0];
+        Q.beta_i = c.be[1];
+        for (int q = 0; q < n; ++q) {
+            Q.p[q] = h.tab.p[q];
+            for (int l = 0; l < kCrtLimbs; ++l) Q.W[q][l] = h.W[q][l];
+        }
+        std::memcpy(Q.M, h.M, sizeof Q.M);
+        std::memcpy(Q.Mhalf, h.Mhalf, sizeof Q.Mhalf);
+        Q.Minv = h.Minv;
+        dim3 grid((unsigned)((rows_pad * groups + 255) / 256), (unsigned)c.batch);
+        {
+            ProfScope ps(st, PH_OTHER);
+            switch (h.L) {
+                case 1: k_crt<1><<<grid, 256, 0, st>>>(Q); break;
+                case 2: k_crt<2><<<grid, 256, 0, st>>>(Q); break;
+                case 3: k_crt<3><<<grid, 256, 0, st>>>(Q); break;
+                case 4: k_crt<4><<<grid, 256, 0, st>>>(Q); break;
+                default: k_crt<5><<<grid, 256, 0, st>>>(Q); break;
+            }
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = fail(OZAKI_ERR_CUDA, "k_crt: %s", cudaGetErrorString(e));
+        g_stats.launches += 1;
+    }
+    cudaFreeAsync(base, st);
+    if (rc) return rc;
+    g_stats.entries += (uint64_t)c.batch;
+    g_stats.equiv += (uint64_t)n * (cplx ? 4 : 1) * (uint64_t)c.batch;
+    g_stats.macs += (uint64_t)n * (uint64_t)(2 * tiles_m * 128) * (uint64_t)(tiles_n * 256) * (uint64_t)Kp *
+                    (uint64_t)c.batch;
+    g_stats.crt += 1;
+    return 0;
+}
+
 int run(const Call &c0) {
     t_err.clear();
     if (int rc = validate(c0)) return rc;
@@ -895,6 +1188,8 @@ int run(const Call &c0) {
         g_stats.launches += 1;
         return 0;
     }
+
+    if (c.crt) return run_crt(c, dev, st);
 
     Plan P;
     const Kind pk = (c.kind == KIND_4M) ? KIND_4M : KIND_REAL;
@@ -991,6 +1286,15 @@ Call make_call(Kind kind, char ta, char tb, int64_t m, int64_t n, int64_t k, con
     return c;
 }
 
+Call make_call_crt(Kind kind, char ta, char tb, int64_t m, int64_t n, int64_t k, const double *al,
+                   const double *A, int64_t lda, int64_t sA, const double *B, int64_t ldb, int64_t sB,
+                   const double *be, double *C, int64_t ldc, int64_t sC, int64_t batch, int nmod,
+                   bool batched) {
+    Call c = make_call(kind, ta, tb, m, n, k, al, A, lda, sA, B, ldb, sB, be, C, ldc, sC, batch, nmod, batched);
+    c.crt = true;
+    return c;
+}
+
 }  // namespace
 
 // =========================================================================
@@ -1046,6 +1350,39 @@ int ozaki_zgemm3m_strided_batched(char transa, char transb, int64_t m, int64_t n
                          beta, C, ldc, strideC, batch, num_slices, true));
 }
 
+// ---- Ozaki-II (CRT), NEXT-1
+int ozaki2_dgemm(char transa, char transb, int64_t m, int64_t n, int64_t k, double alpha,
+                 const double *A, int64_t lda, const double *B, int64_t ldb, double beta, double *C,
+                 int64_t ldc, int num_moduli) {
+    const double al[2] = {alpha, 0.0}, be[2] = {beta, 0.0};
+    return run(make_call_crt(KIND_REAL, transa, transb, m, n, k, al, A, lda, 0, B, ldb, 0, be, C, ldc, 0, 1,
+                             num_moduli, false));
+}
+
+int ozaki2_zgemm(char transa, char transb, int64_t m, int64_t n, int64_t k, const double *alpha,
+                 const double *A, int64_t lda, const double *B, int64_t ldb, const double *beta,
+                 double *C, int64_t ldc, int num_moduli) {
+    return run(make_call_crt(KIND_4M, transa, transb, m, n, k, alpha, A, lda, 0, B, ldb, 0, beta, C, ldc, 0, 1,
+                             num_moduli, false));
+}
+
+int ozaki2_dgemm_strided_batched(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                                 double alpha, const double *A, int64_t lda, int64_t strideA,
+                                 const double *B, int64_t ldb, int64_t strideB, double beta, double *C,
+                                 int64_t ldc, int64_t strideC, int64_t batch, int num_moduli) {
+    const double al[2] = {alpha, 0.0}, be[2] = {beta, 0.0};
+    return run(make_call_crt(KIND_REAL, transa, transb, m, n, k, al, A, lda, strideA, B, ldb, strideB, be, C,
+                             ldc, strideC, batch, num_moduli, true));
+}
+
+int ozaki2_zgemm_strided_batched(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                                 const double *alpha, const double *A, int64_t lda, int64_t strideA,
+                                 const double *B, int64_t ldb, int64_t strideB, const double *beta,
+                                 double *C, int64_t ldc, int64_t strideC, int64_t batch, int num_moduli) {
+    return run(make_call_crt(KIND_4M, transa, transb, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta,
+                             C, ldc, strideC, batch, num_moduli, true));
+}
+
 int ozaki_set_stream(void *stream) {
     t_stream = (cudaStream_t)stream;
     return 0;
@@ -1069,6 +1406,7 @@ int ozaki_get_stats(ozaki_stats_t *out) {
     out->int8_macs = g_stats.macs;
     out->k_chunks = g_stats.chunks;
     out->kernel_launches = g_stats.launches;
+    out->crt_calls = g_stats.crt;
     uint64_t nf = 0;
     std::lock_guard<std::mutex> lk(g_mu);
     for (int d = 0; d < kMaxDev; ++d) {

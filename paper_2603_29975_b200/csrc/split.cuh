@@ -20,6 +20,7 @@
 
 #include <type_traits>
 
+#include "crt.cuh"
 #include "numerics.cuh"
 
 namespace ozk {
@@ -52,6 +53,9 @@ struct SplitParams {
     int8_t *out;          // tiled slices
     int32_t *exps;        // [batch][rows_out]
     unsigned long long *nonfinite;   // device counter (rows/cols with Inf/NaN)
+    int64_t kbs_bytes;    // bytes between k-blocks of one tile (Ozaki-I: s*blk; Ozaki-II: blk)
+    int64_t ss_bytes;     // bytes between slices / moduli  (Ozaki-I: blk;  Ozaki-II: KB*blk)
+    CrtTab crt;           // Ozaki-II constants (CRT instantiation only)
 };
 
 __device__ __forceinline__ bool is_complex_mode(int m) { return m != SPLIT_REAL; }
@@ -74,9 +78,8 @@ __device__ __forceinline__ uint64_t mag_bits(const SplitParams &p, const void *b
     }
 }
 
-__device__ __forceinline__ void reduce_and_store(const SplitParams &p, int64_t b, int64_t r,
-                                                 uint64_t maxb, uint32_t nf) {
-    int32_t e = nf ? kNonFinite : exponent_from_maxbits(maxb);
+__device__ __forceinline__ void reduce_and_store(const SplitParams &p, int64_t b, int64_t r, int32_t e,
+                                                 uint32_t nf) {
     int32_t *ex = p.exps + b * p.rows_out;
     if (p.mode == SPLIT_B4M) {
         ex[2 * r] = e;
@@ -202,8 +205,11 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
-template <int SMAX, bool RCONTIG, bool CPLX>
-__global__ void __launch_bounds__(256) k_split_sm(const SplitParams p, int KW) {
+// CRT = false: Ozaki-I digits (R3, R4); CRT = true: Ozaki-II exponent, int64
+// quantisation and centred residues per modulus (R17, R18), written
+// modulus-major within a tile (contiguous k-blocks per modulus).
+template <int SMAX, bool RCONTIG, bool CPLX, bool CRT = false>
+__global__ void __launch_bounds__(256) k_split_sm(const __grid_constant__ SplitParams p, int KW) {
     extern __shared__ __align__(16) uint8_t sbuf[];
     __shared__ uint64_t s_max[8][33];
     __shared__ uint32_t s_nf[8][33];
@@ -222,13 +228,14 @@ __global__ void __launch_bounds__(256) k_split_sm(const SplitParams p, int KW) {
     const int64_t kpad = four_m ? p.kh : p.KB * 32;  // input depth covered by output chunks
     const int64_t nwin = (kpad + KW - 1) / KW;
     const int nrows = (int)min((int64_t)8, max((int64_t)0, p.rows - r0));
-    const int64_t blk = (int64_t)p.tile_h * 32;      // bytes between slices of one (tile, k-block)
-    const int64_t kbs = (int64_t)p.s * blk;          // bytes between k-blocks of one tile
+    const int64_t blk = (int64_t)p.tile_h * 32;      // bytes of one (tile, k-block, slice) block
+    const int64_t kbs = p.kbs_bytes;                 // bytes between k-blocks of one tile
+    const int64_t tile_bytes = (int64_t)p.s * p.KB * blk;
 
     if (tid < 16) {   // output rows of this block: r0..r0+7 (B4M: 2r0 .. 2r0+15)
         const int64_t R = (p.mode == SPLIT_B4M ? 2 * r0 : r0) + tid;
         const int64_t tile = R / p.tile_h, rr = R % p.tile_h;
-        s_rowbase[tid] = p.out + (b * p.tiles + tile) * p.KB * kbs + (rr >> 3) * 256 + (rr & 7) * 16;
+        s_rowbase[tid] = p.out + (b * p.tiles + tile) * tile_bytes + (rr >> 3) * 256 + (rr & 7) * 16;
     }
 
     auto load_window = [&](int64_t w0) {
@@ -297,11 +304,11 @@ __global__ void __launch_bounds__(256) k_split_sm(const SplitParams p, int KW) {
         if (lane == 0) {
             int32_t e = 0;
             if (row < nrows) {
-                reduce_and_store(p, b, r0 + row, m, nf);
-                e = nf ? kNonFinite : exponent_from_maxbits(m);
+                e = nf ? kNonFinite : (CRT ? crt_exponent(m, p.crt.nu) : exponent_from_maxbits(m));
+                reduce_and_store(p, b, r0 + row, e, nf);
             }
             s_e[row] = e;
-            const int sh = 8 * p.s - 1 - e;               // 2^(P-e) as one exact DMUL when representable
+            const int sh = (CRT ? p.crt.nu : 8 * p.s - 1) - e;   // 2^(P-e) as one exact DMUL when representable
             s_scale[row] = (sh >= -1022 && sh <= 1023) ? pow2(sh) : 0.0;
         }
         __syncthreads();
@@ -330,11 +337,15 @@ __global__ void __launch_bounds__(256) k_split_sm(const SplitParams p, int KW) {
             const int hh = (int)((l0 >> 3) & 1);
             const int64_t coff = (c >> 1) * kbs + (c & 1) * 128 + hh * 8;            // first half
             const int64_t coff2 = ((c + c2off) >> 1) * kbs + ((c + c2off) & 1) * 128 + hh * 8;   // second half
+            auto emit = [&](const double (&vv)[8], int8_t *d0, int8_t *d1, int8_t *dn) {
+                if constexpr (CRT) residues_store8(vv, scale, e, p.crt, d0, d1, dn, p.ss_bytes);
+                else digits_store8<SMAX>(vv, scale, e, p.s, d0, d1, dn, blk);
+            };
             if constexpr (!CPLX) {
                 double v[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) v[i] = (i < nvalid) ? src[i] : 0.0;
-                digits_store8<SMAX>(v, scale, e, p.s, s_rowbase[row] + coff, nullptr, nullptr, blk);
+                emit(v, s_rowbase[row] + coff, nullptr, nullptr);
             } else {
                 // one component at a time (8 live values): 0 = Re, 1 = Im (conj applied), 2 = Re + Im
                 auto comp8 = [&](int comp, double (&v)[8]) {
@@ -356,21 +367,19 @@ __global__ void __launch_bounds__(256) k_split_sm(const SplitParams p, int KW) {
                     case SPLIT_IM:
                     case SPLIT_SUM:
                         comp8(p.mode == SPLIT_RE ? 0 : (p.mode == SPLIT_IM ? 1 : 2), v);
-                        digits_store8<SMAX>(v, scale, e, p.s, s_rowbase[row] + coff, nullptr, nullptr, blk);
+                        emit(v, s_rowbase[row] + coff, nullptr, nullptr);
                         break;
                     case SPLIT_A4M:   // row r = [Re | Im]
                         comp8(0, v);
-                        digits_store8<SMAX>(v, scale, e, p.s, s_rowbase[row] + coff, nullptr, nullptr, blk);
+                        emit(v, s_rowbase[row] + coff, nullptr, nullptr);
                         comp8(1, v);
-                        digits_store8<SMAX>(v, scale, e, p.s, s_rowbase[row] + coff2, nullptr, nullptr, blk);
+                        emit(v, s_rowbase[row] + coff2, nullptr, nullptr);
                         break;
                     default:          // SPLIT_B4M: 2r = [Re | -Im], 2r+1 = [Im | Re] (R9)
                         comp8(0, v);
-                        digits_store8<SMAX>(v, scale, e, p.s, s_rowbase[2 * row] + coff,
-                                            s_rowbase[2 * row + 1] + coff2, nullptr, blk);
+                        emit(v, s_rowbase[2 * row] + coff, s_rowbase[2 * row + 1] + coff2, nullptr);
                         comp8(1, v);
-                        digits_store8<SMAX>(v, scale, e, p.s, s_rowbase[2 * row + 1] + coff, nullptr,
-                                            s_rowbase[2 * row] + coff2, blk);
+                        emit(v, s_rowbase[2 * row + 1] + coff, nullptr, s_rowbase[2 * row] + coff2);
                         break;
                 }
             }
