@@ -118,7 +118,27 @@ __device__ __forceinline__ void residues_store8(const double (&v)[8], double sca
         q2[i] = (int32_t)(Q >> 42);
     }
     const int nw = (t.n + 3) >> 2;
-    for (int j = 0; j < nw; ++j) {
+    if (!dstn) {
+        for (int j = 0; j < nw; ++j) {
+            uint32_t w[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[i] = 0;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                const int q = 4 * j + qq;
+                if (q < t.n) {
+                    const uint32_t p = t.p[q];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        w[i] |= centre_byte(residue_u(q2[i], q1[i], q0[i], t, q), p) << (8 * qq);
+                }
+            }
+            crt_store_word(w, j, t.n, dst0, ss);
+            if (dst1) crt_store_word(w, j, t.n, dst1, ss);
+        }
+        return;
+    }
+    for (int j = 0; j < nw; ++j) {   // B4M: also the residues of -Q (the -Im block, R9)
         uint32_t w[8], wn[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -140,7 +160,7 @@ __device__ __forceinline__ void residues_store8(const double (&v)[8], double sca
         }
         crt_store_word(w, j, t.n, dst0, ss);
         if (dst1) crt_store_word(w, j, t.n, dst1, ss);
-        if (dstn) crt_store_word(wn, j, t.n, dstn, ss);
+        crt_store_word(wn, j, t.n, dstn, ss);
     }
 }
 

@@ -31,7 +31,7 @@ struct CrtParams {
     uint32_t W[kMaxModuli][kCrtLimbs];
     uint32_t M[kCrtLimbs + 1];
     uint32_t Mhalf[kCrtLimbs];
-    double Minv;                                            // ~1/M (quotient estimate)
+    double Minv;                                            // 2^(32(L-1)) / M (quotient from the top two limbs)
 };
 
 // RNE(mag * 2^sh) for a non-negative integer mag of L 32-bit limbs, one rounding
@@ -82,71 +82,73 @@ __device__ __forceinline__ double round_scaled(const uint32_t (&mag)[L], int sh)
     return ldexp_rn((double)Rq, BL - 64 + d + sh);
 }
 
+// One thread per (row, 4 consecutive columns): 4 lanes share one 16-byte plane
+// chunk, so a warp reads 8 rows x 16 B = 128 contiguous bytes per plane.
 template <int L>
 __global__ void __launch_bounds__(256) k_crt(const __grid_constant__ CrtParams P) {
-    const int64_t per_b = P.rows_pad * P.groups;
+    const int64_t per_b = P.rows_pad * P.groups * 4;
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t b = blockIdx.y;
     if (idx >= per_b) return;
-    const int64_t G = idx / P.rows_pad, row = idx - G * P.rows_pad;   // consecutive threads: consecutive rows
-    if (row >= P.Mp || G * 16 >= P.Np) return;
+    const int quad = (int)(idx & 3);
+    const int64_t rg = idx >> 2;
+    const int64_t G = rg / P.rows_pad, row = rg - G * P.rows_pad;
+    const int64_t col0 = G * 16 + quad * 4;
+    if (row >= P.Mp || col0 >= P.Np) return;
     const int n = P.n;
-    const int8_t *src = P.R + b * P.batch_bytes + (G * P.rows_pad + row) * 16;
-    uint4 z[kMaxModuli];
+    const int8_t *src = P.R + b * P.batch_bytes + (G * P.rows_pad + row) * 16 + quad * 4;
+    // S_x = sum_q u_q W_q for the 4 elements, 64-bit accumulator per limb
+    unsigned long long acc[4][L];
 #pragma unroll
-    for (int q = 0; q < kMaxModuli; ++q)
-        if (q < n) z[q] = __ldg(reinterpret_cast<const uint4 *>(src + (int64_t)q * P.plane_bytes));
-    const int32_t e = __ldg(P.ea + b * P.Mp + row);
-    double Pv[16];
-#pragma unroll 1
-    for (int x = 0; x < 16; ++x) {
-        const int64_t col = G * 16 + x;
-        if (col >= P.Np) {
-            Pv[x] = 0.0;
-            continue;
-        }
-        // S = sum u_q W_q in 64-bit per-limb accumulators
-        unsigned long long acc[L];
+    for (int x = 0; x < 4; ++x)
 #pragma unroll
-        for (int l = 0; l < L; ++l) acc[l] = 0;
+        for (int l = 0; l < L; ++l) acc[x][l] = 0;
 #pragma unroll
-        for (int q = 0; q < kMaxModuli; ++q) {
-            if (q < n) {
-                const uint32_t word = (x < 4) ? z[q].x : (x < 8) ? z[q].y : (x < 12) ? z[q].z : z[q].w;
-                const int32_t zc = (int32_t)(int8_t)(word >> (8 * (x & 3)));
-                const uint32_t u = (uint32_t)(zc < 0 ? zc + (int32_t)P.p[q] : zc);
+    for (int q = 0; q < kMaxModuli; ++q) {
+        if (q < n) {
+            const uint32_t word = __ldg(reinterpret_cast<const uint32_t *>(src + (int64_t)q * P.plane_bytes));
+            const uint32_t p = P.p[q];
 #pragma unroll
-                for (int l = 0; l < L; ++l) acc[l] += (unsigned long long)u * P.W[q][l];
+            for (int x = 0; x < 4; ++x) {
+                const int32_t zc = (int32_t)(int8_t)(word >> (8 * x));
+                const uint32_t u = (uint32_t)(zc < 0 ? zc + (int32_t)p : zc);
+#pragma unroll
+                for (int l = 0; l < L; ++l) acc[x][l] += (unsigned long long)u * P.W[q][l];
             }
         }
+    }
+    const int32_t e = __ldg(P.ea + b * P.Mp + row);
+    double Pv[4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+        const int64_t col = col0 + x;
         uint32_t s[L + 1];
         unsigned long long c = 0;
 #pragma unroll
         for (int l = 0; l < L; ++l) {
-            const unsigned long long t = acc[l] + c;
+            const unsigned long long t = acc[x][l] + c;
             s[l] = (uint32_t)t;
             c = t >> 32;
         }
         s[L] = (uint32_t)c;
-        // quotient estimate q = floor(S / M) (< 2^13), then S - q M exactly, corrected
-        double Sd = 0.0;
-#pragma unroll
-        for (int l = L; l >= 0; --l) Sd = Sd * 4294967296.0 + (double)s[l];
-        long long qe = (long long)(Sd * P.Minv);
+        // q = floor(S / M) < 2^13 from the top 64 bits of S (error < 1), then exact fix-up
+        const unsigned long long top = ((unsigned long long)s[L] << 32) | s[L - 1];
+        long long qe = (long long)(__ull2double_rn(top) * P.Minv);
         if (qe < 0) qe = 0;
         {
-            unsigned long long br = 0, cm = 0;
+            unsigned long long cm = 0;
+            uint32_t br = 0;
 #pragma unroll
             for (int l = 0; l <= L; ++l) {
                 const unsigned long long prod = (unsigned long long)P.M[l] * (unsigned long long)qe + cm;
                 cm = prod >> 32;
                 const unsigned long long diff = (unsigned long long)s[l] - (uint32_t)prod - br;
                 s[l] = (uint32_t)diff;
-                br = (diff >> 63) & 1ull;
+                br = (uint32_t)(diff >> 63);
             }
-            // s = S - qe M (two's complement over L+1 limbs); fix up by +-M
+#pragma unroll
             for (int it = 0; it < 2; ++it) {
-                if ((int32_t)s[L] < 0) {            // negative: add M
+                if ((int32_t)s[L] < 0) {                     // negative: add M
                     unsigned long long cc = 0;
 #pragma unroll
                     for (int l = 0; l <= L; ++l) {
@@ -154,85 +156,87 @@ __global__ void __launch_bounds__(256) k_crt(const __grid_constant__ CrtParams P
                         s[l] = (uint32_t)t;
                         cc = t >> 32;
                     }
-                } else {                             // s >= M ? subtract M
-                    bool ge = true;
+                } else {                                      // s >= M: subtract M
+                    unsigned long long bb = 0;
+                    uint32_t d[L + 1];
 #pragma unroll
-                    for (int l = L; l >= 0; --l) {
-                        if (s[l] != P.M[l]) {
-                            ge = s[l] > P.M[l];
-                            break;
-                        }
+                    for (int l = 0; l <= L; ++l) {
+                        const unsigned long long t = (unsigned long long)s[l] - P.M[l] - bb;
+                        d[l] = (uint32_t)t;
+                        bb = (t >> 63) & 1ull;
                     }
-                    if (ge) {
-                        unsigned long long bb = 0;
+                    if (!bb) {
 #pragma unroll
-                        for (int l = 0; l <= L; ++l) {
-                            const unsigned long long t = (unsigned long long)s[l] - P.M[l] - bb;
-                            s[l] = (uint32_t)t;
-                            bb = (t >> 63) & 1ull;
-                        }
+                        for (int l = 0; l <= L; ++l) s[l] = d[l];
                     }
                 }
             }
         }
-        // now 0 <= s < M; centre: s > M/2 -> Z = s - M < 0
-        bool neg = false;
+        // 0 <= s < M; centre: s > M/2 -> Z = s - M
+        unsigned long long bb = 0;
+        uint32_t d[L];
 #pragma unroll
-        for (int l = L - 1; l >= 0; --l) {
-            if (s[l] != P.Mhalf[l]) {
-                neg = s[l] > P.Mhalf[l];
-                break;
-            }
+        for (int l = 0; l < L; ++l) {                        // d = Mhalf - s (borrow -> s > Mhalf)
+            const unsigned long long t = (unsigned long long)P.Mhalf[l] - s[l] - bb;
+            d[l] = (uint32_t)t;
+            bb = (t >> 63) & 1ull;
         }
+        const bool neg = bb != 0;
         uint32_t mag[L];
-        if (neg) {                                   // |Z| = M - s
-            unsigned long long bb = 0;
+        if (neg) {                                           // |Z| = M - s
+            unsigned long long b2 = 0;
 #pragma unroll
             for (int l = 0; l < L; ++l) {
-                const unsigned long long t = (unsigned long long)P.M[l] - s[l] - bb;
+                const unsigned long long t = (unsigned long long)P.M[l] - s[l] - b2;
                 mag[l] = (uint32_t)t;
-                bb = (t >> 63) & 1ull;
+                b2 = (t >> 63) & 1ull;
             }
         } else {
 #pragma unroll
             for (int l = 0; l < L; ++l) mag[l] = s[l];
         }
-        const int32_t f = __ldg(P.fb + b * P.Np + col);
-        double v;
-        if (e == kNonFinite || f == kNonFinite) v = __longlong_as_double(0x7ff8000000000000ll);
-        else {
-            v = round_scaled<L>(mag, e + f - 2 * P.nu);
-            if (neg) v = -v;
+        double v = 0.0;
+        if (col < P.Np) {
+            const int32_t f = __ldg(P.fb + b * P.Np + col);
+            if (e == kNonFinite || f == kNonFinite) v = __longlong_as_double(0x7ff8000000000000ll);
+            else {
+                v = round_scaled<L>(mag, e + f - 2 * P.nu);
+                if (neg) v = -v;
+            }
         }
         Pv[x] = v;
     }
     // C = alpha P + beta C (R7); complex: columns 2j / 2j+1 are Re / Im (R9)
     if (!P.cplx) {
-        double *cp = P.C + b * P.strideC + row + G * 16 * P.ldc;
-        const bool beta0 = P.beta_r == 0.0;
-        for (int x = 0; x < 16; ++x) {
-            if (G * 16 + x >= P.Np) break;
-            if (P.ab_unit) *cp = Pv[x];
-            else *cp = beta0 ? __dmul_rn(P.alpha_r, Pv[x]) : __fma_rn(P.alpha_r, Pv[x], __dmul_rn(P.beta_r, *cp));
+        double *cp = P.C + b * P.strideC + row + col0 * P.ldc;
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+            if (col0 + x < P.Np) {
+                if (P.ab_unit) *cp = Pv[x];
+                else *cp = (P.beta_r == 0.0) ? __dmul_rn(P.alpha_r, Pv[x])
+                                             : __fma_rn(P.alpha_r, Pv[x], __dmul_rn(P.beta_r, *cp));
+            }
             cp += P.ldc;
         }
     } else {
-        double2 *cp = reinterpret_cast<double2 *>(P.C) + b * P.strideC + row + G * 8 * P.ldc;
+        double2 *cp = reinterpret_cast<double2 *>(P.C) + b * P.strideC + row + (col0 >> 1) * P.ldc;
         const bool beta0 = P.beta_r == 0.0 && P.beta_i == 0.0;
-        for (int c = 0; c < 8; ++c) {
-            if (G * 16 + 2 * c >= P.Np) break;
-            const double Pr = Pv[2 * c], Pi = Pv[2 * c + 1];
-            if (P.ab_unit) {
-                *cp = make_double2(plus_zero(Pr, Pi), plus_zero(Pi, Pr));
-            } else {
-                double tr = 0.0, ti = 0.0;
-                if (!beta0) {
-                    const double2 cv = *cp;
-                    tr = __fma_rn(P.beta_r, cv.x, -__dmul_rn(P.beta_i, cv.y));
-                    ti = __fma_rn(P.beta_r, cv.y, __dmul_rn(P.beta_i, cv.x));
+#pragma unroll
+        for (int c2 = 0; c2 < 2; ++c2) {
+            if (col0 + 2 * c2 < P.Np) {
+                const double Pr = Pv[2 * c2], Pi = Pv[2 * c2 + 1];
+                if (P.ab_unit) {
+                    *cp = make_double2(plus_zero(Pr, Pi), plus_zero(Pi, Pr));
+                } else {
+                    double tr = 0.0, ti = 0.0;
+                    if (!beta0) {
+                        const double2 cv = *cp;
+                        tr = __fma_rn(P.beta_r, cv.x, -__dmul_rn(P.beta_i, cv.y));
+                        ti = __fma_rn(P.beta_r, cv.y, __dmul_rn(P.beta_i, cv.x));
+                    }
+                    *cp = make_double2(__fma_rn(P.alpha_r, Pr, __fma_rn(-P.alpha_i, Pi, tr)),
+                                       __fma_rn(P.alpha_r, Pi, __fma_rn(P.alpha_i, Pr, ti)));
                 }
-                *cp = make_double2(__fma_rn(P.alpha_r, Pr, __fma_rn(-P.alpha_i, Pi, tr)),
-                                   __fma_rn(P.alpha_r, Pi, __fma_rn(P.alpha_i, Pr, ti)));
             }
             cp += P.ldc;
         }

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstdarg>
 #include <cstdint>
@@ -1110,8 +1111,8 @@ int run_crt(const Call &c, DevState *dev, cudaStream_t st) {
         }
         std::memcpy(Q.M, h.M, sizeof Q.M);
         std::memcpy(Q.Mhalf, h.Mhalf, sizeof Q.Mhalf);
-        Q.Minv = h.Minv;
-        dim3 grid((unsigned)((rows_pad * groups + 255) / 256), (unsigned)c.batch);
+        Q.Minv = std::ldexp(h.Minv, 32 * (h.L - 1));   // top-two-limb quotient estimate
+        dim3 grid((unsigned)((rows_pad * groups * 4 + 255) / 256), (unsigned)c.batch);
         {
             ProfScope ps(st, PH_OTHER);
             switch (h.L) {
