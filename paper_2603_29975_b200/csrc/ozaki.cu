@@ -390,17 +390,21 @@ int launch_split(const Plan &P, const Operand &op, bool sideA, int8_t *slices, i
     const bool cplx = op.mode != SPLIT_REAL;
     dim3 grid((unsigned)((sp.rows_grid + 7) / 8), (unsigned)P.batch);
     // SMEM window: 8 rows x KW elements (+ pad), 64 KB
-    const int KW = cplx ? 512 : 1024;
+    int KW = cplx ? 512 : 1024;
+    if (const char *kw = getenv("OZAKI_SPLIT_KW")) {   // tuning hook: window elements per row
+        const int v = atoi(kw);
+        if (v >= 64 && v <= 1024) KW = cplx ? std::min(v, 512) : v;
+    }
     const size_t smem = (size_t)8 * (KW + (cplx ? 1 : 2)) * (cplx ? 16 : 8);
     {
         ProfScope ps(st, PH_SLICE);
 #define OZK_SPLIT(SM, RC, CX)                                                                       \
         {                                                                                           \
-            static bool attr = false;                                                               \
-            if (!attr) {                                                                            \
+            static size_t attr = 0;                                                                 \
+            if (attr < smem) {                                                                      \
                 cudaFuncSetAttribute(k_split_sm<SM, RC, CX>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                      (int)smem);                                                    \
-                attr = true;                                                                        \
+                attr = smem;                                                                        \
             }                                                                                       \
             k_split_sm<SM, RC, CX><<<grid, 256, smem, st>>>(sp, KW);                                \
         }

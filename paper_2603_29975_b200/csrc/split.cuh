@@ -135,9 +135,9 @@ __device__ __forceinline__ void store_planes(const uint32_t (&w)[NW][8], int s, 
 // an 8x8 byte transpose (PRMT) gives one 8-byte word per slice.  dst0 / dst1
 // receive the digits of X, dstn (optional) the digits of -X (RNE is sign-
 // symmetric, so -X is exactly the integer of the negated values).
-template <int SMAX>
-__device__ __forceinline__ void digits_store8(const double (&v)[8], double scale, int32_t e, int s,
-                                              int8_t *dst0, int8_t *dst1, int8_t *dstn, int64_t blk) {
+template <int SMAX, bool NEG>
+__device__ __forceinline__ void digits_store8_impl(const double (&v)[8], double scale, int32_t e, int s,
+                                                   int8_t *dst0, int8_t *dst1, int8_t *dstn, int64_t blk) {
     const int P = 8 * s - 1;
     constexpr int NW = SMAX / 4;   // 32-bit words of Y per value
     uint32_t w[NW][8], wn[NW][8];
@@ -148,11 +148,13 @@ __device__ __forceinline__ void digits_store8(const double (&v)[8], double scale
             const double xs = (scale != 0.0) ? __dmul_rn(v[i], scale) : ldexp_rn(v[i], P - e);
             const long long X = __double2ll_rn(xs);                     // |X| <= 127*2^(8s-8)
             const unsigned long long Y = ((unsigned long long)X + B) ^ B;
-            const unsigned long long Yn = ((unsigned long long)(-X) + B) ^ B;
             w[0][i] = (uint32_t)Y;
             w[1][i] = (uint32_t)(Y >> 32);
-            wn[0][i] = (uint32_t)Yn;
-            wn[1][i] = (uint32_t)(Yn >> 32);
+            if constexpr (NEG) {
+                const unsigned long long Yn = ((unsigned long long)(-X) + B) ^ B;
+                wn[0][i] = (uint32_t)Yn;
+                wn[1][i] = (uint32_t)(Yn >> 32);
+            }
         }
     } else {
         unsigned __int128 B = 0;
@@ -170,16 +172,25 @@ __device__ __forceinline__ void digits_store8(const double (&v)[8], double scale
                 if (bits >> 63) X = -X;
             }
             const unsigned __int128 Y = ((unsigned __int128)X + B) ^ B;
-            const unsigned __int128 Yn = ((unsigned __int128)(-X) + B) ^ B;
 #pragma unroll
-            for (int j = 0; j < NW; ++j) {
-                w[j][i] = (uint32_t)(Y >> (32 * j));
-                wn[j][i] = (uint32_t)(Yn >> (32 * j));
+            for (int j = 0; j < NW; ++j) w[j][i] = (uint32_t)(Y >> (32 * j));
+            if constexpr (NEG) {
+                const unsigned __int128 Yn = ((unsigned __int128)(-X) + B) ^ B;
+#pragma unroll
+                for (int j = 0; j < NW; ++j) wn[j][i] = (uint32_t)(Yn >> (32 * j));
             }
         }
     }
     store_planes<NW>(w, s, dst0, dst1, blk);
-    if (dstn) store_planes<NW>(wn, s, dstn, nullptr, blk);
+    if constexpr (NEG) store_planes<NW>(wn, s, dstn, nullptr, blk);
+}
+
+// dstn == nullptr (every target but 4M's -Im block): no negated digits at all
+template <int SMAX>
+__device__ __forceinline__ void digits_store8(const double (&v)[8], double scale, int32_t e, int s,
+                                              int8_t *dst0, int8_t *dst1, int8_t *dstn, int64_t blk) {
+    if (dstn) digits_store8_impl<SMAX, true>(v, scale, e, s, dst0, dst1, dstn, blk);
+    else digits_store8_impl<SMAX, false>(v, scale, e, s, dst0, dst1, nullptr, blk);
 }
 
 // address of the 8-byte half hh of 16-byte chunk C of output row R, slice 1
