@@ -681,6 +681,28 @@ bool overlaps(const void *a, size_t abytes, const void *b, size_t bbytes) {
     return abytes && bbytes && x < y + bbytes && y < x + abytes;
 }
 
+// Exact element overlap of two column-major views X (xr x xc, ld) and C (cr x cc, ld)
+// of the SAME leading dimension (e.g. sub-blocks of one LAPACK-style array, where the
+// byte spans interleave but the elements are disjoint).  Different leading dimensions
+// or misaligned bases: conservatively "overlap".
+bool elems_overlap(const void *x, int64_t xr, int64_t xc, int64_t ldx, const void *cp, int64_t cr, int64_t cc,
+                   int64_t ldc, size_t es) {
+    if (xr == 0 || xc == 0 || cr == 0 || cc == 0) return false;
+    if (ldx != ldc) return true;
+    const int64_t diff = (const char *)cp - (const char *)x;
+    if (diff % (int64_t)es) return true;
+    const int64_t ld = ldx, d = diff / (int64_t)es;
+    int64_t dc = d / ld, dr = d % ld;                   // C(0,0) sits at X(dr, dc) of the ld-grid
+    if (dr < 0) { dr += ld; dc -= 1; }
+    auto meet = [](int64_t a0, int64_t a1, int64_t b0, int64_t b1) { return a0 < b1 && b0 < a1; };
+    // C rows i' with dr + i' < ld land in grid rows dr + i' of columns dc + j'
+    const int64_t r1 = std::min(cr, ld - dr);
+    if (r1 > 0 && meet(dr, dr + r1, 0, xr) && meet(dc, dc + cc, 0, xc)) return true;
+    // C rows wrapping past ld land in rows dr + i' - ld of columns dc + j' + 1
+    if (cr > ld - dr && meet(0, dr + cr - ld, 0, xr) && meet(dc + 1, dc + cc + 1, 0, xc)) return true;
+    return false;
+}
+
 size_t span_bytes(int64_t rows, int64_t cols, int64_t ld, int64_t stride, int64_t batch, size_t es) {
     if (rows == 0 || cols == 0 || batch == 0) return 0;
     return es * (size_t)((batch - 1) * stride + (cols - 1) * ld + rows);
@@ -1176,9 +1198,11 @@ int run(const Call &c0) {
         const size_t cb = span_bytes(c.m, c.n, c.ldc, c.sC, c.batch, es);
         const int64_t ar = c.ta == 'N' ? c.m : c.k, ac = c.ta == 'N' ? c.k : c.m;
         const int64_t br = c.tb == 'N' ? c.k : c.n, bc = c.tb == 'N' ? c.n : c.k;
-        if (overlaps(c.C, cb, c.A, span_bytes(ar, ac, c.lda, c.sA, c.batch, es)) ||
-            overlaps(c.C, cb, c.B, span_bytes(br, bc, c.ldb, c.sB, c.batch, es)))
-            return fail(OZAKI_ERR_ALIAS, "C overlaps A or B");
+        const bool oa = overlaps(c.C, cb, c.A, span_bytes(ar, ac, c.lda, c.sA, c.batch, es)) &&
+                        (c.batch > 1 || elems_overlap(c.A, ar, ac, c.lda, c.C, c.m, c.n, c.ldc, es));
+        const bool ob = overlaps(c.C, cb, c.B, span_bytes(br, bc, c.ldb, c.sB, c.batch, es)) &&
+                        (c.batch > 1 || elems_overlap(c.B, br, bc, c.ldb, c.C, c.m, c.n, c.ldc, es));
+        if (oa || ob) return fail(OZAKI_ERR_ALIAS, "C overlaps A or B");
     }
     // quick return (R7): alpha == 0 or k == 0 -> C = beta C
     if (alpha0 || c.k == 0) {

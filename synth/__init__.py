@@ -15,6 +15,9 @@ distribution mimics the workloads the paper talks about:
   angular-momentum scaling of the multiple-scattering matrices that LSMS
   inverts (§3.2, 33,750^2 double-complex at PAPER.md:151).
 * ``integer``  -- integer-valued entries |x| < 2^bits (exactness pins).
+* ``hamiltonian`` -- Hermitian test operator H = Q diag(lambda) Q^H with a seeded
+  random unitary Q (SPEC.md [MODULE] workload build_test_hamiltonian: the
+  synthetic stand-in for the Kohn-Sham operator of PAPER.md:113-117).
 
 All matrices are returned in Fortran (column-major) order, the BLAS layout the
 C ABI consumes; complex matrices are ``complex128`` (interleaved re, im).
@@ -23,7 +26,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["rng", "uniform", "spread", "kkr", "integer", "make", "FAMILIES"]
+__all__ = ["rng", "uniform", "spread", "kkr", "integer", "hamiltonian", "make", "FAMILIES"]
 
 
 def rng(seed: int) -> np.random.Generator:
@@ -100,3 +103,19 @@ FAMILIES = {
 def make(family, rows, cols, seed, complex_=False, **kw):
     """Dispatch by family name; ``kw`` carries phi / gamma / bits."""
     return FAMILIES[family](rows, cols, seed, complex_=complex_, **kw)
+
+
+def hamiltonian(n, seed, eigs=None):
+    """Hermitian n x n complex128 H = Q diag(eigs) Q^H (Fortran order) and its sorted
+    eigenvalues.  Q: QR of a seeded complex Gaussian matrix (phase-fixed), eigs default
+    U[-1, 1).  H is symmetrised exactly: H = (H + H^H) / 2 computed entrywise."""
+    g = rng(seed)
+    if eigs is None:
+        eigs = np.sort(g.uniform(-1.0, 1.0, size=n))
+    eigs = np.asarray(eigs, dtype=np.float64)
+    Z = g.standard_normal((n, n)) + 1j * g.standard_normal((n, n))
+    Q, R = np.linalg.qr(Z)
+    Q = Q * (np.diag(R) / np.abs(np.diag(R)))          # unique unitary factor
+    H = (Q * eigs) @ Q.conj().T
+    H = 0.5 * (H + H.conj().T)
+    return np.asfortranarray(H), np.sort(eigs)

@@ -390,3 +390,20 @@ def test_host_offload_bitexact(orc, pinned):
     # mixed host/device operands are refused
     with pytest.raises(oz.OzakiError):
         oz.dgemm("N", "N", 1.0, dev(A), torch.from_numpy(np.asfortranarray(B)), 0.0, C, s)
+
+
+def test_disjoint_views_of_one_matrix(orc):
+    """LAPACK-style Schur update C = A22 - L21 U12 on sub-blocks of ONE column-major array:
+    the byte spans interleave but the elements are disjoint, so it must run (and match the
+    oracle); truly overlapping views are still rejected (OZAKI_ERR_ALIAS)."""
+    n, nb = 200, 48
+    X = synth.make("uniform", n, n, seed=77, complex_=True)
+    Xd = dev(X)
+    L21, U12, A22 = Xd[nb:, :nb], Xd[:nb, nb:], Xd[nb:, nb:]
+    want = orc.zgemm("N", "N", -1.0, X[nb:, :nb], X[:nb, nb:], 1.0, X[nb:, nb:], 7)
+    oz.zgemm("N", "N", -1.0, L21, U12, 1.0, A22, 7)
+    assert same(A22.cpu().numpy(), want)
+    assert same(Xd[:nb].cpu().numpy(), X[:nb]) and same(Xd[:, :nb].cpu().numpy(), X[:, :nb])
+    with pytest.raises(oz.OzakiError) as ei:
+        oz.zgemm("N", "N", 1.0, Xd[10:60, 10:60], Xd[10:60, 10:60], 0.0, Xd[40:90, 40:90], 7)
+    assert ei.value.code == 5
