@@ -24,8 +24,12 @@
  *   - Matrices are column-major with leading dimensions, exactly as BLAS
  *     dgemm/zgemm.  Complex matrices are interleaved (re, im) doubles.
  *   - A, B, C (and strided-batched bases) are DEVICE pointers owned by the
- *     caller (e.g. torch tensors).  A and B are read-only; C must not alias A
- *     or B.  When beta == 0, C is never read (NaN-safe).
+ *     caller (e.g. torch tensors).  A and B are read-only; C must not share an
+ *     element with A or B (OZAKI_ERR_ALIAS).  Views with the same leading
+ *     dimension are compared element-exactly, so LAPACK-style updates of
+ *     disjoint sub-blocks of one array (A22 -= L21 U12) are accepted; other
+ *     combinations (and batched calls) are compared by address span.  When
+ *     beta == 0, C is never read (NaN-safe).
  *   - Offload: if A, B and C are all HOST pointers (pinned or pageable), the
  *     call stages batch chunks through device memory on internal streams with
  *     H2D copy / GEMM / D2H copy overlapped, and returns once C is written
