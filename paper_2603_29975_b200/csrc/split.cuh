@@ -143,10 +143,16 @@ __device__ __forceinline__ void digits_store8_impl(const double (&v)[8], double 
     uint32_t w[NW][8], wn[NW][8];
     if constexpr (SMAX <= 8) {
         const unsigned long long B = 0x0080808080808080ull >> (8 * (8 - s));
+        long long Xs[8];
+        if (scale != 0.0) {          // the power 2^(P-e) is a normal double: one exact DMUL
+#pragma unroll
+            for (int i = 0; i < 8; ++i) Xs[i] = __double2ll_rn(__dmul_rn(v[i], scale));
+        } else {
+            for (int i = 0; i < 8; ++i) Xs[i] = __double2ll_rn(ldexp_rn(v[i], P - e));
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const double xs = (scale != 0.0) ? __dmul_rn(v[i], scale) : ldexp_rn(v[i], P - e);
-            const long long X = __double2ll_rn(xs);                     // |X| <= 127*2^(8s-8)
+            const long long X = Xs[i];                                  // |X| <= 127*2^(8s-8)
             const unsigned long long Y = ((unsigned long long)X + B) ^ B;
             w[0][i] = (uint32_t)Y;
             w[1][i] = (uint32_t)(Y >> 32);
@@ -253,13 +259,19 @@ __global__ void __launch_bounds__(256) k_split_sm(const __grid_constant__ SplitP
         const int wlen = (int)min((int64_t)KW, p.k - w0);   // valid elements in this window
         if (wlen <= 0) return;
         if (RCONTIG) {   // 8 rows adjacent in memory for each l
-            const Elem *g0 = X + r0 * p.rs + w0 * p.ls;
-            for (int idx = tid; idx < 8 * wlen; idx += blockDim.x) {
-                const int row = idx & 7, l = idx >> 3;
-                if (row < nrows) {
-                    const Elem *g = g0 + row + (int64_t)l * p.ls;
-                    if (CPLX) cp_async16(slab + row * ld + l, g);
-                    else cp_async8(slab + row * ld + l, g);
+            // blockDim = 256 is a multiple of 8: a thread keeps its row (tid & 7) and walks l
+            // in steps of 32 -- pointer increments only, no per-copy index math
+            const int row = tid & 7;
+            if (row < nrows) {
+                const int64_t gstep = 32 * p.ls;
+                const Elem *g = X + r0 * p.rs + w0 * p.ls + row + (int64_t)(tid >> 3) * p.ls;
+                Elem *d = slab + row * ld + (tid >> 3);
+#pragma unroll 4
+                for (int l = tid >> 3; l < wlen; l += 32) {
+                    if (CPLX) cp_async16(d, g);
+                    else cp_async8(d, g);
+                    g += gstep;
+                    d += 32;
                 }
             }
         } else {         // each row contiguous along l
@@ -300,8 +312,7 @@ __global__ void __launch_bounds__(256) k_split_sm(const __grid_constant__ SplitP
                             u = (uint64_t)__double_as_longlong(__dadd_rn(x.x, p.conj ? -x.y : x.y)) & kAbsMask;
                         else u = ur > ui ? ur : ui;
                     }
-                    nf |= (u >= kExpInf);
-                    m = (u < kExpInf && u > m) ? u : m;
+                    m = u > m ? u : m;   // Inf/NaN patterns exceed every finite |x|
                 }
             }
             __syncthreads();
@@ -310,8 +321,8 @@ __global__ void __launch_bounds__(256) k_split_sm(const __grid_constant__ SplitP
         for (int o = 16; o > 0; o >>= 1) {
             const uint64_t om = __shfl_xor_sync(0xffffffffu, m, o);
             m = om > m ? om : m;
-            nf |= __shfl_xor_sync(0xffffffffu, nf, o);
         }
+        nf = (m >= kExpInf);     // some entry of the row is Inf / NaN (R10)
         if (lane == 0) {
             int32_t e = 0;
             if (row < nrows) {
@@ -354,18 +365,29 @@ __global__ void __launch_bounds__(256) k_split_sm(const __grid_constant__ SplitP
             };
             if constexpr (!CPLX) {
                 double v[8];
+                if (nvalid == 8) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) v[i] = (i < nvalid) ? src[i] : 0.0;
+                    for (int i = 0; i < 8; ++i) v[i] = src[i];
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) v[i] = (i < nvalid) ? src[i] : 0.0;
+                }
                 emit(v, s_rowbase[row] + coff, nullptr, nullptr);
             } else {
                 // one component at a time (8 live values): 0 = Re, 1 = Im (conj applied), 2 = Re + Im
                 auto comp8 = [&](int comp, double (&v)[8]) {
+                    const double *xe = reinterpret_cast<const double *>(src);
+                    if (nvalid == 8 && comp < 2) {          // full item, plain component
+                        const double sg = (comp == 1 && p.conj) ? -1.0 : 1.0;
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) v[i] = (comp == 0) ? xe[2 * i] : sg * xe[2 * i + 1];
+                        return;
+                    }
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         double val = 0.0;
                         if (i < nvalid) {
-                            const double *xe = reinterpret_cast<const double *>(src + i);
-                            const double re = xe[0], im0 = xe[1];
+                            const double re = xe[2 * i], im0 = xe[2 * i + 1];
                             const double im = p.conj ? -im0 : im0;
                             val = comp == 0 ? re : (comp == 1 ? im : __dadd_rn(re, im));
                         }
