@@ -99,7 +99,32 @@ def timed_gemm(gemm):
     return f
 
 
-def blocked_lu_invert(M, nb: int, gemm, stats: dict | None = None):
+def blocked_trsm(T, B, nb: int, gemm, lower: bool, unit: bool, stats: dict | None = None):
+    """NEXT-4 emulated ZTRSM: solve T X = B in place of B (T triangular n x n, B n x r,
+    column-major CUDA/CPU tensors) by blocks of nb rows.  The nb x nb diagonal solves are
+    native FP64; every off-diagonal update B_rest -= T_rest,i X_i goes through ``gemm``
+    (SURVEY.md §8(f) NEXT-4 "emulated ZTRSM through blocked TRSM with GEMM updates";
+    PAPER.md:115 ZGEMM + ZTRSM dominate LSMS)."""
+    import torch
+    n = T.shape[0]
+    order = range(0, n, nb) if lower else reversed(range(0, n, nb))
+    updates = 0
+    for i0 in order:
+        i1 = min(n, i0 + nb)
+        B[i0:i1] = torch.linalg.solve_triangular(T[i0:i1, i0:i1], B[i0:i1], upper=not lower,
+                                                 unitriangular=unit)
+        if lower and i1 < n:
+            gemm(T[i1:, i0:i1], B[i0:i1], B[i1:], -1.0, 1.0)
+            updates += 1
+        if not lower and i0 > 0:
+            gemm(T[:i0, i0:i1], B[i0:i1], B[:i0], -1.0, 1.0)
+            updates += 1
+    if stats is not None:
+        stats["trsm_updates"] = stats.get("trsm_updates", 0) + updates
+    return B
+
+
+def blocked_lu_invert(M, nb: int, gemm, stats: dict | None = None, emulated_trsm: bool = False):
     """Inverse of a square complex128 CUDA tensor by right-looking blocked LU with partial
     pivoting; the trailing updates A22 -= L21 U12 go through ``gemm``.  Returns (Minv,
     residual max|M Minv - I|)."""
@@ -135,8 +160,13 @@ def blocked_lu_invert(M, nb: int, gemm, stats: dict | None = None):
     U = torch.triu(A)
     Pm = torch.zeros((n, n), dtype=A.dtype, device=A.device)
     Pm[torch.arange(n, device=M.device), perm] = 1.0                 # P M = L U
-    Y = torch.linalg.solve_triangular(L, Pm, upper=False, unitriangular=True)
-    Minv = torch.linalg.solve_triangular(U, Y, upper=True)
+    if emulated_trsm:      # M^-1 = U^-1 (L^-1 P) with blocked TRSMs whose updates use ``gemm``
+        L, U = colmajor(L), colmajor(U)
+        Y = blocked_trsm(L, colmajor(Pm), nb, gemm, lower=True, unit=True, stats=stats)
+        Minv = blocked_trsm(U, Y, nb, gemm, lower=False, unit=False, stats=stats)
+    else:
+        Y = torch.linalg.solve_triangular(L, Pm, upper=False, unitriangular=True)
+        Minv = torch.linalg.solve_triangular(U, Y, upper=True)
     I = torch.eye(n, dtype=A.dtype, device=A.device)
     resid = float((M @ Minv - I).abs().max())
     return Minv, resid

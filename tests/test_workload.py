@@ -59,6 +59,21 @@ def test_blocked_lu_cpu_native():
     assert W.trailing_updates(200, 64) == 3 and W.trailing_updates(64, 64) == 0
 
 
+def test_blocked_trsm_cpu_native():
+    n, r, nb = 70, 33, 16
+    g = np.random.default_rng(5)
+    Tl = np.tril(g.standard_normal((n, n)) + 1j * g.standard_normal((n, n))) + 8 * np.eye(n)
+    Tu = np.triu(g.standard_normal((n, n)) + 1j * g.standard_normal((n, n))) + 8 * np.eye(n)
+    B = g.standard_normal((n, r)) + 1j * g.standard_normal((n, r))
+    for T, lower, unit in ((Tl, True, False), (Tu, False, False), (0.05 * np.tril(Tl, -1) + np.eye(n), True, True)):
+        X = W.blocked_trsm(torch.from_numpy(T), torch.from_numpy(B.copy()), nb, _cpu_native(), lower, unit)
+        assert np.abs(T @ X.numpy() - B).max() < 1e-12
+    Mt = torch.from_numpy(Tl @ Tu)
+    st = {}
+    Minv, res = W.blocked_lu_invert(Mt, nb, _cpu_native(), st, emulated_trsm=True)
+    assert res < 1e-12 and st["trsm_updates"] == 2 * W.trailing_updates(n, nb)
+
+
 def test_integrated_density_cpu():
     H, ev = synth.hamiltonian(3, seed=1, eigs=[-0.5, 0.2, 0.9])
     rep = W.green_function_sweep(H, -1.0, 0.5, 30, [_cpu_native()], nb=2, device="cpu")
@@ -95,7 +110,25 @@ def test_green_function_sweep_gpu():
     assert all(b <= a * 1.5 + 1e-13 for a, b in zip(e2, e2[1:])) and e2[1] > e2[4]
     for lab, rec in R.items():
         assert rec["residual_max"] < 1e-4, lab            # 23-bit mode: ~5e-6
-    for lab in (W.gemm_ozaki1(7).label, W.gemm_ozaki2(16).label):
-        assert R[lab]["residual_max"] < 1e-12, lab         # FP64-level modes
         # the contour integral suppresses the per-node emulation error
         assert abs(rec["N_est"] - R["native"]["N_est"]) < 1e-5, lab
+    for lab in (W.gemm_ozaki1(7).label, W.gemm_ozaki2(16).label):
+        assert R[lab]["residual_max"] < 1e-12, lab         # FP64-level modes
+
+
+@pytest.mark.gpu
+def test_emulated_trsm_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    n, nb = 300, 64
+    H, _ = synth.hamiltonian(n, seed=9)
+    M = torch.from_numpy(np.ascontiguousarray(H)).cuda() - (0.1 + 0.2j) * torch.eye(n, dtype=torch.complex128,
+                                                                                       device="cuda")
+    ref, _ = W.blocked_lu_invert(M, nb, W.gemm_native())
+    errs = []
+    for s in (4, 6, 8):
+        st = {}
+        Minv, res = W.blocked_lu_invert(M, nb, W.gemm_ozaki1(s), st, emulated_trsm=True)
+        assert st["trsm_updates"] == 2 * W.trailing_updates(n, nb)
+        errs.append(float((Minv - ref).abs().max() / ref.abs().max()))
+    assert errs[0] > errs[1] > errs[2] and errs[2] < 1e-13, errs

@@ -43,31 +43,34 @@ def accuracy(n=512, nodes=30, nb=64):
     return out
 
 
-def timing(n=4096, nb=512, reps=2):
+def timing(n=4096, nb=512, reps=2, emulated_trsm=False):
     H, ev = synth.hamiltonian(n, seed=12)
     Hd = torch.from_numpy(np.ascontiguousarray(H)).cuda()
     I = torch.eye(n, dtype=torch.complex128, device="cuda")
     M = complex(-0.2 + 0.05j) * I - Hd
     res = {}
     for base in (W.gemm_native(), W.gemm_ozaki1(4), W.gemm_ozaki1(7), W.gemm_ozaki2(12), W.gemm_ozaki2(16)):
-        W.blocked_lu_invert(M, nb, base)          # warm-up
+        W.blocked_lu_invert(M, nb, base, emulated_trsm=emulated_trsm)          # warm-up
         gm = W.timed_gemm(base)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(reps):
-            Minv, r = W.blocked_lu_invert(M, nb, gm)
+            Minv, r = W.blocked_lu_invert(M, nb, gm, emulated_trsm=emulated_trsm)
         torch.cuda.synchronize()
         secs = (time.perf_counter() - t0) / reps
         gms = gm.total_ms() / reps
-        # trailing updates of one LU: sum over panels of 8 (n - j1)^2 nb real flops (complex MACs x 8)
+        # LU trailing updates: sum over panels of 8 (n - j1)^2 nb real flops (complex MACs x 8);
+        # emulated TRSM adds the two block sweeps' updates, each sum_i 8 (rows_left) nb n
         flops = sum(8.0 * (n - j1) ** 2 * nb for j1 in range(nb, n, nb))
+        if emulated_trsm:
+            flops += 2 * sum(8.0 * (n - j1) * nb * n for j1 in range(nb, n, nb))
         res[gm.label] = {"seconds_per_inversion": secs, "trailing_update_ms": gms,
                          "trailing_update_tflops": flops / (gms * 1e-3) / 1e12, "residual_max": r}
-    return {"n": n, "nb": nb, "modes": res}
+    return {"n": n, "nb": nb, "emulated_trsm": emulated_trsm, "modes": res}
 
 
 if __name__ == "__main__":
-    out = {"accuracy": accuracy(), "timing": timing()}
+    out = {"accuracy": accuracy(), "timing": timing(), "timing_emulated_trsm": timing(emulated_trsm=True)}
     os.makedirs("gpurun_out", exist_ok=True)
     with open("gpurun_out/gz_sweep.json", "w") as fh:
         json.dump(out, fh, indent=1)
@@ -76,9 +79,10 @@ if __name__ == "__main__":
     for lab, r in a["modes"].items():
         print(f"  {lab:28s} max % err {r['max_percent_error']:.3e} (node {r['argmax_node']:2d})  "
               f"N_est err {r['N_est_error']:.2e} (vs native {r['N_est_vs_native']:.1e})  resid {r['residual_max']:.1e}")
-    t = out["timing"]
-    print(f"inversion n={t['n']} nb={t['nb']}:")
-    for lab, r in t["modes"].items():
-        print(f"  {lab:28s} {r['seconds_per_inversion'] * 1e3:9.2f} ms total, trailing updates "
+    for key in ("timing", "timing_emulated_trsm"):
+      t = out[key]
+      print(f"inversion n={t['n']} nb={t['nb']} emulated_trsm={t['emulated_trsm']}:")
+      for lab, r in t["modes"].items():
+        print(f"  {lab:28s} {r['seconds_per_inversion'] * 1e3:9.2f} ms total, emulated-GEMM updates "
               f"{r['trailing_update_ms']:8.2f} ms ({r['trailing_update_tflops']:6.1f} TF/s FP64-eq)  "
               f"resid {r['residual_max']:.1e}")
