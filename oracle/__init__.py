@@ -75,6 +75,12 @@ def lib():
         L.orc_num_threads.restype = i32
         L.orc_quick_real.restype = None
         L.orc_quick_real.argtypes = [i64, dbl, p]
+        L.orc_level_sums_full.restype = None
+        L.orc_level_sums_full.argtypes = [i64, i64, i64, i32, p, p, p]
+        L.orc_combine_levels.restype = None
+        L.orc_combine_levels.argtypes = [i64, i64, i32, p, p, p, p, p, p]
+        L.orc_emulated_product_full.restype = i32
+        L.orc_emulated_product_full.argtypes = [i64, i64, i64, i32, p, p, p]
         L.orc_quick_complex.restype = None
         L.orc_quick_complex.argtypes = [i64, dbl, dbl, p, p]
         _lib = L
@@ -172,14 +178,27 @@ def combine(S, e, nfa, f, nfb, s: int) -> np.ndarray:
     return P
 
 
-def emulated_product(A_op, B_op, s: int) -> np.ndarray:
-    """O2..O6: P = emulated A_op @ B_op for real matrices (returns m x n)."""
+def level_sums_full(DA, DB, s: int) -> np.ndarray:
+    """R21 (NEXT-4): all s^2 pairs, S[L-2] for L = 2..2s (int64, exact)."""
+    DA = _c(DA, np.int8)
+    DB = _c(DB, np.int8)
+    _, m, k = DA.shape
+    _, n, _ = DB.shape
+    S = np.zeros((2 * s - 1, m, n), dtype=np.int64)
+    lib().orc_level_sums_full(m, n, k, s, _ptr(DA), _ptr(DB), _ptr(S))
+    return S
+
+
+def emulated_product(A_op, B_op, s: int, pairs: str = "triangular") -> np.ndarray:
+    """O2..O6: P = emulated A_op @ B_op for real matrices (returns m x n).
+    pairs = 'triangular' (R1, t + u <= s + 1) or 'full' (R21, all s^2 products)."""
     A = _c(A_op, np.float64)
     Bt = _c(np.asarray(B_op).T, np.float64)
     m, k = A.shape
     n = Bt.shape[0]
     P = np.zeros((m, n), dtype=np.float64)
-    rc = lib().orc_emulated_product(m, n, k, s, _ptr(A), _ptr(Bt), _ptr(P))
+    fn = lib().orc_emulated_product_full if pairs == "full" else lib().orc_emulated_product
+    rc = fn(m, n, k, s, _ptr(A), _ptr(Bt), _ptr(P))
     if rc != 0:
         raise ArithmeticError("oracle split failed")
     return P
@@ -200,7 +219,7 @@ def _quick(beta, C):
     return out
 
 
-def dgemm(transa, transb, alpha, A, B, beta, C, s: int) -> np.ndarray:
+def dgemm(transa, transb, alpha, A, B, beta, C, s: int, pairs: str = "triangular") -> np.ndarray:
     """Full emulated DGEMM: returns alpha*emul(op(A)op(B)) + beta*C (new array)."""
     Aop = op(np.asarray(A, dtype=np.float64), transa)
     Bop = op(np.asarray(B, dtype=np.float64), transb)
@@ -211,7 +230,7 @@ def dgemm(transa, transb, alpha, A, B, beta, C, s: int) -> np.ndarray:
         return C.copy()
     if alpha == 0 or k == 0:
         return _quick(beta, C)
-    P = emulated_product(Aop, Bop, s)
+    P = emulated_product(Aop, Bop, s, pairs)
     out = _c(C, np.float64).copy()
     lib().orc_apply_real(m * n, float(alpha), _ptr(P), float(beta), _ptr(out))
     return out
@@ -230,19 +249,19 @@ def emb_4m(Aop, Bop):
     return A2, B2
 
 
-def zproduct(Aop, Bop, s: int, method: str = "4m"):
+def zproduct(Aop, Bop, s: int, method: str = "4m", pairs: str = "triangular"):
     """Emulated complex product P = Pr + i Pi (O2..O6, 4M or 3M)."""
     n = Bop.shape[1]
     if method == "4m":
         A2, B2 = emb_4m(Aop, Bop)
-        P2 = emulated_product(A2, B2, s)
+        P2 = emulated_product(A2, B2, s, pairs)
         return P2[:, :n].copy(), P2[:, n:].copy()
     if method == "3m":
         Ar, Ai = np.ascontiguousarray(Aop.real), np.ascontiguousarray(Aop.imag)
         Br, Bi = np.ascontiguousarray(Bop.real), np.ascontiguousarray(Bop.imag)
-        T1 = emulated_product(Ar, Br, s)
-        T2 = emulated_product(Ai, Bi, s)
-        T3 = emulated_product(Ar + Ai, Br + Bi, s)  # fl(Ar+Ai), fl(Br+Bi) in FP64
+        T1 = emulated_product(Ar, Br, s, pairs)
+        T2 = emulated_product(Ai, Bi, s, pairs)
+        T3 = emulated_product(Ar + Ai, Br + Bi, s, pairs)  # fl(Ar+Ai), fl(Br+Bi) in FP64
         Pr = np.zeros_like(T1)
         Pi = np.zeros_like(T1)
         lib().orc_combine_3m(T1.size, _ptr(_c(T1, np.float64)), _ptr(_c(T2, np.float64)),
@@ -251,7 +270,8 @@ def zproduct(Aop, Bop, s: int, method: str = "4m"):
     raise ValueError(method)
 
 
-def zgemm(transa, transb, alpha, A, B, beta, C, s: int, method: str = "4m") -> np.ndarray:
+def zgemm(transa, transb, alpha, A, B, beta, C, s: int, method: str = "4m",
+          pairs: str = "triangular") -> np.ndarray:
     Aop = op(np.asarray(A, dtype=np.complex128), transa)
     Bop = op(np.asarray(B, dtype=np.complex128), transb)
     m, k = Aop.shape
@@ -263,7 +283,7 @@ def zgemm(transa, transb, alpha, A, B, beta, C, s: int, method: str = "4m") -> n
         return C.copy()
     if alpha == 0 or k == 0:
         return _quick(beta, C)
-    Pr, Pi = zproduct(Aop, Bop, s, method)
+    Pr, Pi = zproduct(Aop, Bop, s, method, pairs)
     Cr = _c(C.real, np.float64).copy()
     Ci = _c(C.imag, np.float64).copy()
     lib().orc_apply_complex(m * n, alpha.real, alpha.imag, _ptr(_c(Pr, np.float64)),

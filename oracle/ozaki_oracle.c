@@ -142,6 +142,77 @@ void orc_level_sums(int64_t m, int64_t n, int64_t k, int s,
     }
 }
 
+/* NEXT-4 variant, reading R21: the FULL pair set, all s^2 slice products.    */
+/* Levels L = 2..2s, S_L = sum over 1 <= t, u <= s with t + u = L (the same    */
+/* per-level pair formula, no truncation at s + 1).  Output S[(L-2)*m*n+...]   */
+/* for L = 2..2s (2s - 1 levels).                                             */
+void orc_level_sums_full(int64_t m, int64_t n, int64_t k, int s,
+                         const int8_t *DA, const int8_t *DB, int64_t *S)
+{
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t i = 0; i < m; ++i) {
+        for (int64_t j = 0; j < n; ++j) {
+            for (int L = 2; L <= 2 * s; ++L) {
+                int64_t acc = 0;
+                int tlo = L - s > 1 ? L - s : 1;
+                int thi = L - 1 < s ? L - 1 : s;
+                for (int t = tlo; t <= thi; ++t) {
+                    int u = L - t;
+                    const int8_t *a = DA + (int64_t)(t - 1) * m * k + i * k;
+                    const int8_t *b = DB + (int64_t)(u - 1) * n * k + j * k;
+                    for (int64_t l = 0; l < k; ++l)
+                        acc += (int64_t)a[l] * (int64_t)b[l];
+                }
+                S[(int64_t)(L - 2) * m * n + i * n + j] = acc;
+            }
+        }
+    }
+}
+
+/* R21 combine: as O6 (ascending significance, one RNE per step) over the     */
+/* levels L = Lmax .. 2, Lmax = s + 1 (triangular) or 2s (full).              */
+void orc_combine_levels(int64_t m, int64_t n, int Lmax, const int64_t *S,
+                        const int32_t *e, const int32_t *nfa,
+                        const int32_t *f, const int32_t *nfb, double *P)
+{
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t i = 0; i < m; ++i) {
+        for (int64_t j = 0; j < n; ++j) {
+            if (nfa[i] || nfb[j]) {
+                P[i * n + j] = NAN;
+                continue;
+            }
+            double acc = 0.0;
+            for (int L = Lmax; L >= 2; --L) {
+                double term = (double)S[(int64_t)(L - 2) * m * n + i * n + j] *
+                              ldexp(1.0, -8 * (L - 2)); /* exact */
+                acc = acc + term;
+            }
+            P[i * n + j] = ldexp(acc, e[i] + f[j] - 14);
+        }
+    }
+}
+
+/* O2..O6 with the full pair set (R21). */
+int orc_emulated_product_full(int64_t m, int64_t n, int64_t k, int s,
+                              const double *A, const double *Bt, double *P)
+{
+    int8_t *DA = malloc((size_t)s * m * k + 1);
+    int8_t *DB = malloc((size_t)s * n * k + 1);
+    int64_t *S = malloc(sizeof(int64_t) * ((size_t)(2 * s - 1) * m * n + 1));
+    int32_t *e = malloc(sizeof(int32_t) * (m + 1)), *nfa = malloc(sizeof(int32_t) * (m + 1));
+    int32_t *f = malloc(sizeof(int32_t) * (n + 1)), *nfb = malloc(sizeof(int32_t) * (n + 1));
+    int rc = -2;
+    if (DA && DB && S && e && nfa && f && nfb) {
+        rc = orc_split_rows(m, k, A, s, DA, e, nfa);
+        rc |= orc_split_rows(n, k, Bt, s, DB, f, nfb);
+        orc_level_sums_full(m, n, k, s, DA, DB, S);
+        orc_combine_levels(m, n, 2 * s, S, e, nfa, f, nfb, P);
+    }
+    free(DA); free(DB); free(S); free(e); free(nfa); free(f); free(nfb);
+    return rc;
+}
+
 /* ------------------------------------------------------------------------- */
 /* O6: combine in FP64, ascending significance (reading R6):                  */
 /*   acc = 0; for L = s+1 down to 2: acc = acc + (double)S_L * 2^(-8(L-2))    */
