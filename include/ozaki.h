@@ -165,6 +165,18 @@ int ozaki2_zgemm_strided_batched(char transa, char transb, int64_t m, int64_t n,
                                  const double *beta, double *C, int64_t ldc, int64_t strideC,
                                  int64_t batch, int num_moduli);
 
+/* --- NEXT-4 variant: the Ozaki-I pair set (reading R21) ----------------------
+ * full = 0 (default): the triangular set t + u <= s + 1 of R1, s(s+1)/2 INT8
+ * products.  full = 1: all s^2 slice products (levels L = 2..2s, same
+ * ascending FP64 combine), i.e. the exact integer product of the integerised
+ * operands before one rounding per level step -- more accurate, ~2x the INT8
+ * work.  Thread-local, read at each ozaki_*gemm* call (Ozaki-I routines only).
+ * The full set needs s <= 8 and s * k_eff <= 131071 (no K-chunking) and the
+ * CTA-pair kernel; otherwise the call returns OZAKI_ERR_UNSUPPORTED.
+ * ozaki_debug_level_sums then writes 2s - 1 levels.                          */
+int ozaki_set_pair_set(int full);
+int ozaki_get_pair_set(void);
+
 /* --- streams, stats, errors --------------------------------------------- */
 /* stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
  * thread-local; returns 0.                                                 */

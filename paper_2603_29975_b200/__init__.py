@@ -72,6 +72,10 @@ def lib():
     L.ozaki_zgemm_strided_batched.argtypes = [c, c, i64, i64, i64, dP, p, i64, i64, p, i64, i64,
                                               dP, p, i64, i64, i64, i32]
     L.ozaki_zgemm3m_strided_batched.argtypes = L.ozaki_zgemm_strided_batched.argtypes
+    L.ozaki_set_pair_set.argtypes = [i32]
+    L.ozaki_set_pair_set.restype = i32
+    L.ozaki_get_pair_set.argtypes = []
+    L.ozaki_get_pair_set.restype = i32
     L.ozaki2_dgemm.argtypes = L.ozaki_dgemm.argtypes
     L.ozaki2_zgemm.argtypes = L.ozaki_zgemm.argtypes
     L.ozaki2_dgemm_strided_batched.argtypes = L.ozaki_dgemm_strided_batched.argtypes
@@ -290,6 +294,17 @@ def ozaki2_zgemm_strided_batched(transa, transb, alpha, A, B, beta, C, num_modul
 
 
 # ------------------------------------------------------------- utilities
+def set_pair_set(kind: str) -> None:
+    """Ozaki-I pair set for this thread: 'triangular' (R1, default) or 'full' (R21, NEXT-4)."""
+    if kind not in ("triangular", "full"):
+        raise ValueError(kind)
+    lib().ozaki_set_pair_set(1 if kind == "full" else 0)
+
+
+def get_pair_set() -> str:
+    return "full" if lib().ozaki_get_pair_set() else "triangular"
+
+
 def set_stream(stream) -> None:
     lib().ozaki_set_stream(ctypes.c_void_p(getattr(stream, "cuda_stream", stream) or 0))
 
@@ -366,7 +381,8 @@ def debug_level_sums(transa, transb, A, B, num_slices, stream=None):
     _cuda(B, torch.float64, "B")
     m, n, k = _dims(transa, transb, A, B)
     s = int(num_slices)
-    S = torch.zeros((s, n, m), dtype=torch.int32, device=A.device)   # column-major per level
+    nlev = 2 * s - 1 if get_pair_set() == "full" else s
+    S = torch.zeros((nlev, n, m), dtype=torch.int32, device=A.device)   # column-major per level
     _bind_stream(stream)
     rc = lib().ozaki_debug_level_sums(_ch(transa), _ch(transb), m, n, k, A.data_ptr(), _ld(A),
                                       B.data_ptr(), _ld(B), s, S.data_ptr())

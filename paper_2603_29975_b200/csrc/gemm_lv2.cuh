@@ -32,11 +32,11 @@ struct Lv2Params {
     CUtensorMap tmB[kMaxPassMaps];        // B slices (64-row tiles), box = 8 n rows
 };
 
-template <int S>
+template <int S, bool FULL = false>
 __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem, uint64_t *full,
                                              uint64_t *empty, uint64_t *pass_full,
                                              uint64_t *slot_empty, uint32_t tbase) {
-    constexpr PassPlan PP = make_pass_plan(S);
+    constexpr PassPlan PP = FULL ? make_pass_plan_full(S) : make_pass_plan(S);
     constexpr uint32_t idesc = idesc_i8(256, kLvBN);
     const LvParams &lp = P2.lv;
     const GemmParams &p = lp.g;
@@ -108,7 +108,8 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
 // CHUNK (compile time, reading R8): 0 = whole K in one INT32 accumulation;
 // 1 = first/middle K chunk (W = S or W += S, nothing stored to C);
 // 2 = last K chunk (level sum = W + S, then the FP64 combine and store).
-template <int EPI, int CHUNK>
+// FULL (reading R21, NEXT-4): all s^2 pairs, levels 2s .. 2 (s <= 8, CHUNK 0 only).
+template <int EPI, int CHUNK, bool FULL = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     k_gemm_lv2(const __grid_constant__ Lv2Params P2) {
     const LvParams &lp = P2.lv;
@@ -126,6 +127,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     const int lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
     const int s = p.s;
+    const int Lmax = FULL ? 2 * s : s + 1;   // levels Lmax (least significant) .. 2 (R1 / R21)
     const int64_t total = p.batch * p.tiles_m * p.tiles_n;
 
     if (warp == 0 && lane == 0) {
@@ -184,13 +186,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     } else if (warp == 1) {
         // ========================= MMA issuer: leader CTA only
         if (rank == 0) {
-            switch (s) {
-#define OZK_MMA2_CASE(SS) case SS: lv2_mma_role<SS>(P2, smem, full, empty, pass_full, slot_empty, tbase); break;
-                OZK_MMA2_CASE(1) OZK_MMA2_CASE(2) OZK_MMA2_CASE(3) OZK_MMA2_CASE(4)
-                OZK_MMA2_CASE(5) OZK_MMA2_CASE(6) OZK_MMA2_CASE(7) OZK_MMA2_CASE(8)
-                OZK_MMA2_CASE(9) OZK_MMA2_CASE(10) OZK_MMA2_CASE(11) OZK_MMA2_CASE(12)
+            if constexpr (FULL) {
+                switch (s) {
+#define OZK_MMA2_CASE(SS) case SS: lv2_mma_role<SS, true>(P2, smem, full, empty, pass_full, slot_empty, tbase); break;
+                    OZK_MMA2_CASE(1) OZK_MMA2_CASE(2) OZK_MMA2_CASE(3) OZK_MMA2_CASE(4)
+                    OZK_MMA2_CASE(5) OZK_MMA2_CASE(6) OZK_MMA2_CASE(7) OZK_MMA2_CASE(8)
 #undef OZK_MMA2_CASE
-                default: break;
+                    default: break;
+                }
+            } else {
+                switch (s) {
+#define OZK_MMA2_CASE(SS) case SS: lv2_mma_role<SS>(P2, smem, full, empty, pass_full, slot_empty, tbase); break;
+                    OZK_MMA2_CASE(1) OZK_MMA2_CASE(2) OZK_MMA2_CASE(3) OZK_MMA2_CASE(4)
+                    OZK_MMA2_CASE(5) OZK_MMA2_CASE(6) OZK_MMA2_CASE(7) OZK_MMA2_CASE(8)
+                    OZK_MMA2_CASE(9) OZK_MMA2_CASE(10) OZK_MMA2_CASE(11) OZK_MMA2_CASE(12)
+#undef OZK_MMA2_CASE
+                    default: break;
+                }
             }
         }
     } else {
@@ -282,7 +294,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     }
 #pragma unroll 1
                     for (int j = j0; j < nlev; ++j) {
-                        const double sc = pow2(8 * (s + 1 - (pa.hi - j)));
+                        const double sc = pow2(8 * (Lmax - (pa.hi - j)));
                         tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN), v);
                         tmem_wait_ld();
 #pragma unroll
@@ -352,7 +364,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             }
             const long long s0 = p.dbg ? clock64() : 0;
             if constexpr (EPI != EPI_LEVELS && CHUNK != 1)
-                lv_store<EPI, kNC2>(p, b, grow, e, tn * kLvBN + half * kNC2, acc, CHUNK == 0 ? -8 * (s - 1) : 0);
+                lv_store<EPI, kNC2>(p, b, grow, e, tn * kLvBN + half * kNC2, acc, CHUNK == 0 ? -8 * (Lmax - 2) : 0);
             if (dbgw) dbg_add(p, DBG_EPI_STORE, clock64() - s0);
         }
     }

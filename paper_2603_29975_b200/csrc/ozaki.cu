@@ -34,6 +34,7 @@ namespace {
 
 thread_local cudaStream_t t_stream = nullptr;
 thread_local std::string t_err;
+thread_local int t_full_pairs = 0;   // R21 pair set for Ozaki-I calls (ozaki_set_pair_set)
 
 struct Stats {
     std::atomic<uint64_t> dgemm{0}, zgemm{0}, zgemm3m{0}, entries{0}, equiv{0}, macs{0},
@@ -162,6 +163,7 @@ enum Kind { KIND_REAL = 0, KIND_4M = 1, KIND_3M = 2 };
 // ------------------------------------------------------------------- plan
 struct Plan {
     int s, BN;
+    bool full = false;   // R21 full pair set (levels 2s .. 2)
     int64_t m, n, k, batch;
     int64_t Mp;          // output rows of the real product
     int64_t Np;          // output columns of the real product (2n for 4M: Re/Im interleaved)
@@ -183,7 +185,7 @@ struct Plan {
 // Pass plan of the level-pass kernel: make_pass_plan (passplan.cuh, shared
 // with the device code) plus the per-pass k-blocks per stage.
 void plan_passes(int s, Plan &P) {
-    const PassPlan pp = make_pass_plan(s);
+    const PassPlan pp = P.full ? make_pass_plan_full(s) : make_pass_plan(s);
     P.npass = pp.npass;
     const uint32_t kb_bytes_per_slice = (uint32_t)(P.a_tile_h + P.b_tile_h) * kKB;   // A + B rows
     uint32_t maxb = 0;
@@ -216,8 +218,9 @@ int kernel_choice() {
 
 size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
-int make_plan(Kind kind, int64_t m, int64_t n, int64_t k, int64_t batch, int s, Plan &P) {
+int make_plan(Kind kind, int64_t m, int64_t n, int64_t k, int64_t batch, int s, Plan &P, bool full = false) {
     P.s = s;
+    P.full = full;
     P.BN = (s <= 8) ? 64 : 32;
     P.m = m;
     P.n = n;
@@ -247,6 +250,9 @@ int make_plan(Kind kind, int64_t m, int64_t n, int64_t k, int64_t batch, int s, 
                     "s*k_eff = %lld exceeds the INT32 level-sum bound 131071 and K-chunking needs the "
                     "CTA-pair kernel (s <= 12)",
                     (long long)((int64_t)s * keff));
+    if (full && (!P.pair || s > 8 || P.kchunk_needed))
+        return fail(OZAKI_ERR_UNSUPPORTED,
+                    "the full pair set (R21) needs the CTA-pair kernel, s <= 8 and s*k_eff <= 131071");
     if (P.lv) P.BN = kLvBN;
     P.a_tile_h = kBM;
     P.b_tile_h = P.pair ? kLvBN / 2 : P.BN;
@@ -468,12 +474,12 @@ int rows_map(CUtensorMap *m, const void *base, size_t bytes, uint32_t box_rows) 
     return 0;
 }
 
-template <int EPI, int CHUNK = 0>
+template <int EPI, int CHUNK = 0, bool FULL = false>
 int launch_gemm_lv2(const Plan &P, const GemmParams &gp, size_t a_avail, size_t b_avail, DevState *dev,
                     cudaStream_t st) {
     static std::atomic<size_t> done{0};
     if (done.load() < P.smem) {
-        CUDA_TRY(cudaFuncSetAttribute(k_gemm_lv2<EPI, CHUNK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CUDA_TRY(cudaFuncSetAttribute(k_gemm_lv2<EPI, CHUNK, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)P.smem));
         done.store(P.smem);
     }
@@ -491,7 +497,7 @@ int launch_gemm_lv2(const Plan &P, const GemmParams &gp, size_t a_avail, size_t 
     const unsigned pairs = (unsigned)std::min<int64_t>(tiles, dev->sms / 2);
     {
         ProfScope ps(st, PH_GEMM);
-        k_gemm_lv2<EPI, CHUNK><<<2 * pairs, kThreads2, P.smem, st>>>(P2);
+        k_gemm_lv2<EPI, CHUNK, FULL><<<2 * pairs, kThreads2, P.smem, st>>>(P2);
     }
     CUDA_TRY(cudaGetLastError());
     g_stats.launches += 1;
@@ -618,6 +624,11 @@ int launch_gemm(const Plan &P, int epi, const int8_t *sa, const int8_t *sb, cons
         const int64_t kc_env = ev ? atoll(ev) : 0;
         if ((P.kchunk_needed || kc_env > 0) && epi != EPI_LEVELS)
             return launch_gemm_chunked(P, gp, epi, kc_env, dev, st);
+        if (P.full) {   // R21: all s^2 pairs (planned only without K-chunking)
+            if (epi == EPI_REAL) return launch_gemm_lv2<EPI_REAL, 0, true>(P, gp, P.a_bytes, P.b_bytes, dev, st);
+            if (epi == EPI_CPLX4M) return launch_gemm_lv2<EPI_CPLX4M, 0, true>(P, gp, P.a_bytes, P.b_bytes, dev, st);
+            return launch_gemm_lv2<EPI_LEVELS, 0, true>(P, gp, P.a_bytes, P.b_bytes, dev, st);
+        }
         if (epi == EPI_REAL) return launch_gemm_lv2<EPI_REAL>(P, gp, P.a_bytes, P.b_bytes, dev, st);
         if (epi == EPI_CPLX4M) return launch_gemm_lv2<EPI_CPLX4M>(P, gp, P.a_bytes, P.b_bytes, dev, st);
         return launch_gemm_lv2<EPI_LEVELS>(P, gp, P.a_bytes, P.b_bytes, dev, st);
@@ -723,6 +734,7 @@ struct Call {
     bool batched;
     int32_t *S_out;   // debug level dump (real only)
     bool crt;         // Ozaki-II (NEXT-1)
+    bool full;        // Ozaki-I full pair set (R21, NEXT-4)
 };
 
 int validate(const Call &c) {
@@ -1222,7 +1234,7 @@ int run(const Call &c0) {
 
     Plan P;
     const Kind pk = (c.kind == KIND_4M) ? KIND_4M : KIND_REAL;
-    if (int rc = make_plan(pk, c.m, c.n, c.k, c.batch, c.s, P)) return rc;
+    if (int rc = make_plan(pk, c.m, c.n, c.k, c.batch, c.s, P, c.full)) return rc;
     size_t ws = plan_workspace(P);
     size_t t_bytes = 0;
     if (c.kind == KIND_3M) t_bytes = al256(sizeof(double) * c.m * c.n * c.batch);
@@ -1272,7 +1284,7 @@ int run(const Call &c0) {
     cudaFreeAsync(base, st);
     if (rc) return rc;
 
-    const uint64_t pr = (uint64_t)c.s * (c.s + 1) / 2;
+    const uint64_t pr = c.full ? (uint64_t)c.s * c.s : (uint64_t)c.s * (c.s + 1) / 2;
     const uint64_t mult = c.kind == KIND_REAL ? 1 : (c.kind == KIND_4M ? 4 : 3);
     g_stats.entries += (uint64_t)c.batch;
     g_stats.equiv += pr * mult * (uint64_t)c.batch;
@@ -1312,6 +1324,7 @@ Call make_call(Kind kind, char ta, char tb, int64_t m, int64_t n, int64_t k, con
     c.batch = batch;
     c.s = s;
     c.batched = batched;
+    c.full = t_full_pairs != 0;
     return c;
 }
 
@@ -1411,6 +1424,13 @@ int ozaki2_zgemm_strided_batched(char transa, char transb, int64_t m, int64_t n,
     return run(make_call_crt(KIND_4M, transa, transb, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta,
                              C, ldc, strideC, batch, num_moduli, true));
 }
+
+int ozaki_set_pair_set(int full) {
+    t_full_pairs = full ? 1 : 0;
+    return 0;
+}
+
+int ozaki_get_pair_set(void) { return t_full_pairs; }
 
 int ozaki_set_stream(void *stream) {
     t_stream = (cudaStream_t)stream;

@@ -21,19 +21,22 @@ __host__ __device__ constexpr int pp_min(int a, int b) { return a < b ? a : b; }
 __host__ __device__ constexpr int pp_max(int a, int b) { return a > b ? a : b; }
 __host__ __device__ constexpr int pp_npairs(int L, int s) { return pp_min(s, L - 1) - pp_max(1, L - s) + 1; }
 
-__host__ __device__ constexpr PassPlan make_pass_plan(int s) {
+// Levels Lmax .. 2: Lmax = s + 1 for the triangular pair set (R1), 2s for the
+// full set (R21, s <= 8 so that the 2s - 1 levels fit 4 passes).
+__host__ __device__ constexpr PassPlan make_pass_plan_L(int s, int Lmax) {
     PassPlan best{};
-    const int np = (s + 3) / 4;
+    const int nlev = Lmax - 1;
+    const int np = (nlev + 3) / 4;
     double best_worst = 1e30, best_bytes = 1e30;
     for (int c0 = 1; c0 <= 4; ++c0)
         for (int c1 = (np > 1 ? 1 : 0); c1 <= (np > 1 ? 4 : 0); ++c1)
             for (int c2 = (np > 2 ? 1 : 0); c2 <= (np > 2 ? 4 : 0); ++c2)
                 for (int c3 = (np > 3 ? 1 : 0); c3 <= (np > 3 ? 4 : 0); ++c3) {
-                    if (c0 + c1 + c2 + c3 != s) continue;
+                    if (c0 + c1 + c2 + c3 != nlev) continue;
                     const int c[4] = {c0, c1, c2, c3};
                     PassPlan cand{};
                     cand.npass = np;
-                    int hi = s + 1;
+                    int hi = Lmax;
                     double worst = 0, bytes = 0;
                     for (int q = 0; q < np; ++q) {
                         const int lo = hi - c[q] + 1;
@@ -58,5 +61,8 @@ __host__ __device__ constexpr PassPlan make_pass_plan(int s) {
                 }
     return best;
 }
+
+__host__ __device__ constexpr PassPlan make_pass_plan(int s) { return make_pass_plan_L(s, s + 1); }
+__host__ __device__ constexpr PassPlan make_pass_plan_full(int s) { return make_pass_plan_L(s, 2 * s); }
 
 }  // namespace ozk
