@@ -219,6 +219,64 @@ def _quick(beta, C):
     return out
 
 
+def blocked_product(A_op, B_op, s: int, kb: int, pairs: str = "triangular", cplx: bool = False):
+    """R22 (NEXT-4 per-block exponent alignment): K in blocks of kb; each block's product is
+    emulated with its OWN row / column exponents (O2..O6 on the sub-matrices), and the block
+    products are summed in ascending block order in FP64 (one RNE per addition).  Real:
+    returns P; complex (4M): returns (Pr, Pi)."""
+    k = A_op.shape[1]
+    acc = None
+    for b0 in range(0, k, kb):
+        Ab = A_op[:, b0:b0 + kb]
+        Bb = B_op[b0:b0 + kb, :]
+        Pb = zproduct(Ab, Bb, s, "4m", pairs) if cplx else emulated_product(Ab, Bb, s, pairs)
+        if acc is None:
+            acc = Pb
+        elif cplx:
+            acc = (acc[0] + Pb[0], acc[1] + Pb[1])       # numpy float64 '+' = one RNE each
+        else:
+            acc = acc + Pb
+    return acc
+
+
+def dgemm_blocked(transa, transb, alpha, A, B, beta, C, s: int, kb: int) -> np.ndarray:
+    """R22 DGEMM: per-block exponents, then O7 alpha/beta on the summed P."""
+    Aop = op(np.asarray(A, dtype=np.float64), transa)
+    Bop = op(np.asarray(B, dtype=np.float64), transb)
+    m, k = Aop.shape
+    n = Bop.shape[1]
+    C = np.zeros((m, n)) if C is None else np.asarray(C, dtype=np.float64)
+    if m == 0 or n == 0:
+        return C.copy()
+    if alpha == 0 or k == 0:
+        return _quick(beta, C)
+    P = blocked_product(Aop, Bop, s, kb)
+    out = _c(C, np.float64).copy()
+    lib().orc_apply_real(m * n, float(alpha), _ptr(_c(P, np.float64)), float(beta), _ptr(out))
+    return out
+
+
+def zgemm_blocked(transa, transb, alpha, A, B, beta, C, s: int, kb: int) -> np.ndarray:
+    """R22 ZGEMM (4M per block)."""
+    Aop = op(np.asarray(A, dtype=np.complex128), transa)
+    Bop = op(np.asarray(B, dtype=np.complex128), transb)
+    m, k = Aop.shape
+    n = Bop.shape[1]
+    alpha = complex(alpha)
+    beta = complex(beta)
+    C = np.zeros((m, n), dtype=np.complex128) if C is None else np.asarray(C, dtype=np.complex128)
+    if m == 0 or n == 0:
+        return C.copy()
+    if alpha == 0 or k == 0:
+        return _quick(beta, C)
+    Pr, Pi = blocked_product(Aop, Bop, s, kb, cplx=True)
+    Cr = _c(C.real, np.float64).copy()
+    Ci = _c(C.imag, np.float64).copy()
+    lib().orc_apply_complex(m * n, alpha.real, alpha.imag, _ptr(_c(Pr, np.float64)),
+                            _ptr(_c(Pi, np.float64)), beta.real, beta.imag, _ptr(Cr), _ptr(Ci))
+    return _cplx(Cr, Ci)
+
+
 def dgemm(transa, transb, alpha, A, B, beta, C, s: int, pairs: str = "triangular") -> np.ndarray:
     """Full emulated DGEMM: returns alpha*emul(op(A)op(B)) + beta*C (new array)."""
     Aop = op(np.asarray(A, dtype=np.float64), transa)
