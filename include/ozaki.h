@@ -177,6 +177,17 @@ int ozaki2_zgemm_strided_batched(char transa, char transb, int64_t m, int64_t n,
 int ozaki_set_pair_set(int full);
 int ozaki_get_pair_set(void);
 
+/* --- NEXT-4 variant: per-block exponent alignment (reading R22) -------------
+ * kb = 0 (default): one exponent per row of op(A) / column of op(B).  kb > 0:
+ * K is cut into blocks of kb; each block is emulated with its own row /
+ * column exponents (same slices, pairs and combine), the block products are
+ * summed in ascending block order in FP64 (one RNE each) into a workspace T,
+ * then C = alpha T + beta C (R7).  Thread-local, read at each Ozaki-I call;
+ * kb >= k is the per-row scheme.  Ozaki-II calls ignore it.  Returns -1 for
+ * kb < 0.                                                                    */
+int ozaki_set_exponent_block(int64_t kb);
+int64_t ozaki_get_exponent_block(void);
+
 /* --- streams, stats, errors --------------------------------------------- */
 /* stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
  * thread-local; returns 0.                                                 */

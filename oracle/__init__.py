@@ -219,7 +219,8 @@ def _quick(beta, C):
     return out
 
 
-def blocked_product(A_op, B_op, s: int, kb: int, pairs: str = "triangular", cplx: bool = False):
+def blocked_product(A_op, B_op, s: int, kb: int, pairs: str = "triangular", cplx: bool = False,
+                    method: str = "4m"):
     """R22 (NEXT-4 per-block exponent alignment): K in blocks of kb; each block's product is
     emulated with its OWN row / column exponents (O2..O6 on the sub-matrices), and the block
     products are summed in ascending block order in FP64 (one RNE per addition).  Real:
@@ -229,7 +230,7 @@ def blocked_product(A_op, B_op, s: int, kb: int, pairs: str = "triangular", cplx
     for b0 in range(0, k, kb):
         Ab = A_op[:, b0:b0 + kb]
         Bb = B_op[b0:b0 + kb, :]
-        Pb = zproduct(Ab, Bb, s, "4m", pairs) if cplx else emulated_product(Ab, Bb, s, pairs)
+        Pb = zproduct(Ab, Bb, s, method, pairs) if cplx else emulated_product(Ab, Bb, s, pairs)
         if acc is None:
             acc = Pb
         elif cplx:
@@ -256,8 +257,8 @@ def dgemm_blocked(transa, transb, alpha, A, B, beta, C, s: int, kb: int) -> np.n
     return out
 
 
-def zgemm_blocked(transa, transb, alpha, A, B, beta, C, s: int, kb: int) -> np.ndarray:
-    """R22 ZGEMM (4M per block)."""
+def zgemm_blocked(transa, transb, alpha, A, B, beta, C, s: int, kb: int, method: str = "4m") -> np.ndarray:
+    """R22 ZGEMM (4M or 3M per block)."""
     Aop = op(np.asarray(A, dtype=np.complex128), transa)
     Bop = op(np.asarray(B, dtype=np.complex128), transb)
     m, k = Aop.shape
@@ -269,7 +270,7 @@ def zgemm_blocked(transa, transb, alpha, A, B, beta, C, s: int, kb: int) -> np.n
         return C.copy()
     if alpha == 0 or k == 0:
         return _quick(beta, C)
-    Pr, Pi = blocked_product(Aop, Bop, s, kb, cplx=True)
+    Pr, Pi = blocked_product(Aop, Bop, s, kb, cplx=True, method=method)
     Cr = _c(C.real, np.float64).copy()
     Ci = _c(C.imag, np.float64).copy()
     lib().orc_apply_complex(m * n, alpha.real, alpha.imag, _ptr(_c(Pr, np.float64)),

@@ -72,6 +72,10 @@ def lib():
     L.ozaki_zgemm_strided_batched.argtypes = [c, c, i64, i64, i64, dP, p, i64, i64, p, i64, i64,
                                               dP, p, i64, i64, i64, i32]
     L.ozaki_zgemm3m_strided_batched.argtypes = L.ozaki_zgemm_strided_batched.argtypes
+    L.ozaki_set_exponent_block.argtypes = [i64]
+    L.ozaki_set_exponent_block.restype = i32
+    L.ozaki_get_exponent_block.argtypes = []
+    L.ozaki_get_exponent_block.restype = i64
     L.ozaki_set_pair_set.argtypes = [i32]
     L.ozaki_set_pair_set.restype = i32
     L.ozaki_get_pair_set.argtypes = []
@@ -303,6 +307,15 @@ def set_pair_set(kind: str) -> None:
 
 def get_pair_set() -> str:
     return "full" if lib().ozaki_get_pair_set() else "triangular"
+
+
+def set_exponent_block(kb: int) -> None:
+    """Per-block exponent alignment along K for this thread (R22, NEXT-4); 0 = per row/column."""
+    _check(lib().ozaki_set_exponent_block(int(kb)), "ozaki_set_exponent_block")
+
+
+def get_exponent_block() -> int:
+    return int(lib().ozaki_get_exponent_block())
 
 
 def set_stream(stream) -> None:

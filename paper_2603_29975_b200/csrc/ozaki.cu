@@ -35,6 +35,7 @@ namespace {
 thread_local cudaStream_t t_stream = nullptr;
 thread_local std::string t_err;
 thread_local int t_full_pairs = 0;   // R21 pair set for Ozaki-I calls (ozaki_set_pair_set)
+thread_local int64_t t_kblock = 0;    // R22 exponent block along K (0 = per row / column)
 
 struct Stats {
     std::atomic<uint64_t> dgemm{0}, zgemm{0}, zgemm3m{0}, entries{0}, equiv{0}, macs{0},
@@ -336,6 +337,31 @@ __global__ void k_combine_3m(const double *T1, const double *T2, const double *T
             ti = __fma_rn(br, c.y, __dmul_rn(bi, c.x));
         }
         *cp = make_double2(__fma_rn(ar, pr, __fma_rn(-ai, pi, tr)), __fma_rn(ar, pi, __fma_rn(ai, pr, ti)));
+    }
+}
+
+// R22: C = alpha T + beta C with R7's operation shapes (T: batch x m x n, ld m).
+__global__ void k_apply_ab(const double *T, double *C, int64_t m, int64_t n, int64_t ldc, int64_t strideC,
+                           int cplx, double ar, double ai, double br, double bi) {
+    const int64_t b = blockIdx.z;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < m * n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx % m, j = idx / m;
+        if (!cplx) {
+            const double P = T[b * m * n + idx];
+            double *cp = C + b * strideC + i + j * ldc;
+            *cp = (br == 0.0) ? __dmul_rn(ar, P) : __fma_rn(ar, P, __dmul_rn(br, *cp));
+        } else {
+            const double2 P = reinterpret_cast<const double2 *>(T)[b * m * n + idx];
+            double2 *cp = reinterpret_cast<double2 *>(C) + b * strideC + i + j * ldc;
+            double tr = 0.0, ti = 0.0;
+            if (!(br == 0.0 && bi == 0.0)) {
+                const double2 cv = *cp;
+                tr = __fma_rn(br, cv.x, -__dmul_rn(bi, cv.y));
+                ti = __fma_rn(br, cv.y, __dmul_rn(bi, cv.x));
+            }
+            *cp = make_double2(__fma_rn(ar, P.x, __fma_rn(-ai, P.y, tr)), __fma_rn(ar, P.y, __fma_rn(ai, P.x, ti)));
+        }
     }
 }
 
@@ -735,6 +761,7 @@ struct Call {
     int32_t *S_out;   // debug level dump (real only)
     bool crt;         // Ozaki-II (NEXT-1)
     bool full;        // Ozaki-I full pair set (R21, NEXT-4)
+    int64_t kblock;   // R22 per-block exponents (0: per row / column)
 };
 
 int validate(const Call &c) {
@@ -1232,6 +1259,46 @@ int run(const Call &c0) {
 
     if (c.crt) return run_crt(c, dev, st);
 
+    // R22 (NEXT-4): per-block exponents -- emulate each K block with its own exponents into T
+    // (T = P_0, then T = P_b + T: one RNE per block), then C = alpha T + beta C.
+    if (c.kblock > 0 && c.kblock < c.k && !c.S_out) {
+        const size_t tb = al256(es * (size_t)c.m * c.n * c.batch);
+        double *T = nullptr;
+        {
+            cudaError_t e = cudaMallocAsync((void **)&T, tb, st);
+            if (e != cudaSuccess) return fail(OZAKI_ERR_ALLOC, "cudaMallocAsync(%zu): %s", tb, cudaGetErrorString(e));
+        }
+        const int64_t ew = cplx ? 2 : 1;   // doubles per element
+        int rc = 0;
+        for (int64_t b0 = 0; b0 < c.k && !rc; b0 += c.kblock) {
+            Call cb = c;
+            cb.k = std::min<int64_t>(c.kblock, c.k - b0);
+            cb.A = c.A + ew * (c.ta == 'N' ? b0 * c.lda : b0);
+            cb.B = c.B + ew * (c.tb == 'N' ? b0 : b0 * c.ldb);
+            cb.C = T;
+            cb.ldc = c.m;
+            cb.sC = c.m * c.n;
+            cb.al[0] = 1.0;
+            cb.al[1] = 0.0;
+            cb.be[0] = (b0 == 0) ? 0.0 : 1.0;
+            cb.be[1] = 0.0;
+            cb.kblock = 0;
+            cb.batched = true;
+            rc = run(cb);
+        }
+        if (!rc) {
+            dim3 grid(grid1d(c.m * c.n, dev->sms), 1, (unsigned)c.batch);
+            ProfScope ps(st, PH_OTHER);
+            k_apply_ab<<<grid, 256, 0, st>>>(T, c.C, c.m, c.n, c.ldc, c.sC, cplx ? 1 : 0, c.al[0], c.al[1],
+                                            c.be[0], c.be[1]);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) rc = fail(OZAKI_ERR_CUDA, "apply_ab: %s", cudaGetErrorString(e));
+            g_stats.launches += 1;
+        }
+        cudaFreeAsync(T, st);
+        return rc;
+    }
+
     Plan P;
     const Kind pk = (c.kind == KIND_4M) ? KIND_4M : KIND_REAL;
     if (int rc = make_plan(pk, c.m, c.n, c.k, c.batch, c.s, P, c.full)) return rc;
@@ -1325,6 +1392,7 @@ Call make_call(Kind kind, char ta, char tb, int64_t m, int64_t n, int64_t k, con
     c.s = s;
     c.batched = batched;
     c.full = t_full_pairs != 0;
+    c.kblock = t_kblock;
     return c;
 }
 
@@ -1424,6 +1492,14 @@ int ozaki2_zgemm_strided_batched(char transa, char transb, int64_t m, int64_t n,
     return run(make_call_crt(KIND_4M, transa, transb, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta,
                              C, ldc, strideC, batch, num_moduli, true));
 }
+
+int ozaki_set_exponent_block(int64_t kb) {
+    if (kb < 0) return fail(-1, "exponent block < 0");
+    t_kblock = kb;
+    return 0;
+}
+
+int64_t ozaki_get_exponent_block(void) { return t_kblock; }
 
 int ozaki_set_pair_set(int full) {
     t_full_pairs = full ? 1 : 0;
