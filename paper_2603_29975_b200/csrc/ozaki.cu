@@ -172,6 +172,7 @@ struct Plan {
     int64_t Kp, KB;      // padded depth (bytes) and 32-B blocks
     int64_t tiles_m, tiles_n;
     size_t a_bytes, b_bytes, ea_bytes, fb_bytes;   // per whole batch, 256-B aligned
+    size_t a_bytes_entry, b_bytes_entry;           // slice bytes of one batch entry (unaligned)
     int kps, stages;
     size_t smem;
     bool kchunk_needed;      // s * k_eff > 131071 (reading R8)
@@ -260,13 +261,17 @@ int make_plan(Kind kind, int64_t m, int64_t n, int64_t k, int64_t batch, int s, 
     if (P.pair) {   // super-tiles of 256 x 128; A in 128-row tiles (padded to pairs), B in 64-row halves
         P.tiles_m = (P.Mp + 2 * kBM - 1) / (2 * kBM);
         P.tiles_n = (P.Np + kLvBN - 1) / kLvBN;
-        P.a_bytes = al256((size_t)s * kBM * kKB * P.KB * (2 * P.tiles_m) * batch);
-        P.b_bytes = al256((size_t)s * (kLvBN / 2) * kKB * P.KB * (2 * P.tiles_n) * batch);
+        P.a_bytes_entry = (size_t)s * kBM * kKB * P.KB * (2 * P.tiles_m);
+        P.b_bytes_entry = (size_t)s * (kLvBN / 2) * kKB * P.KB * (2 * P.tiles_n);
+        P.a_bytes = al256(P.a_bytes_entry * batch);
+        P.b_bytes = al256(P.b_bytes_entry * batch);
     } else {
         P.tiles_m = (P.Mp + kBM - 1) / kBM;
         P.tiles_n = (P.Np + P.BN - 1) / P.BN;
-        P.a_bytes = al256((size_t)s * kBM * kKB * P.KB * P.tiles_m * batch);
-        P.b_bytes = al256((size_t)s * P.BN * kKB * P.KB * P.tiles_n * batch);
+        P.a_bytes_entry = (size_t)s * kBM * kKB * P.KB * P.tiles_m;
+        P.b_bytes_entry = (size_t)s * P.BN * kKB * P.KB * P.tiles_n;
+        P.a_bytes = al256(P.a_bytes_entry * batch);
+        P.b_bytes = al256(P.b_bytes_entry * batch);
     }
     const size_t a_kb = (size_t)s * kBM * kKB, b_kb = (size_t)s * P.BN * kKB;
     P.ea_bytes = al256(sizeof(int32_t) * P.Mp * batch);
@@ -395,7 +400,7 @@ struct Operand {
 };
 
 int launch_split(const Plan &P, const Operand &op, bool sideA, int8_t *slices, int32_t *exps,
-                 DevState *dev, cudaStream_t st) {
+                 DevState *dev, cudaStream_t st, int64_t x_batch = 0) {
     SplitParams sp{};
     sp.X = op.X;
     sp.rs = op.rs;
@@ -417,10 +422,17 @@ int launch_split(const Plan &P, const Operand &op, bool sideA, int8_t *slices, i
     sp.out = slices;
     sp.exps = exps;
     sp.nonfinite = dev->nonfinite;
+    // SPLIT_3M: the plan covers 3 x x_batch entries; the three operands go to regions x = 0, 1, 2
+    int64_t gb = P.batch;
+    if (op.mode == SPLIT_3M) {
+        gb = x_batch;
+        sp.x_bytes = (int64_t)((sideA ? P.a_bytes_entry : P.b_bytes_entry) * x_batch);
+        sp.x_exps = (sideA ? P.Mp : P.Np) * x_batch;
+    }
     if (op.rows == 0) return 0;
     const bool rcontig = (op.rs == 1);
     const bool cplx = op.mode != SPLIT_REAL;
-    dim3 grid((unsigned)((sp.rows_grid + 7) / 8), (unsigned)P.batch);
+    dim3 grid((unsigned)((sp.rows_grid + 7) / 8), (unsigned)gb);
     // SMEM window: 8 rows x KW elements (+ pad), 64 KB
     int KW = cplx ? 512 : 1024;
     if (const char *kw = getenv("OZAKI_SPLIT_KW")) {   // tuning hook: window elements per row
@@ -1301,7 +1313,9 @@ int run(const Call &c0) {
 
     Plan P;
     const Kind pk = (c.kind == KIND_4M) ? KIND_4M : KIND_REAL;
-    if (int rc = make_plan(pk, c.m, c.n, c.k, c.batch, c.s, P, c.full)) return rc;
+    // 3M: the three real products run as 3 x batch entries of ONE plan / split / GEMM launch
+    const int64_t pbatch = (c.kind == KIND_3M) ? 3 * c.batch : c.batch;
+    if (int rc = make_plan(pk, c.m, c.n, c.k, pbatch, c.s, P, c.full)) return rc;
     size_t ws = plan_workspace(P);
     size_t t_bytes = 0;
     if (c.kind == KIND_3M) t_bytes = al256(sizeof(double) * c.m * c.n * c.batch);
@@ -1328,20 +1342,17 @@ int run(const Call &c0) {
             const int epi = c.S_out ? EPI_LEVELS : (c.kind == KIND_4M ? EPI_CPLX4M : EPI_REAL);
             rc = launch_gemm(P, epi, sa, sb, ea, fb, c.C, c.ldc, c.sC, c.al, c.be, c.S_out, dev, st);
         }
-    } else {   // 3M: three emulated real products into T, then the combine
-        const int modes[3] = {SPLIT_RE, SPLIT_IM, SPLIT_SUM};
+    } else {   // 3M: one fused split per operand (Re, Im, fl(Re+Im) regions) and ONE GEMM launch
+               // over 3 x batch entries into T = [T1 | T2 | T3], then the combine
         const double one[2] = {1.0, 0.0}, zero[2] = {0.0, 0.0};
-        for (int x = 0; x < 3 && !rc; ++x) {
-            double *Tx = (double *)((char *)T + x * t_bytes);
-            rc = launch_split(P, view_A(c.A, c.ta, c.m, c.k, c.lda, c.sA, modes[x]), true, sa, ea, dev, st);
-            if (!rc) rc = launch_split(P, view_B(c.B, c.tb, c.n, c.k, c.ldb, c.sB, modes[x]), false, sb, fb, dev, st);
-            if (!rc) rc = launch_gemm(P, EPI_REAL, sa, sb, ea, fb, Tx, c.m, c.m * c.n, one, zero, nullptr, dev, st);
-        }
+        rc = launch_split(P, view_A(c.A, c.ta, c.m, c.k, c.lda, c.sA, SPLIT_3M), true, sa, ea, dev, st, c.batch);
+        if (!rc) rc = launch_split(P, view_B(c.B, c.tb, c.n, c.k, c.ldb, c.sB, SPLIT_3M), false, sb, fb, dev, st, c.batch);
+        if (!rc) rc = launch_gemm(P, EPI_REAL, sa, sb, ea, fb, T, c.m, c.m * c.n, one, zero, nullptr, dev, st);
         if (!rc) {
             dim3 grid(grid1d(c.m * c.n, dev->sms), 1, (unsigned)c.batch);
             ProfScope ps(st, PH_OTHER);
-            k_combine_3m<<<grid, 256, 0, st>>>(T, (double *)((char *)T + t_bytes),
-                                              (double *)((char *)T + 2 * t_bytes), c.C, c.m, c.n,
+            const int64_t tx = c.m * c.n * c.batch;   // the GEMM wrote T1, T2, T3 back to back
+            k_combine_3m<<<grid, 256, 0, st>>>(T, T + tx, T + 2 * tx, c.C, c.m, c.n,
                                               c.ldc, c.sC, c.al[0], c.al[1], c.be[0], c.be[1]);
             cudaError_t e = cudaGetLastError();
             if (e != cudaSuccess) rc = fail(OZAKI_ERR_CUDA, "combine_3m: %s", cudaGetErrorString(e));

@@ -36,6 +36,7 @@ enum SplitMode : int {
     SPLIT_RE = 3,     // 3M operands: Re, Im, fl(Re + Im)
     SPLIT_IM = 4,
     SPLIT_SUM = 5,
+    SPLIT_3M = 6,     // all three 3M operands (Re, Im, fl(Re + Im)) in one pass, regions x = 0, 1, 2
 };
 
 struct SplitParams {
@@ -55,6 +56,8 @@ struct SplitParams {
     unsigned long long *nonfinite;   // device counter (rows/cols with Inf/NaN)
     int64_t kbs_bytes;    // bytes between k-blocks of one tile (Ozaki-I: s*blk; Ozaki-II: blk)
     int64_t ss_bytes;     // bytes between slices / moduli  (Ozaki-I: blk;  Ozaki-II: KB*blk)
+    int64_t x_bytes;      // SPLIT_3M: bytes between the Re / Im / Sum slice regions
+    int64_t x_exps;       // SPLIT_3M: exponents between the three regions
     CrtTab crt;           // Ozaki-II constants (CRT instantiation only)
 };
 
@@ -232,6 +235,8 @@ __global__ void __launch_bounds__(256) k_split_sm(const __grid_constant__ SplitP
     __shared__ uint32_t s_nf[8][33];
     __shared__ int32_t s_e[8];
     __shared__ double s_scale[8];
+    __shared__ int32_t s_e3[3][8];         // SPLIT_3M: per-operand exponents / scales
+    __shared__ double s_scale3[3][8];
     __shared__ int8_t *s_rowbase[16];      // output row base (tile, row-in-tile part of the address)
     using Elem = typename std::conditional<CPLX, double2, double>::type;
     constexpr int ES = sizeof(Elem);
@@ -287,7 +292,53 @@ __global__ void __launch_bounds__(256) k_split_sm(const __grid_constant__ SplitP
     };
 
     // ---------------- pass 1: exponents
-    {
+    if (CPLX && !CRT && p.mode == SPLIT_3M) {
+        // R9 3M: three operands Re, Im (conj applied) and fl(Re + Im), each with its own exponent
+        const int row = tid >> 5, lane = tid & 31;
+        uint64_t m3[3] = {0, 0, 0};
+        for (int64_t w = 0; w < nwin; ++w) {
+            const int64_t w0 = w * KW;
+            load_window(w0);
+            __syncthreads();
+            const int wlen = (int)min((int64_t)KW, p.k - w0);
+            if (row < nrows) {
+                const double *src = reinterpret_cast<const double *>(slab + row * ld);
+                for (int l = lane; l < wlen; l += 32) {
+                    const double re = src[2 * l], im = p.conj ? -src[2 * l + 1] : src[2 * l + 1];
+                    const uint64_t u0 = (uint64_t)__double_as_longlong(re) & kAbsMask;
+                    const uint64_t u1 = (uint64_t)__double_as_longlong(im) & kAbsMask;
+                    const uint64_t u2 = (uint64_t)__double_as_longlong(__dadd_rn(re, im)) & kAbsMask;
+                    m3[0] = u0 > m3[0] ? u0 : m3[0];
+                    m3[1] = u1 > m3[1] ? u1 : m3[1];
+                    m3[2] = u2 > m3[2] ? u2 : m3[2];
+                }
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int x = 0; x < 3; ++x) {
+            uint64_t m = m3[x];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const uint64_t om = __shfl_xor_sync(0xffffffffu, m, o);
+                m = om > m ? om : m;
+            }
+            if (lane == 0) {
+                int32_t e = 0;
+                if (row < nrows) {
+                    const uint32_t nf3 = (m >= kExpInf);
+                    e = nf3 ? kNonFinite : exponent_from_maxbits(m);
+                    p.exps[x * p.x_exps + b * p.rows_out + r0 + row] = e;
+                    if (nf3) atomicAdd(p.nonfinite, 1ull);
+                }
+                s_e3[x][row] = e;
+                const int sh = 8 * p.s - 1 - e;
+                s_scale3[x][row] = (sh >= -1022 && sh <= 1023) ? pow2(sh) : 0.0;
+                if (x == 0) s_e[row] = 0;   // pass 2's row-liveness; each operand checks its own e
+            }
+        }
+        __syncthreads();
+    } else {
         const int row = tid >> 5, lane = tid & 31;
         uint64_t m = 0;
         uint32_t nf = 0;
@@ -396,6 +447,22 @@ __global__ void __launch_bounds__(256) k_split_sm(const __grid_constant__ SplitP
                 };
                 double v[8];
                 switch (p.mode) {
+                    case SPLIT_3M:
+                        if constexpr (!CRT) {
+                            const bool live3 = row < nrows;
+#pragma unroll 1
+                            for (int x = 0; x < 3; ++x) {
+                                const int32_t ex = s_e3[x][row];
+                                if (live3 && ex != kNonFinite) comp8(x, v);
+                                else {
+#pragma unroll
+                                    for (int q = 0; q < 8; ++q) v[q] = 0.0;
+                                }
+                                digits_store8<SMAX>(v, s_scale3[x][row], ex, p.s,
+                                                    s_rowbase[row] + x * p.x_bytes + coff, nullptr, nullptr, blk);
+                            }
+                        }
+                        break;
                     case SPLIT_RE:
                     case SPLIT_IM:
                     case SPLIT_SUM:
