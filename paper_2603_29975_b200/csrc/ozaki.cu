@@ -855,7 +855,12 @@ int run_offload(const Call &c) {
     const int64_t spanA = (ac - 1) * c.lda + ar, spanB = (bc - 1) * c.ldb + br, spanC = (c.n - 1) * c.ldc + c.m;
     const bool readC = !(c.be[0] == 0.0 && c.be[1] == 0.0);
     const size_t per_entry = (size_t)(spanA + spanB + spanC) * es;
-    int64_t cb = (int64_t)((64ull << 20) / std::max<size_t>(per_entry, 1));   // ~64 MB per chunk
+    size_t chunk_bytes = 32ull << 20;   // ~32 MB per chunk (measured best: 5.6 vs 5.9 ms for C2x30; OZAKI_OFFLOAD_CHUNK_MB overrides)
+    if (const char *ce = getenv("OZAKI_OFFLOAD_CHUNK_MB")) {
+        const long long v = atoll(ce);
+        if (v >= 1 && v <= 4096) chunk_bytes = (size_t)v << 20;
+    }
+    int64_t cb = (int64_t)(chunk_bytes / std::max<size_t>(per_entry, 1));
     cb = std::max<int64_t>(1, std::min<int64_t>(cb, (c.batch + 1) / 2 > 0 ? (c.batch + 1) / 2 : 1));
     const int64_t nchunk = (c.batch + cb - 1) / cb;
     OffloadCtx *o = nullptr;
