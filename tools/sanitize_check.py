@@ -21,5 +21,15 @@ oz.dgemm("N", "N", 1.0, dev(A), dev(synth.uniform(70, 150, seed=5)), 0.0, C, 6)
 del os.environ["OZAKI_KCHUNK_KB"]
 oz.debug_split("B", "z", "N", dev(W), 8)
 oz.debug_level_sums("N", "N", dev(A), dev(synth.uniform(70, 150, seed=5)), 4)
+# Ozaki-II: split variant, residue GEMM, CRT (real and 4M, ragged)
+oz.ozaki2_dgemm("N", "T", 1.0, dev(A), dev(B.T.copy()), 0.0, C, 14)
+oz.ozaki2_zgemm("N", "N", 1.0, dev(Z), dev(W), 0.5, Zc, 12)
+# NEXT-4: full pair set, per-block exponents
+oz.set_pair_set("full")
+oz.dgemm("N", "N", 1.0, dev(A), dev(synth.uniform(70, 150, seed=6)), 0.0, C, 5)
+oz.set_pair_set("triangular")
+oz.set_exponent_block(32)
+oz.zgemm("N", "N", 1.0, dev(Z), dev(W), 0.0, Zc, 6)
+oz.set_exponent_block(0)
 torch.cuda.synchronize()
 print("sanitize_check done")
