@@ -399,8 +399,8 @@ struct Operand {
     int mode, conj;
 };
 
-int launch_split(const Plan &P, const Operand &op, bool sideA, int8_t *slices, int32_t *exps,
-                 DevState *dev, cudaStream_t st, int64_t x_batch = 0) {
+SplitParams split_params(const Plan &P, const Operand &op, bool sideA, int8_t *slices, int32_t *exps,
+                         DevState *dev, int64_t x_batch) {
     SplitParams sp{};
     sp.X = op.X;
     sp.rs = op.rs;
@@ -418,21 +418,27 @@ int launch_split(const Plan &P, const Operand &op, bool sideA, int8_t *slices, i
     sp.KB = P.KB;
     sp.kh = P.kh;
     sp.rows_out = (op.mode == SPLIT_B4M) ? 2 * op.rows : op.rows;
-    sp.rows_grid = (op.mode == SPLIT_B4M) ? sp.tiles * sp.tile_h / 2 : sp.tiles * sp.tile_h;
+    sp.rows_grid = (op.rows == 0) ? 0 : ((op.mode == SPLIT_B4M) ? sp.tiles * sp.tile_h / 2 : sp.tiles * sp.tile_h);
     sp.out = slices;
     sp.exps = exps;
     sp.nonfinite = dev->nonfinite;
     // SPLIT_3M: the plan covers 3 x x_batch entries; the three operands go to regions x = 0, 1, 2
-    int64_t gb = P.batch;
     if (op.mode == SPLIT_3M) {
-        gb = x_batch;
         sp.x_bytes = (int64_t)((sideA ? P.a_bytes_entry : P.b_bytes_entry) * x_batch);
         sp.x_exps = (sideA ? P.Mp : P.Np) * x_batch;
     }
-    if (op.rows == 0) return 0;
-    const bool rcontig = (op.rs == 1);
-    const bool cplx = op.mode != SPLIT_REAL;
-    dim3 grid((unsigned)((sp.rows_grid + 7) / 8), (unsigned)gb);
+    return sp;
+}
+
+// K1 for one (b == nullptr) or both operands in one launch.
+int launch_split_sides(const Plan &P, const SplitParams &a, const SplitParams *b, int64_t gb, cudaStream_t st) {
+    SplitPair pp;
+    pp.side[0] = a;
+    pp.side[1] = b ? *b : a;
+    const int64_t rows_grid = std::max(a.rows_grid, b ? b->rows_grid : 0);
+    if (rows_grid == 0) return 0;
+    const bool cplx = a.mode != SPLIT_REAL;
+    dim3 grid((unsigned)((rows_grid + 7) / 8), (unsigned)gb, b ? 2u : 1u);
     // SMEM window: 8 rows x KW elements (+ pad), 64 KB
     int KW = cplx ? 512 : 1024;
     if (const char *kw = getenv("OZAKI_SPLIT_KW")) {   // tuning hook: window elements per row
@@ -442,28 +448,40 @@ int launch_split(const Plan &P, const Operand &op, bool sideA, int8_t *slices, i
     const size_t smem = (size_t)8 * (KW + (cplx ? 1 : 2)) * (cplx ? 16 : 8);
     {
         ProfScope ps(st, PH_SLICE);
-#define OZK_SPLIT(SM, RC, CX)                                                                       \
+#define OZK_SPLIT(SM, CX)                                                                           \
         {                                                                                           \
             static size_t attr = 0;                                                                 \
             if (attr < smem) {                                                                      \
-                cudaFuncSetAttribute(k_split_sm<SM, RC, CX>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                cudaFuncSetAttribute(k_split_sm<SM, CX>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                      (int)smem);                                                    \
                 attr = smem;                                                                        \
             }                                                                                       \
-            k_split_sm<SM, RC, CX><<<grid, 256, smem, st>>>(sp, KW);                                \
+            k_split_sm<SM, CX><<<grid, 256, smem, st>>>(pp, KW);                                    \
         }
         if (P.s <= 8) {
-            if (rcontig) { if (cplx) OZK_SPLIT(8, true, true) else OZK_SPLIT(8, true, false) }
-            else { if (cplx) OZK_SPLIT(8, false, true) else OZK_SPLIT(8, false, false) }
+            if (cplx) OZK_SPLIT(8, true) else OZK_SPLIT(8, false)
         } else {
-            if (rcontig) { if (cplx) OZK_SPLIT(16, true, true) else OZK_SPLIT(16, true, false) }
-            else { if (cplx) OZK_SPLIT(16, false, true) else OZK_SPLIT(16, false, false) }
+            if (cplx) OZK_SPLIT(16, true) else OZK_SPLIT(16, false)
         }
 #undef OZK_SPLIT
     }
     CUDA_TRY(cudaGetLastError());
     g_stats.launches += 1;
     return 0;
+}
+
+int launch_split(const Plan &P, const Operand &op, bool sideA, int8_t *slices, int32_t *exps,
+                 DevState *dev, cudaStream_t st, int64_t x_batch = 0) {
+    const SplitParams sp = split_params(P, op, sideA, slices, exps, dev, x_batch);
+    return launch_split_sides(P, sp, nullptr, op.mode == SPLIT_3M ? x_batch : P.batch, st);
+}
+
+// both operands of one product in a single launch
+int launch_split_ab(const Plan &P, const Operand &oa, int8_t *sa, int32_t *ea, const Operand &ob, int8_t *sb,
+                    int32_t *fb, DevState *dev, cudaStream_t st, int64_t x_batch = 0) {
+    const SplitParams pa = split_params(P, oa, true, sa, ea, dev, x_batch);
+    const SplitParams pb = split_params(P, ob, false, sb, fb, dev, x_batch);
+    return launch_split_sides(P, pa, &pb, oa.mode == SPLIT_3M ? x_batch : P.batch, st);
 }
 
 // ---------------------------------------------------------------- K2 launch
@@ -1096,24 +1114,25 @@ int run_crt(const Call &c, DevState *dev, cudaStream_t st) {
         sp.crt = h.tab;
         sp.crt.nu = nu;
         if (op.rows == 0) return 0;
-        const bool rcontig = (op.rs == 1);
         const bool cx = op.mode != SPLIT_REAL;
         dim3 grid((unsigned)((sp.rows_grid + 7) / 8), (unsigned)c.batch);
         const int KW = cx ? 512 : 1024;
         const size_t smem = (size_t)8 * (KW + (cx ? 1 : 2)) * (cx ? 16 : 8);
+        SplitPair pp;
+        pp.side[0] = sp;
+        pp.side[1] = sp;
         ProfScope ps(st, PH_SLICE);
-#define OZK_SPLIT2(RC, CX)                                                                           \
+#define OZK_SPLIT2(CX)                                                                               \
         {                                                                                            \
             static bool attr = false;                                                                \
             if (!attr) {                                                                             \
-                cudaFuncSetAttribute(k_split_sm<8, RC, CX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                cudaFuncSetAttribute(k_split_sm<8, CX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                      (int)smem);                                                     \
                 attr = true;                                                                         \
             }                                                                                        \
-            k_split_sm<8, RC, CX, true><<<grid, 256, smem, st>>>(sp, KW);                           \
+            k_split_sm<8, CX, true><<<grid, 256, smem, st>>>(pp, KW);                               \
         }
-        if (rcontig) { if (cx) OZK_SPLIT2(true, true) else OZK_SPLIT2(true, false) }
-        else { if (cx) OZK_SPLIT2(false, true) else OZK_SPLIT2(false, false) }
+        if (cx) OZK_SPLIT2(true) else OZK_SPLIT2(false)
 #undef OZK_SPLIT2
         CUDA_TRY(cudaGetLastError());
         g_stats.launches += 1;
@@ -1341,8 +1360,8 @@ int run(const Call &c0) {
     if (c.kind == KIND_REAL || c.kind == KIND_4M) {
         const int ma = (c.kind == KIND_4M) ? SPLIT_A4M : SPLIT_REAL;
         const int mb = (c.kind == KIND_4M) ? SPLIT_B4M : SPLIT_REAL;
-        rc = launch_split(P, view_A(c.A, c.ta, c.m, c.k, c.lda, c.sA, ma), true, sa, ea, dev, st);
-        if (!rc) rc = launch_split(P, view_B(c.B, c.tb, c.n, c.k, c.ldb, c.sB, mb), false, sb, fb, dev, st);
+        rc = launch_split_ab(P, view_A(c.A, c.ta, c.m, c.k, c.lda, c.sA, ma), sa, ea,
+                             view_B(c.B, c.tb, c.n, c.k, c.ldb, c.sB, mb), sb, fb, dev, st);
         if (!rc) {
             const int epi = c.S_out ? EPI_LEVELS : (c.kind == KIND_4M ? EPI_CPLX4M : EPI_REAL);
             rc = launch_gemm(P, epi, sa, sb, ea, fb, c.C, c.ldc, c.sC, c.al, c.be, c.S_out, dev, st);
@@ -1350,8 +1369,8 @@ int run(const Call &c0) {
     } else {   // 3M: one fused split per operand (Re, Im, fl(Re+Im) regions) and ONE GEMM launch
                // over 3 x batch entries into T = [T1 | T2 | T3], then the combine
         const double one[2] = {1.0, 0.0}, zero[2] = {0.0, 0.0};
-        rc = launch_split(P, view_A(c.A, c.ta, c.m, c.k, c.lda, c.sA, SPLIT_3M), true, sa, ea, dev, st, c.batch);
-        if (!rc) rc = launch_split(P, view_B(c.B, c.tb, c.n, c.k, c.ldb, c.sB, SPLIT_3M), false, sb, fb, dev, st, c.batch);
+        rc = launch_split_ab(P, view_A(c.A, c.ta, c.m, c.k, c.lda, c.sA, SPLIT_3M), sa, ea,
+                             view_B(c.B, c.tb, c.n, c.k, c.ldb, c.sB, SPLIT_3M), sb, fb, dev, st, c.batch);
         if (!rc) rc = launch_gemm(P, EPI_REAL, sa, sb, ea, fb, T, c.m, c.m * c.n, one, zero, nullptr, dev, st);
         if (!rc) {
             dim3 grid(grid1d(c.m * c.n, dev->sms), 1, (unsigned)c.batch);

@@ -228,8 +228,17 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // CRT = false: Ozaki-I digits (R3, R4); CRT = true: Ozaki-II exponent, int64
 // quantisation and centred residues per modulus (R17, R18), written
 // modulus-major within a tile (contiguous k-blocks per modulus).
-template <int SMAX, bool RCONTIG, bool CPLX, bool CRT = false>
-__global__ void __launch_bounds__(256) k_split_sm(const __grid_constant__ SplitParams p, int KW) {
+// Both operands of a GEMM in ONE launch: blockIdx.z selects the side (one launch gap and one
+// tail fewer than two launches); the row-contiguity of the view is a runtime property.
+struct SplitPair {
+    SplitParams side[2];
+};
+
+template <int SMAX, bool CPLX, bool CRT = false>
+__global__ void __launch_bounds__(256) k_split_sm(const __grid_constant__ SplitPair pp, int KW) {
+    const SplitParams &p = pp.side[blockIdx.z];
+    if ((int64_t)blockIdx.x * 8 >= p.rows_grid) return;   // the other side needs more row groups
+    const bool RCONTIG = (p.rs == 1);                     // 8 rows adjacent in memory for each l
     extern __shared__ __align__(16) uint8_t sbuf[];
     __shared__ uint64_t s_max[8][33];
     __shared__ uint32_t s_nf[8][33];

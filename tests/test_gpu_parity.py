@@ -324,9 +324,9 @@ def test_stats_closed_forms():
     # s(s+1)/2 per real product, x4 (4M), x3 (3M)
     assert st["int8_gemm_equiv"] == 15 + 4 * 15 + 3 * 15
     assert st["dgemm_calls"] == 1 and st["zgemm_calls"] == 1 and st["zgemm3m_calls"] == 1
-    # dgemm: 2 splits + 1 GEMM; zgemm 4M: same; zgemm3m: 2 fused splits (Re/Im/Sum) + ONE GEMM
-    # launch over the three products + the combine
-    assert st["kernel_launches"] == 3 + 3 + (2 + 1 + 1)
+    # dgemm: 1 split launch (both operands) + 1 GEMM; zgemm 4M: same; zgemm3m: 1 split launch
+    # (both operands, Re/Im/Sum) + ONE GEMM launch over the three products + the combine
+    assert st["kernel_launches"] == 2 + 2 + (1 + 1 + 1)
 
 
 _VARIANT_SNIPPET = r"""
