@@ -148,6 +148,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     cluster_sync();          // barriers of both CTAs initialised, TMEM allocated
     tc_fence_after();
     const uint32_t tbase = *tholder;
+    // Programmatic dependent launch: the prologue above overlaps the producer kernel's tail
+    // (K1); everything below reads its output (slices, exponents), so wait for its completion.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp == 0) {
         // ========================= producer (both CTAs): own A rows, own B half

@@ -553,7 +553,17 @@ int launch_gemm_lv2(const Plan &P, const GemmParams &gp, size_t a_avail, size_t 
     const unsigned pairs = (unsigned)std::min<int64_t>(tiles, dev->sms / 2);
     {
         ProfScope ps(st, PH_GEMM);
-        k_gemm_lv2<EPI, CHUNK, FULL><<<2 * pairs, kThreads2, P.smem, st>>>(P2);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * pairs);
+        cfg.blockDim = dim3(kThreads2);
+        cfg.dynamicSmemBytes = P.smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // overlap K1's tail
+        attr[0].val.programmaticStreamSerializationAllowed = getenv("OZAKI_NO_PDL") ? 0 : 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, k_gemm_lv2<EPI, CHUNK, FULL>, P2));
     }
     CUDA_TRY(cudaGetLastError());
     g_stats.launches += 1;

@@ -236,6 +236,9 @@ struct SplitPair {
 
 template <int SMAX, bool CPLX, bool CRT = false>
 __global__ void __launch_bounds__(256) k_split_sm(const __grid_constant__ SplitPair pp, int KW) {
+    // let the dependent GEMM (launched with programmatic stream serialisation) start its
+    // prologue as soon as every split CTA is resident; it waits for our completion itself
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const SplitParams &p = pp.side[blockIdx.z];
     if ((int64_t)blockIdx.x * 8 >= p.rows_grid) return;   // the other side needs more row groups
     const bool RCONTIG = (p.rs == 1);                     // 8 rows adjacent in memory for each l
