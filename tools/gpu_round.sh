@@ -11,7 +11,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --steps 2 --warmup 3 --no-extras ${BENCH_ARGS} > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 3 -c 1 -f -o gpurun_out/prof_gemm_$TAG \
     python bench.py --steps 1 --warmup 3 --no-extras ${BENCH_ARGS} > gpurun_out/ncu_gemm_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_split -s 6 -c 2 -f -o gpurun_out/prof_split_$TAG \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_split -s 3 -c 1 -f -o gpurun_out/prof_split_$TAG \
     python bench.py --steps 1 --warmup 3 --no-extras ${BENCH_ARGS} > gpurun_out/ncu_slice_$TAG.log 2>&1
 fi
 ls -la gpurun_out
