@@ -377,7 +377,7 @@ def debug_split(side, kind, trans, X, num_slices, stream=None):
 
 TIMER_NAMES = ("prod_wait_empty", "mma_wait_full", "mma_wait_slot", "mma_total", "epi_wait_pass",
                "epi_drain", "epi_store", "cta_total", "mma_wait_slot_pass0", "epi_prefix",
-               "epi_first_arrive")
+               "epi_first_arrive", "mma_wait_full_first_kb", "mma_wait_full_pass0")
 
 
 def debug_timing(enable: bool = True, read: bool = False) -> dict | None:

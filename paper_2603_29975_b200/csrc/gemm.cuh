@@ -75,6 +75,8 @@ enum DbgSlot : int {
     DBG_MMA_WAIT_SLOT0,  // part of DBG_MMA_WAIT_SLOT spent before the first pass of a tile
     DBG_EPI_PREFIX,      // part of DBG_EPI_DRAIN spent in the exact-prefix levels (warp 2)
     DBG_EPI_FIRST_ARRIVE,// pass_full -> first slot released, first pass (warp 2)
+    DBG_MMA_WAIT_FULL0,  // part of DBG_MMA_WAIT_FULL at the first k-block of a pass
+    DBG_MMA_WAIT_FULLP0, // part of DBG_MMA_WAIT_FULL inside pass 0
     DBG_NSLOT
 };
 

@@ -58,7 +58,12 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
                 const bool kfirst = (kb0 == p.kb_begin);
                 long long w0 = p.dbg ? clock64() : 0;
                 mbar_wait(&full[stage], phase);
-                if (p.dbg && (threadIdx.x & 31) == 0) dbg_add(p, DBG_MMA_WAIT_FULL, clock64() - w0);
+                if (p.dbg && (threadIdx.x & 31) == 0) {
+                    const long long dw = clock64() - w0;
+                    dbg_add(p, DBG_MMA_WAIT_FULL, dw);
+                    if (kfirst) dbg_add(p, DBG_MMA_WAIT_FULL0, dw);
+                    if (ps == 0) dbg_add(p, DBG_MMA_WAIT_FULLP0, dw);
+                }
                 tc_fence_after();
                 const uint32_t sbase = smem_u32(smem + (size_t)stage * lp.stage_bytes);
                 for (int kk = 0; kk < nk; ++kk) {
