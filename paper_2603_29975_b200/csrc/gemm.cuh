@@ -22,6 +22,8 @@
 //   * Persistent: grid = min(#tiles, #SMs); tiles (batch, m, n) are walked with
 //     a grouped raster so concurrently running CTAs share operand tiles in L2.
 #pragma once
+// EPI_LEVELS (debug) instantiations `continue` before the FP64 epilogue of the same loop body
+#pragma nv_diag_suppress 128
 #include <cstdint>
 
 #include "numerics.cuh"

@@ -243,8 +243,6 @@ __global__ void __launch_bounds__(256) k_split_sm(const __grid_constant__ SplitP
     if ((int64_t)blockIdx.x * 8 >= p.rows_grid) return;   // the other side needs more row groups
     const bool RCONTIG = (p.rs == 1);                     // 8 rows adjacent in memory for each l
     extern __shared__ __align__(16) uint8_t sbuf[];
-    __shared__ uint64_t s_max[8][33];
-    __shared__ uint32_t s_nf[8][33];
     __shared__ int32_t s_e[8];
     __shared__ double s_scale[8];
     __shared__ int32_t s_e3[3][8];         // SPLIT_3M: per-operand exponents / scales
