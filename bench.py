@@ -68,6 +68,22 @@ CONFIGS = {
 }
 
 
+def _rank_device(torch, local):
+    """One process per GPU.  OZAKI_DIST_BACKEND=gloo lets several ranks share one device (a test
+    hook for the multi-rank path on a 1-GPU box); with NCCL every rank owns its own GPU."""
+    idx = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(idx)
+    return torch.device("cuda", idx)
+
+
+def _init_dist(dist, device):
+    backend = os.environ.get("OZAKI_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=device)
+    else:
+        dist.init_process_group(backend)
+
+
 def run_config(args):
     """Secondary workloads: one timed step = the whole GEMM (or this rank's shard of it)."""
     import torch
@@ -79,10 +95,9 @@ def run_config(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    device = torch.device("cuda", local)
+    device = _rank_device(torch, local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        _init_dist(dist, device)
     s = args.slices
     m, n, k, kind = cfg["m"], cfg["n"], cfg["k"], cfg["kind"]
     batch = args.batch if (cfg["shard"] == "batch" and args.batch != 30) else cfg["batch"]
@@ -302,10 +317,9 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    device = torch.device("cuda", local)
+    device = _rank_device(torch, local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        _init_dist(dist, device)
 
     n, batch, s = args.n, args.batch, args.slices
     fn = oz.zgemm_strided_batched if args.method == "4m" else oz.zgemm3m_strided_batched
