@@ -34,7 +34,6 @@ import synth  # noqa: E402
 BURST_FALLBACK_BF16 = 1590.0    # B200_PROFILING.md fallback (TFLOP/s) if MEASURED_PEAKS.json absent
 INT8_OVER_BF16 = 4.5 / 2.25     # nominal dense ratio (B200_PROFILING.md / datasheet)
 
-
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -52,7 +51,6 @@ def parse():
                     help="c2x30 (default, the headline) or another BASELINE config (see CONFIGS)")
     return ap.parse_args()
 
-
 # The other BASELINE.json configs (parity cases / secondary measurements).
 CONFIGS = {
     "c1": dict(kind="d", m=64, n=64, k=64, batch=1, fam="uniform", shard="replica",
@@ -67,7 +65,6 @@ CONFIGS = {
                desc="configs[4]: DGEMM 32768x32768x4096 spread(phi=4), column slabs + all-gather of C"),
 }
 
-
 def _rank_device(torch, local):
     """One process per GPU.  OZAKI_DIST_BACKEND=gloo lets several ranks share one device (a test
     hook for the multi-rank path on a 1-GPU box); with NCCL every rank owns its own GPU."""
@@ -75,14 +72,12 @@ def _rank_device(torch, local):
     torch.cuda.set_device(idx)
     return torch.device("cuda", idx)
 
-
 def _init_dist(dist, device):
     backend = os.environ.get("OZAKI_DIST_BACKEND", "nccl")
     if backend == "nccl":
         dist.init_process_group("nccl", device_id=device)
     else:
         dist.init_process_group(backend)
-
 
 def run_config(args):
     """Secondary workloads: one timed step = the whole GEMM (or this rank's shard of it)."""
@@ -201,7 +196,6 @@ def run_config(args):
     if world > 1:
         dist.destroy_process_group()
 
-
 def traffic_from_profile(s, method, n, batch, gamma):
     """DRAM bytes/launch of the GEMM from the committed ncu capture (profiles/gemm_traffic.json),
     only for the default workload it was captured on; else None."""
@@ -213,7 +207,6 @@ def traffic_from_profile(s, method, n, batch, gamma):
     except Exception:  # noqa: BLE001
         return None
 
-
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -222,7 +215,6 @@ def peaks():
         return float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
     except Exception:  # noqa: BLE001
         return BURST_FALLBACK_BF16, 1400.0, "fallback"
-
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
@@ -281,7 +273,6 @@ class ClockSampler:
         return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
                 "reasons": names, "samples": len(self.samples), "source": "nvml 5 ms"}
 
-
 # ------------------------------------------------------------ workload
 def make_inputs(batch, n, gamma, seed0):
     """Batch of KKR-like complex blocks (column-major per entry), numpy."""
@@ -292,21 +283,17 @@ def make_inputs(batch, n, gamma, seed0):
         B[i] = synth.kkr(n, n, seed=seed0 + 2 * i + 1, gamma=gamma)
     return A, B
 
-
 def to_dev_batched(torch, X, device):
     # (batch, n, n) numpy with Fortran entries -> column-major per entry on device
     t = torch.from_numpy(np.ascontiguousarray(np.transpose(X, (0, 2, 1))))  # row-major of X^T
     return t.to(device).transpose(1, 2)
 
-
 def fp64_equiv_flops(batch, n, cplx=True):
     return batch * (8 if cplx else 2) * n ** 3
-
 
 def int8_ops(batch, n, s, method):
     mult = 4 if method == "4m" else 3
     return 2 * mult * (s * (s + 1) // 2) * n ** 3 * batch
-
 
 # ------------------------------------------------------------------ main
 def run_ours(args):
@@ -442,18 +429,18 @@ def run_ours(args):
     if not args.no_extras:
         C0 = C[0].cpu().numpy()          # entry 0 of the timed result, checked in the cpu_baseline leg
         out["e2e"] = e2e_leg(torch, oz, fn, A_h, B_h, batch, n, s, device, args, world)
-        out["sweep"] = sweep_leg(torch, oz, A, B, C, batch, n)
-        out["ozaki2"], C0_oz2 = ozaki2_leg(torch, oz, A, B, C, batch, n)
+        out["sweep"], sweep_samples = sweep_leg(torch, oz, A, B, C, batch, n)
+        out["ozaki2"], C0_oz2, oz2_samples = ozaki2_leg(torch, oz, A, B, C, batch, n)
         out["native_fp64"] = native_leg(torch, A, B, batch, n)
     if rank == 0 and not args.no_extras and not args.no_cpu:
         # the ONLY use of oracle/ in the GPU arm: the host-core baseline and the parity samples
         out["cpu_baseline"], out["accuracy"], out["ozaki2"]["bitexact_vs_oracle_N16_sample"] = \
             cpu_baseline_leg(A_h, B_h, C0, C0_oz2, s, args.method, n)
+        out["error_vs_true_fp64"] = error_table(A_h, B_h, n, {**sweep_samples, **oz2_samples})
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
-
 
 def e2e_leg(torch, oz, fn, A_h, B_h, batch, n, s, device, args, world):
     """End to end through the public API with HOST (pinned) buffers: the library's
@@ -490,7 +477,6 @@ def e2e_leg(torch, oz, fn, A_h, B_h, batch, n, s, device, args, world):
             "path": "ozaki_zgemm_strided_batched on pinned HOST tensors (library offload: chunked, "
                     "H2D / GEMM / D2H overlapped on 3 streams)"}
 
-
 def accuracy_leg(A_h, B_h, C0, s, method):
     """Entry 0: parity vs the oracle and error vs the TRUE product on a sample (called from the
     cpu_baseline leg, the only place bench.py uses oracle/)."""
@@ -511,7 +497,6 @@ def accuracy_leg(A_h, B_h, C0, s, method):
             "max_rel_err_vs_true_fp64": float(np.max(np.abs(got - truth)[nz] / np.abs(truth[nz]))),
             "max_err_over_absAB": float(np.max(np.abs(got - truth) / absab))}
 
-
 def ozaki2_parity(A_h, B_h, C0_oz2, n, nmod=16):
     """Entry 0 of the Ozaki-II N=16 run vs oracle/ozaki2.py on a sample (cpu_baseline leg)."""
     from oracle import ozaki2 as o2
@@ -523,6 +508,22 @@ def ozaki2_parity(A_h, B_h, C0_oz2, n, nmod=16):
     want = o2.zgemm("N", "N", 1.0, A0[rows], B0[:, cols], 0.0, None, nmod)
     return bool((got.real == want.real).all() and (got.imag == want.imag).all())
 
+def error_table(A_h, B_h, n, samples):
+    """North star: "max relative error against true FP64 per slice count" (SURVEY c-13, both
+    definitions) for every swept mode, on the entry-0 sample; truth = oracle's exact product."""
+    import oracle
+    rows, cols = err_sample_idx(n)
+    A0 = np.asfortranarray(A_h[0])
+    B0 = np.asfortranarray(B_h[0])
+    truth = oracle.exact_zproduct(A0[rows], B0[:, cols])
+    absab = np.abs(A0[rows]) @ np.abs(B0[:, cols])
+    nz = truth != 0
+    out = {"sample": f"entry 0, {len(rows)}x{len(cols)} entries incl. tile edges",
+           "definitions": "rel = max |C-T|/|T| over T != 0; comp = max |C-T| / (|A||B|)"}
+    for key, got in samples.items():
+        out[key] = {"rel": float(np.max(np.abs(got - truth)[nz] / np.abs(truth[nz]))),
+                    "comp": float(np.max(np.abs(got - truth) / absab))}
+    return out
 
 def cpu_baseline_leg(A_h, B_h, C0, C0_oz2, s, method, n):
     base = cpu_baseline(A_h, B_h, s, method, n)
@@ -530,10 +531,18 @@ def cpu_baseline_leg(A_h, B_h, C0, C0_oz2, s, method, n):
     oz2 = ozaki2_parity(A_h, B_h, C0_oz2, n) if C0_oz2 is not None else "not run"
     return base, acc, oz2
 
+def err_sample_idx(n):
+    rows = np.unique(np.r_[0, 1, 127, 128, 255, n - 1, np.arange(3, n, 29)])
+    cols = np.unique(np.r_[0, 63, 64, 127, n - 1, np.arange(5, n, 31)])
+    return rows, cols
 
 def sweep_leg(torch, oz, A, B, C, batch, n):
-    """FP64-eq TFLOP/s vs s for 4M and 3M on the same inputs (short timing)."""
+    """FP64-eq TFLOP/s vs s for 4M and 3M on the same inputs (short timing).  Returns (table,
+    entry-0 samples per (method, s)) -- the samples' error vs the TRUE product is computed in the
+    cpu_baseline leg (the only place bench.py touches oracle/)."""
     res = {}
+    samples = {}
+    rows, cols = err_sample_idx(n)
     for method, fn in (("4m", oz.zgemm_strided_batched), ("3m", oz.zgemm3m_strided_batched)):
         for s in (3, 4, 5, 6, 7, 8, 9):
             for _ in range(2):
@@ -549,8 +558,8 @@ def sweep_leg(torch, oz, A, B, C, batch, n):
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / reps
             res[f"{method}_s{s}"] = round(fp64_equiv_flops(batch, n) / (ms * 1e-3) / 1e12, 2)
-    return res
-
+            samples[f"{method}_s{s}"] = C[0].cpu().numpy()[np.ix_(rows, cols)]
+    return res, samples
 
 def split_roofline(split_ms, batch, n, s, method):
     """K1 (split) vs HBM: algorithmic bytes per step = FP64 inputs read once + the INT8 slices of
@@ -569,12 +578,12 @@ def split_roofline(split_ms, batch, n, s, method):
             "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(gbs / hbm, 4),
             "algorithmic_bytes_per_step": int(read + write), "peak_source": src}
 
-
 def ozaki2_leg(torch, oz, A, B, C, batch, n):
     """NEXT-1: Ozaki-II (CRT) on the same inputs, FP64-eq TFLOP/s, phase split and the residue
     GEMM's INT8 TOPS per moduli count.  Returns (record, entry-0 result at N=16 for the parity
     sample checked in the cpu_baseline leg)."""
     res = {}
+    oz2_samples = {}
     for nmod in (10, 12, 14, 16, 18):
         for _ in range(2):
             oz.ozaki2_zgemm_strided_batched("N", "N", 1.0, A, B, 0.0, C, nmod)
@@ -594,6 +603,7 @@ def ozaki2_leg(torch, oz, A, B, C, batch, n):
         ms = e0.elapsed_time(e1) / reps
         gemm_ms = pr["k2_gemm"]["ms"] / reps
         ops = 2 * nmod * n * (2 * n) * (2 * n) * batch     # one m x 2k x 2n INT8 GEMM per modulus (4M)
+        oz2_samples[f"ozaki2_N{nmod}"] = C[0].cpu().numpy()[np.ix_(*err_sample_idx(n))]
         res[f"N{nmod}"] = {"tflops": round(fp64_equiv_flops(batch, n) / (ms * 1e-3) / 1e12, 2),
                            "ms": round(ms, 4),
                            "phase_ms": {"split": round(pr["k1_slice"]["ms"] / reps, 4),
@@ -604,8 +614,7 @@ def ozaki2_leg(torch, oz, A, B, C, batch, n):
            "path": "ozaki2_zgemm_strided_batched (split -> k_gemm_crt -> k_crt)"}
     oz.ozaki2_zgemm_strided_batched("N", "N", 1.0, A, B, 0.0, C, 16)
     torch.cuda.synchronize()
-    return out, C[0].cpu().numpy()
-
+    return out, C[0].cpu().numpy(), oz2_samples
 
 def native_leg(torch, A, B, batch, n):
     """Context only (PAPER.md:119 'native FP64 GEMM'): cuBLAS complex128 batched matmul on the same
@@ -624,7 +633,6 @@ def native_leg(torch, A, B, batch, n):
     ms = e0.elapsed_time(e1) / reps
     return {"value": round(fp64_equiv_flops(batch, n) / (ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
             "path": "torch.bmm complex128 (cuBLAS native FP64), context only"}
-
 
 def cpu_baseline(A_h, B_h, s, method, n, budget_s=10.0):
     """The oracle on the host cores: whole n^3 ZGEMM entries of the same batch,
@@ -646,7 +654,6 @@ def cpu_baseline(A_h, B_h, s, method, n, budget_s=10.0):
             "sample": f"{done} full {n}^3 ZGEMM entries of the batch ({method}, s={s}), exact-integer oracle, "
                       f"time-bounded ~{budget_s:.0f} s",
             "seconds": round(dt, 3)}
-
 
 def run_reference(args):
     """Reference arm of this tier: the CPU oracle, as it stands, on host cores."""
@@ -687,7 +694,6 @@ def run_reference(args):
     }
     print(json.dumps(line), flush=True)
 
-
 def main():
     args = parse()
     if args.impl == "reference":
@@ -696,7 +702,6 @@ def main():
         run_config(args)
     else:
         run_ours(args)
-
 
 if __name__ == "__main__":
     main()
