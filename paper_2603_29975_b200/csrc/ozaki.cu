@@ -27,6 +27,7 @@
 #include "gemm_lv2.cuh"
 #include "ozaki.h"
 #include "split.cuh"
+#include "split_fast.cuh"
 
 using namespace ozk;
 
@@ -430,6 +431,59 @@ SplitParams split_params(const Plan &P, const Operand &op, bool sideA, int8_t *s
     return sp;
 }
 
+// K1 specialised for the production layout (k_split_fast, split_fast.cuh): both operands in one
+// launch, CTA-pair tiles (A 128 rows, B 64 rows), s <= 8, Ozaki-I digit layout.  Returns 1 when
+// the call does not qualify (the generic k_split_sm runs), else 0 / an error code.
+// OZAKI_SPLIT=generic forces the generic kernel (A/B tests).
+int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b, dim3 grid, cudaStream_t st) {
+    if (!b || !P.pair || P.s < 1 || P.s > 8) return 1;
+    if (a.tile_h != 128 || b->tile_h != 64) return 1;
+    if (a.kbs_bytes != (int64_t)P.s * 128 * 32 || b->kbs_bytes != (int64_t)P.s * 64 * 32) return 1;
+    const bool real = a.mode == SPLIT_REAL && b->mode == SPLIT_REAL;
+    const bool fourm = a.mode == SPLIT_A4M && b->mode == SPLIT_B4M;
+    const bool threem = a.mode == SPLIT_3M && b->mode == SPLIT_3M;
+    if (!real && !fourm && !threem) return 1;
+    if (const char *e = getenv("OZAKI_SPLIT"))
+        if (!strcmp(e, "generic")) return 1;
+    int KW = real ? 1024 : 512;
+    if (const char *kw = getenv("OZAKI_SPLIT_KW")) {   // tuning hook: window elements per row
+        const int v = atoi(kw);
+        if (v >= 64 && v <= 1024 && v % 32 == 0) KW = real ? v : std::min(v, 512);
+    }
+    SplitPair pp;
+    pp.side[0] = a;
+    pp.side[1] = *b;
+    const size_t smem = (size_t)8 * (KW + (real ? 2 : 1)) * (real ? 8 : 16);
+    {
+        ProfScope ps(st, PH_SLICE);
+#define OZK_FAST(S, MA, MB)                                                                          \
+        {                                                                                            \
+            static size_t attr = 0;                                                                  \
+            if (attr < smem) {                                                                       \
+                cudaFuncSetAttribute(k_split_fast<S, MA, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     (int)smem);                                                     \
+                attr = smem;                                                                         \
+            }                                                                                        \
+            k_split_fast<S, MA, MB><<<grid, 256, smem, st>>>(pp, KW);                                \
+        }
+#define OZK_FAST_S(S)                                                                                \
+        case S:                                                                                      \
+            if (real) OZK_FAST(S, SPLIT_REAL, SPLIT_REAL)                                            \
+            else if (fourm) OZK_FAST(S, SPLIT_A4M, SPLIT_B4M)                                        \
+            else OZK_FAST(S, SPLIT_3M, SPLIT_3M)                                                     \
+            break;
+        switch (P.s) {
+            OZK_FAST_S(1) OZK_FAST_S(2) OZK_FAST_S(3) OZK_FAST_S(4)
+            OZK_FAST_S(5) OZK_FAST_S(6) OZK_FAST_S(7) OZK_FAST_S(8)
+        }
+#undef OZK_FAST_S
+#undef OZK_FAST
+    }
+    CUDA_TRY(cudaGetLastError());
+    g_stats.launches += 1;
+    return 0;
+}
+
 // K1 for one (b == nullptr) or both operands in one launch.
 int launch_split_sides(const Plan &P, const SplitParams &a, const SplitParams *b, int64_t gb, cudaStream_t st) {
     SplitPair pp;
@@ -439,6 +493,7 @@ int launch_split_sides(const Plan &P, const SplitParams &a, const SplitParams *b
     if (rows_grid == 0) return 0;
     const bool cplx = a.mode != SPLIT_REAL;
     dim3 grid((unsigned)((rows_grid + 7) / 8), (unsigned)gb, b ? 2u : 1u);
+    if (int rc = launch_split_fast(P, a, b, grid, st); rc <= 0) return rc;   // production layout
     // SMEM window: 8 rows x KW elements (+ pad), 64 KB
     int KW = cplx ? 512 : 1024;
     if (const char *kw = getenv("OZAKI_SPLIT_KW")) {   // tuning hook: window elements per row

@@ -1,0 +1,378 @@
+// split_fast.cuh -- K1 for the production Ozaki-I path (CTA-pair GEMM layout, s <= 8).
+//
+// Same method and output as k_split_sm (split.cuh): §2.2 ("splits
+// high-precision input matrices into slices ... based on their significant bits
+// and exponent alignment"), readings R3 (exponent), R4 (X = RNE(x 2^(8s-1-e)),
+// balanced base-256 digits), R9 (4M embedding, 3M operands) in DESIGN.md §3.
+// The difference is specialisation: the slice count S, the operand mode of each
+// side and the tile height (hence every output offset) are compile-time, so one
+// item (8 values of one row) costs ~8 LDS + 8 DMUL + 8 F2I + 4 int ops / value +
+// the PRMT transposes + S immediate-offset stores per target, and each thread
+// keeps one row for the whole CTA (one base pointer, constant strides).
+//
+// Exponent scan (pass 1): the max of |x| is taken over the IEEE high words only
+// (32-bit IMNMX).  R3 needs the full 64-bit max M only when the high word cannot
+// decide it: M subnormal / zero (leading bit may sit in the low word) or the
+// 127-rule tie (fraction's top 20 bits exactly 0b111111 followed by 14 zeros,
+// where "f > 63/64" depends on the low word).  Those rows (warp-uniform) rescan
+// with the exact 64-bit max -- so the exponent is bit-identical to k_split_sm.
+#pragma once
+#include <cstdint>
+
+#include "numerics.cuh"
+#include "split.cuh"
+
+namespace ozk {
+
+// R3 from the max high word H = max (hi(x) & 0x7fffffff) of a row (finite: H < 0x7ff00000).
+// Returns false when the low words are needed (see header).
+__device__ __forceinline__ bool exponent_from_hi(uint32_t H, int32_t &e) {
+    const uint32_t ex = H >> 20, f = H & 0xfffffu;
+    if (ex == 0 || f == (63u << 14)) return false;
+    e = (int32_t)ex - 1022 + (f > (63u << 14) ? 1 : 0);
+    return true;
+}
+
+__device__ __forceinline__ uint32_t hi_abs(double x) {
+    return (uint32_t)__double2hiint(x) & 0x7fffffffu;
+}
+
+__device__ __forceinline__ void st_global_v2(int8_t *p, uint32_t a, uint32_t b) {
+    asm volatile("st.global.v2.b32 [%0], {%1, %2};" ::"l"(p), "r"(a), "r"(b) : "memory");
+}
+
+template <int S>
+struct FastDigits {
+    static constexpr int NW = (S + 3) / 4;   // 32-bit words of Y holding the S digit bytes
+    static constexpr unsigned long long B = 0x0080808080808080ull >> (8 * (8 - S));
+
+    // R4 for 8 values: X = RNE(v * 2^(P-e)) (scale = +-2^(P-e) when that power is a normal
+    // double: one exact-or-correctly-rounded DMUL; else ldexp_rn on sgn*v), Y = (X + B) ^ B
+    // (byte q = balanced digit of slice S - q).  NEG also forms the digits of -X.
+    template <bool NEG>
+    __device__ __forceinline__ static void words(const double (&v)[8], double scale, double sgn, int sh,
+                                                 uint32_t (&w)[NW][8], uint32_t (&wn)[NW][8]) {
+        long long X[8];
+        if (scale != 0.0) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) X[i] = __double2ll_rn(__dmul_rn(v[i], scale));
+        } else {   // 2^(P-e) is not a normal double (extreme exponents): exact ldexp
+#pragma unroll
+            for (int i = 0; i < 8; ++i) X[i] = __double2ll_rn(ldexp_rn(sgn * v[i], sh));
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const unsigned long long Y = ((unsigned long long)X[i] + B) ^ B;
+            w[0][i] = (uint32_t)Y;
+            if constexpr (NW > 1) w[1][i] = (uint32_t)(Y >> 32);
+            if constexpr (NEG) {
+                const unsigned long long Yn = (B - (unsigned long long)X[i]) ^ B;
+                wn[0][i] = (uint32_t)Yn;
+                if constexpr (NW > 1) wn[1][i] = (uint32_t)(Yn >> 32);
+            }
+        }
+    }
+
+    // 8x8 byte transpose of the words and one 8-byte store per slice; slice t = S - q of
+    // byte q goes to block (t - 1) = S - 1 - q of the (tile, k-block) group, BLK bytes apart.
+    template <int BLK>
+    __device__ __forceinline__ static void store(const uint32_t (&w)[NW][8], int8_t *p) {
+#pragma unroll
+        for (int j = 0; j < NW; ++j) {
+            uint32_t lo[4], hi[4];
+            transpose4x4(w[j][0], w[j][1], w[j][2], w[j][3], lo[0], lo[1], lo[2], lo[3]);
+            transpose4x4(w[j][4], w[j][5], w[j][6], w[j][7], hi[0], hi[1], hi[2], hi[3]);
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                const int q = 4 * j + qq;
+                if (q < S) st_global_v2(p + (S - 1 - q) * BLK, lo[qq], hi[qq]);
+            }
+        }
+    }
+};
+
+// Exact 64-bit max |x| of row r over the valid depth, straight from global memory (rare path).
+template <bool CPLX>
+__device__ uint64_t row_max_bits_slow(const SplitParams &p, const void *Xb, int64_t r, int comp, int lane) {
+    uint64_t m = 0;
+    for (int64_t l = lane; l < p.k; l += 32) {
+        const int64_t off = r * p.rs + l * p.ls;
+        uint64_t u;
+        if constexpr (!CPLX) {
+            u = (uint64_t)__double_as_longlong(reinterpret_cast<const double *>(Xb)[off]) & kAbsMask;
+        } else {
+            const double2 x = reinterpret_cast<const double2 *>(Xb)[off];
+            const double im = p.conj ? -x.y : x.y;
+            const uint64_t ur = (uint64_t)__double_as_longlong(x.x) & kAbsMask;
+            const uint64_t ui = (uint64_t)__double_as_longlong(im) & kAbsMask;
+            if (comp == 0) u = ur;
+            else if (comp == 1) u = ui;
+            else if (comp == 2) u = (uint64_t)__double_as_longlong(__dadd_rn(x.x, im)) & kAbsMask;
+            else u = ur > ui ? ur : ui;
+        }
+        m = u > m ? u : m;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t om = __shfl_xor_sync(0xffffffffu, m, o);
+        m = om > m ? om : m;
+    }
+    return m;
+}
+
+__device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
+    return __reduce_max_sync(0xffffffffu, v);
+}
+
+// One side of the split: 8 input rows r0..r0+7 of batch entry b; MODE and the output tile
+// height TH are compile-time.  256 threads.
+template <int S, int MODE, int TH>
+__device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, uint8_t *sbuf) {
+    constexpr bool CPLX = (MODE != SPLIT_REAL);
+    constexpr int NX = (MODE == SPLIT_3M) ? 3 : 1;   // operands (exponents) per row
+    constexpr int BLK = TH * 32;                      // bytes of one (tile, k-block, slice) block
+    constexpr int KBS = S * BLK;                      // bytes between k-blocks of one tile
+    constexpr int P = 8 * S - 1;
+    using D = FastDigits<S>;
+    using Elem = typename std::conditional<CPLX, double2, double>::type;
+
+    __shared__ int32_t s_e[3][8];
+    __shared__ double s_scale[3][8];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t b = blockIdx.y;
+    const int64_t r0 = (int64_t)blockIdx.x * 8;
+    const bool RCONTIG = (p.rs == 1);
+    const int ld = KW + (16 / (int)sizeof(Elem));     // padded row stride (elements)
+    Elem *slab = reinterpret_cast<Elem *>(sbuf);
+    const Elem *X = reinterpret_cast<const Elem *>(p.X) + b * p.bstride;
+    constexpr bool FOURM = (MODE == SPLIT_A4M || MODE == SPLIT_B4M);
+    const int64_t kpad = FOURM ? p.kh : p.KB * 32;
+    const int64_t nwin = (kpad + KW - 1) / KW;
+    const int nrows = (int)min((int64_t)8, max((int64_t)0, p.rows - r0));
+
+    auto load_window = [&](int64_t w0) {
+        const int wlen = (int)min((int64_t)KW, p.k - w0);
+        if (wlen > 0) {
+            if (RCONTIG) {   // the 8 rows are adjacent for each l: thread keeps row tid & 7
+                const int row = tid & 7;
+                if (row < nrows) {
+                    const int64_t gstep = 32 * p.ls;
+                    const Elem *g = X + r0 + row + (w0 + (tid >> 3)) * p.ls;
+                    Elem *d = slab + row * ld + (tid >> 3);
+#pragma unroll 4
+                    for (int l = tid >> 3; l < wlen; l += 32) {
+                        if (CPLX) cp_async16(d, g);
+                        else cp_async8(d, g);
+                        g += gstep;
+                        d += 32;
+                    }
+                }
+            } else {         // row contiguous along l: one warp per row, 32 consecutive elements
+                if (warp < nrows) {
+                    const Elem *g = X + (r0 + warp) * p.rs + w0;
+                    Elem *d = slab + warp * ld;
+#pragma unroll 4
+                    for (int l = lane; l < wlen; l += 32) {
+                        if (CPLX) cp_async16(d + l, g + l);
+                        else cp_async8(d + l, g + l);
+                    }
+                }
+            }
+        }
+        cp_async_wait_all();
+    };
+
+    // ---------------- pass 1: exponents (warp = row)
+    uint32_t hm[NX];
+#pragma unroll
+    for (int x = 0; x < NX; ++x) hm[x] = 0;
+    for (int64_t w = 0; w < nwin; ++w) {
+        const int64_t w0 = w * KW;
+        if (w > 0) __syncthreads();
+        load_window(w0);
+        __syncthreads();
+        const int wlen = (int)min((int64_t)KW, p.k - w0);
+        if (warp < nrows) {
+            const Elem *src = slab + warp * ld;
+#pragma unroll 4
+            for (int l = lane; l < wlen; l += 32) {
+                const Elem v = src[l];
+                if constexpr (!CPLX) {
+                    hm[0] = max(hm[0], hi_abs(v));
+                } else if constexpr (MODE == SPLIT_3M) {
+                    const double im = p.conj ? -v.y : v.y;
+                    hm[0] = max(hm[0], hi_abs(v.x));
+                    hm[1] = max(hm[1], hi_abs(v.y));
+                    hm[2] = max(hm[2], hi_abs(__dadd_rn(v.x, im)));
+                } else {
+                    hm[0] = max(hm[0], max(hi_abs(v.x), hi_abs(v.y)));
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int x = 0; x < NX; ++x) {
+        const uint32_t H = warp_max_u32(hm[x]);
+        int32_t e = 0;
+        bool nf = false;
+        if (warp < nrows) {
+            if (H >= 0x7ff00000u) {          // an Inf / NaN in the row (R10)
+                nf = true;
+                e = kNonFinite;
+            } else if (!exponent_from_hi(H, e)) {
+                const int comp = (MODE == SPLIT_3M) ? x : (CPLX ? 3 : 0);
+                e = exponent_from_maxbits(row_max_bits_slow<CPLX>(p, X, r0 + warp, comp, lane));
+            }
+        }
+        if (lane == 0) {
+            if (warp < nrows) {
+                int32_t *ex = p.exps + (MODE == SPLIT_3M ? x * p.x_exps : 0) + b * p.rows_out;
+                if (MODE == SPLIT_B4M) {
+                    ex[2 * (r0 + warp)] = e;
+                    ex[2 * (r0 + warp) + 1] = e;
+                } else {
+                    ex[r0 + warp] = e;
+                }
+                if (nf) atomicAdd(p.nonfinite, 1ull);
+            }
+            s_e[x][warp] = e;
+            const int sh = P - e;
+            s_scale[x][warp] = (sh >= -1022 && sh <= 1023) ? pow2(sh) : 0.0;
+        }
+    }
+    __syncthreads();
+
+    // ---------------- pass 2: digits; thread = (row, 8-value units h = h0 + 32 j)
+    const int row = tid & 7, h0 = tid >> 3;
+    const int64_t R = (MODE == SPLIT_B4M) ? 2 * (r0 + row) : r0 + row;   // first output row
+    const int64_t tile = R / TH, rr = R % TH;
+    const int64_t tile_bytes = (int64_t)KBS * p.KB;
+    int8_t *obase = p.out + (b * p.tiles + tile) * tile_bytes + (rr >> 3) * 256 + (rr & 7) * 16 +
+                    ((h0 >> 1) & 1) * 128 + (h0 & 1) * 8;
+    const int64_t half_off = (p.kh >> 5) * KBS;        // 4M: the second K half (Im / Re block)
+    int32_t ex[NX];
+    double sc[NX], sg[NX];
+    bool live[NX];
+#pragma unroll
+    for (int x = 0; x < NX; ++x) {
+        ex[x] = s_e[x][row];
+        live[x] = (row < nrows) && (ex[x] != kNonFinite);
+        // R9 conj for 3M's Im operand: RNE is sign-symmetric, so digits of -v = digits with -scale
+        sg[x] = (MODE == SPLIT_3M && x == 1 && p.conj) ? -1.0 : 1.0;
+        sc[x] = s_scale[x][row] * sg[x];
+    }
+    const bool anylive = live[0];
+
+    for (int64_t w = 0; w < nwin; ++w) {
+        const int64_t w0 = w * KW;
+        if (nwin > 1) {
+            __syncthreads();
+            load_window(w0);
+            __syncthreads();
+        }
+        const int wh = (int)((min((int64_t)KW, kpad - w0) + 7) / 8);   // 8-value units in window
+        int8_t *op = obase + ((w0 >> 5) + (h0 >> 2)) * (int64_t)KBS;
+        for (int h = h0; h < wh; h += 32, op += 8 * (int64_t)KBS) {
+            const int64_t l0 = w0 + 8 * h;
+            const int nvalid = (int)min((int64_t)8, max((int64_t)0, p.k - l0));
+            const Elem *src = slab + row * ld + 8 * h;
+            if constexpr (!CPLX) {
+                double v[8];
+                if (anylive && nvalid == 8) {
+                    const double2 *s2 = reinterpret_cast<const double2 *>(src);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const double2 t = s2[i];
+                        v[2 * i] = t.x;
+                        v[2 * i + 1] = t.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) v[i] = (anylive && i < nvalid) ? src[i] : 0.0;
+                }
+                uint32_t w_[D::NW][8], wn_[D::NW][8];
+                D::template words<false>(v, sc[0], sg[0], P - ex[0], w_, wn_);
+                D::template store<BLK>(w_, op);
+            } else {
+                double re[8], im[8];
+                if (anylive && nvalid == 8) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const double2 t = src[i];
+                        re[i] = t.x;
+                        im[i] = t.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const double2 t = (i < nvalid) ? src[i] : make_double2(0.0, 0.0);
+                        re[i] = t.x;
+                        im[i] = t.y;
+                    }
+                }
+                if constexpr (MODE == SPLIT_A4M) {   // row r = [Re | Im] (Im conjugated: -scale)
+                    if (!anylive) {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) re[i] = im[i] = 0.0;
+                    }
+                    const double sim = p.conj ? -sc[0] : sc[0];
+                    uint32_t w_[D::NW][8], wn_[D::NW][8];
+                    D::template words<false>(re, sc[0], 1.0, P - ex[0], w_, wn_);
+                    D::template store<BLK>(w_, op);
+                    D::template words<false>(im, sim, p.conj ? -1.0 : 1.0, P - ex[0], w_, wn_);
+                    D::template store<BLK>(w_, op + half_off);
+                } else if constexpr (MODE == SPLIT_B4M) {
+                    // R9 N side: output row 2r = [Re | -Im'], 2r+1 = [Im' | Re] with Im' = conj ? -Im : Im.
+                    // Rows 2r and 2r+1 share a tile; 2r+1 sits 16 B after 2r in the core matrix.
+                    if (!anylive) {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) re[i] = im[i] = 0.0;
+                    }
+                    uint32_t w_[D::NW][8], wn_[D::NW][8];
+                    D::template words<false>(re, sc[0], 1.0, P - ex[0], w_, wn_);
+                    D::template store<BLK>(w_, op);
+                    D::template store<BLK>(w_, op + half_off + 16);
+                    D::template words<true>(im, sc[0], 1.0, P - ex[0], w_, wn_);   // w_ = Im, wn_ = -Im
+                    if (!p.conj) {
+                        D::template store<BLK>(w_, op + 16);
+                        D::template store<BLK>(wn_, op + half_off);
+                    } else {
+                        D::template store<BLK>(wn_, op + 16);
+                        D::template store<BLK>(w_, op + half_off);
+                    }
+                } else {   // SPLIT_3M: regions x = 0 (Re), 1 (Im'), 2 (fl(Re + Im')), own exponents
+#pragma unroll
+                    for (int x = 0; x < 3; ++x) {
+                        double v[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const double imc = p.conj ? -im[i] : im[i];
+                            v[i] = live[x] ? (x == 0 ? re[i] : (x == 1 ? im[i] : __dadd_rn(re[i], imc))) : 0.0;
+                        }
+                        uint32_t w_[D::NW][8], wn_[D::NW][8];
+                        D::template words<false>(v, sc[x], sg[x], P - ex[x], w_, wn_);
+                        D::template store<BLK>(w_, op + x * p.x_bytes);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Both operands of one product in ONE launch (blockIdx.z = side), A rows in 128-row tiles,
+// B rows in 64-row halves (the CTA-pair GEMM's layout).
+template <int S, int MA, int MB>
+__global__ void __launch_bounds__(256) k_split_fast(const __grid_constant__ SplitPair pp, int KW) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    extern __shared__ __align__(16) uint8_t sbuf[];
+    if (blockIdx.z == 0) {
+        if ((int64_t)blockIdx.x * 8 >= pp.side[0].rows_grid) return;
+        split_fast_side<S, MA, 128>(pp.side[0], KW, sbuf);
+    } else {
+        if ((int64_t)blockIdx.x * 8 >= pp.side[1].rows_grid) return;
+        split_fast_side<S, MB, 64>(pp.side[1], KW, sbuf);
+    }
+}
+
+}  // namespace ozk
