@@ -450,22 +450,30 @@ int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b,
         const int v = atoi(kw);
         if (v >= 64 && v <= 1024 && v % 32 == 0) KW = real ? v : std::min(v, 512);
     }
+    // rows per CTA (one warp each): 4 by default -- twice the CTAs of 8, so more load / compute
+    // phases overlap per SM at the same SMEM per row; OZAKI_SPLIT_ROWS=8 for A/B tests
+    int RG = 4;
+    if (const char *rg = getenv("OZAKI_SPLIT_ROWS"))
+        if (atoi(rg) == 8) RG = 8;
+    grid.x = (unsigned)((std::max(a.rows_grid, b->rows_grid) + RG - 1) / RG);
     SplitPair pp;
     pp.side[0] = a;
     pp.side[1] = *b;
-    const size_t smem = (size_t)8 * (KW + (real ? 2 : 1)) * (real ? 8 : 16);
+    const size_t smem = (size_t)RG * (KW + (real ? 2 : 1)) * (real ? 8 : 16);
     {
         ProfScope ps(st, PH_SLICE);
-#define OZK_FAST(S, MA, MB)                                                                          \
+#define OZK_FAST_RG(S, MA, MB, R)                                                                    \
         {                                                                                            \
             static size_t attr = 0;                                                                  \
             if (attr < smem) {                                                                       \
-                cudaFuncSetAttribute(k_split_fast<S, MA, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                     (int)smem);                                                     \
+                cudaFuncSetAttribute(k_split_fast<S, MA, MB, R>,                                     \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
                 attr = smem;                                                                         \
             }                                                                                        \
-            k_split_fast<S, MA, MB><<<grid, 256, smem, st>>>(pp, KW);                                \
+            k_split_fast<S, MA, MB, R><<<grid, 32 * R, smem, st>>>(pp, KW);                          \
         }
+#define OZK_FAST(S, MA, MB)                                                                          \
+        if (RG == 4) OZK_FAST_RG(S, MA, MB, 4) else OZK_FAST_RG(S, MA, MB, 8)
 #define OZK_FAST_S(S)                                                                                \
         case S:                                                                                      \
             if (real) OZK_FAST(S, SPLIT_REAL, SPLIT_REAL)                                            \
@@ -478,6 +486,7 @@ int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b,
         }
 #undef OZK_FAST_S
 #undef OZK_FAST
+#undef OZK_FAST_RG
     }
     CUDA_TRY(cudaGetLastError());
     g_stats.launches += 1;

@@ -48,10 +48,12 @@ struct FastDigits {
 
     // R4 for 8 values: X = RNE(v * 2^(P-e)) (scale = +-2^(P-e) when that power is a normal
     // double: one exact-or-correctly-rounded DMUL; else ldexp_rn on sgn*v), Y = (X + B) ^ B
-    // (byte q = balanced digit of slice S - q).  NEG also forms the digits of -X.
+    // (byte q = balanced digit of slice S - q).  NEG also forms wn = the digits of X2, where
+    // X2 = -X if neg2 else X (a per-lane choice without register-array selects).
     template <bool NEG>
     __device__ __forceinline__ static void words(const double (&v)[8], double scale, double sgn, int sh,
-                                                 uint32_t (&w)[NW][8], uint32_t (&wn)[NW][8]) {
+                                                 uint32_t (&w)[NW][8], uint32_t (&wn)[NW][8],
+                                                 bool neg2 = true) {
         long long X[8];
         if (scale != 0.0) {
 #pragma unroll
@@ -66,7 +68,8 @@ struct FastDigits {
             w[0][i] = (uint32_t)Y;
             if constexpr (NW > 1) w[1][i] = (uint32_t)(Y >> 32);
             if constexpr (NEG) {
-                const unsigned long long Yn = (B - (unsigned long long)X[i]) ^ B;
+                const unsigned long long X2 = neg2 ? 0ull - (unsigned long long)X[i] : (unsigned long long)X[i];
+                const unsigned long long Yn = (X2 + B) ^ B;
                 wn[0][i] = (uint32_t)Yn;
                 if constexpr (NW > 1) wn[1][i] = (uint32_t)(Yn >> 32);
             }
@@ -124,9 +127,9 @@ __device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
     return __reduce_max_sync(0xffffffffu, v);
 }
 
-// One side of the split: 8 input rows r0..r0+7 of batch entry b; MODE and the output tile
-// height TH are compile-time.  256 threads.
-template <int S, int MODE, int TH>
+// One side of the split: RG input rows r0..r0+RG-1 of batch entry b (one warp per row in
+// pass 1, 32 * RG threads); MODE and the output tile height TH are compile-time.
+template <int S, int MODE, int TH, int RG>
 __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, uint8_t *sbuf) {
     constexpr bool CPLX = (MODE != SPLIT_REAL);
     constexpr int NX = (MODE == SPLIT_3M) ? 3 : 1;   // operands (exponents) per row
@@ -136,12 +139,12 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
     using D = FastDigits<S>;
     using Elem = typename std::conditional<CPLX, double2, double>::type;
 
-    __shared__ int32_t s_e[3][8];
-    __shared__ double s_scale[3][8];
+    __shared__ int32_t s_e[3][RG];
+    __shared__ double s_scale[3][RG];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t b = blockIdx.y;
-    const int64_t r0 = (int64_t)blockIdx.x * 8;
+    const int64_t r0 = (int64_t)blockIdx.x * RG;
     const bool RCONTIG = (p.rs == 1);
     const int ld = KW + (16 / (int)sizeof(Elem));     // padded row stride (elements)
     Elem *slab = reinterpret_cast<Elem *>(sbuf);
@@ -149,19 +152,19 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
     constexpr bool FOURM = (MODE == SPLIT_A4M || MODE == SPLIT_B4M);
     const int64_t kpad = FOURM ? p.kh : p.KB * 32;
     const int64_t nwin = (kpad + KW - 1) / KW;
-    const int nrows = (int)min((int64_t)8, max((int64_t)0, p.rows - r0));
+    const int nrows = (int)min((int64_t)RG, max((int64_t)0, p.rows - r0));
 
     auto load_window = [&](int64_t w0) {
         const int wlen = (int)min((int64_t)KW, p.k - w0);
         if (wlen > 0) {
-            if (RCONTIG) {   // the 8 rows are adjacent for each l: thread keeps row tid & 7
-                const int row = tid & 7;
+            if (RCONTIG) {   // the RG rows are adjacent for each l: thread keeps row tid % RG
+                const int row = tid % RG;
                 if (row < nrows) {
                     const int64_t gstep = 32 * p.ls;
-                    const Elem *g = X + r0 + row + (w0 + (tid >> 3)) * p.ls;
-                    Elem *d = slab + row * ld + (tid >> 3);
+                    const Elem *g = X + r0 + row + (w0 + tid / RG) * p.ls;
+                    Elem *d = slab + row * ld + tid / RG;
 #pragma unroll 4
-                    for (int l = tid >> 3; l < wlen; l += 32) {
+                    for (int l = tid / RG; l < wlen; l += 32) {
                         if (CPLX) cp_async16(d, g);
                         else cp_async8(d, g);
                         g += gstep;
@@ -243,8 +246,14 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
     }
     __syncthreads();
 
-    // ---------------- pass 2: digits; thread = (row, 8-value units h = h0 + 32 j)
-    const int row = tid & 7, h0 = tid >> 3;
+    // ---------------- pass 2: digits; thread = (row, 8-value units h = h0 + HSTEP j).
+    // 4M: the lanes also split by component c (0 = Re, 1 = Im'), so that one store instruction
+    // of a warp fills whole 32-B sectors: B4M rows 2r (Re) and 2r+1 (Im') are adjacent 16-B
+    // slots of a core matrix, both halves hh of each come from the same instruction.
+    const int row = tid % RG;
+    constexpr int HSTEP = FOURM ? 16 : 32;
+    const int c = FOURM ? ((tid / RG) & 1) : 0;
+    const int h0 = FOURM ? ((tid / RG) >> 1) : tid / RG;
     const int64_t R = (MODE == SPLIT_B4M) ? 2 * (r0 + row) : r0 + row;   // first output row
     const int64_t tile = R / TH, rr = R % TH;
     const int64_t tile_bytes = (int64_t)KBS * p.KB;
@@ -273,7 +282,7 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
         }
         const int wh = (int)((min((int64_t)KW, kpad - w0) + 7) / 8);   // 8-value units in window
         int8_t *op = obase + ((w0 >> 5) + (h0 >> 2)) * (int64_t)KBS;
-        for (int h = h0; h < wh; h += 32, op += 8 * (int64_t)KBS) {
+        for (int h = h0; h < wh; h += HSTEP, op += (HSTEP / 4) * (int64_t)KBS) {
             const int64_t l0 = w0 + 8 * h;
             const int nvalid = (int)min((int64_t)8, max((int64_t)0, p.k - l0));
             const Elem *src = slab + row * ld + 8 * h;
@@ -294,6 +303,31 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
                 uint32_t w_[D::NW][8], wn_[D::NW][8];
                 D::template words<false>(v, sc[0], sg[0], P - ex[0], w_, wn_);
                 D::template store<BLK>(w_, op);
+            } else if constexpr (FOURM) {
+                // this lane's component of 8 complex values; Im' = conj ? -Im : Im via -scale (RNE
+                // is sign-symmetric).  A4M: row r = [Re | Im'].  B4M (R9 N side): row 2r = [Re | -Im'],
+                // row 2r+1 = [Im' | Re]; lane c writes row 2r + c (first half, digits of X) and row
+                // 2r + 1 - c (second half, digits of X for Re, of -X for Im'), 16 B apart.
+                const double *sv = reinterpret_cast<const double *>(src) + c;
+                double v[8];
+                if (anylive && nvalid == 8) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) v[i] = sv[2 * i];
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) v[i] = (anylive && i < nvalid) ? sv[2 * i] : 0.0;
+                }
+                const bool negc = (c == 1) && p.conj;
+                uint32_t w_[D::NW][8], wn_[D::NW][8];
+                if constexpr (MODE == SPLIT_A4M) {
+                    D::template words<false>(v, negc ? -sc[0] : sc[0], negc ? -1.0 : 1.0, P - ex[0], w_, wn_);
+                    D::template store<BLK>(w_, op + (c ? half_off : 0));
+                } else {
+                    D::template words<true>(v, negc ? -sc[0] : sc[0], negc ? -1.0 : 1.0, P - ex[0], w_, wn_,
+                                            c == 1);
+                    D::template store<BLK>(w_, op + 16 * c);
+                    D::template store<BLK>(wn_, op + half_off + 16 * (1 - c));
+                }
             } else {
                 double re[8], im[8];
                 if (anylive && nvalid == 8) {
@@ -311,37 +345,7 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
                         im[i] = t.y;
                     }
                 }
-                if constexpr (MODE == SPLIT_A4M) {   // row r = [Re | Im] (Im conjugated: -scale)
-                    if (!anylive) {
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) re[i] = im[i] = 0.0;
-                    }
-                    const double sim = p.conj ? -sc[0] : sc[0];
-                    uint32_t w_[D::NW][8], wn_[D::NW][8];
-                    D::template words<false>(re, sc[0], 1.0, P - ex[0], w_, wn_);
-                    D::template store<BLK>(w_, op);
-                    D::template words<false>(im, sim, p.conj ? -1.0 : 1.0, P - ex[0], w_, wn_);
-                    D::template store<BLK>(w_, op + half_off);
-                } else if constexpr (MODE == SPLIT_B4M) {
-                    // R9 N side: output row 2r = [Re | -Im'], 2r+1 = [Im' | Re] with Im' = conj ? -Im : Im.
-                    // Rows 2r and 2r+1 share a tile; 2r+1 sits 16 B after 2r in the core matrix.
-                    if (!anylive) {
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) re[i] = im[i] = 0.0;
-                    }
-                    uint32_t w_[D::NW][8], wn_[D::NW][8];
-                    D::template words<false>(re, sc[0], 1.0, P - ex[0], w_, wn_);
-                    D::template store<BLK>(w_, op);
-                    D::template store<BLK>(w_, op + half_off + 16);
-                    D::template words<true>(im, sc[0], 1.0, P - ex[0], w_, wn_);   // w_ = Im, wn_ = -Im
-                    if (!p.conj) {
-                        D::template store<BLK>(w_, op + 16);
-                        D::template store<BLK>(wn_, op + half_off);
-                    } else {
-                        D::template store<BLK>(wn_, op + 16);
-                        D::template store<BLK>(w_, op + half_off);
-                    }
-                } else {   // SPLIT_3M: regions x = 0 (Re), 1 (Im'), 2 (fl(Re + Im')), own exponents
+                {          // SPLIT_3M: regions x = 0 (Re), 1 (Im'), 2 (fl(Re + Im')), own exponents
 #pragma unroll
                     for (int x = 0; x < 3; ++x) {
                         double v[8];
@@ -362,16 +366,16 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
 
 // Both operands of one product in ONE launch (blockIdx.z = side), A rows in 128-row tiles,
 // B rows in 64-row halves (the CTA-pair GEMM's layout).
-template <int S, int MA, int MB>
-__global__ void __launch_bounds__(256) k_split_fast(const __grid_constant__ SplitPair pp, int KW) {
+template <int S, int MA, int MB, int RG>
+__global__ void __launch_bounds__(32 * RG) k_split_fast(const __grid_constant__ SplitPair pp, int KW) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     extern __shared__ __align__(16) uint8_t sbuf[];
     if (blockIdx.z == 0) {
-        if ((int64_t)blockIdx.x * 8 >= pp.side[0].rows_grid) return;
-        split_fast_side<S, MA, 128>(pp.side[0], KW, sbuf);
+        if ((int64_t)blockIdx.x * RG >= pp.side[0].rows_grid) return;
+        split_fast_side<S, MA, 128, RG>(pp.side[0], KW, sbuf);
     } else {
-        if ((int64_t)blockIdx.x * 8 >= pp.side[1].rows_grid) return;
-        split_fast_side<S, MB, 64>(pp.side[1], KW, sbuf);
+        if ((int64_t)blockIdx.x * RG >= pp.side[1].rows_grid) return;
+        split_fast_side<S, MB, 64, RG>(pp.side[1], KW, sbuf);
     }
 }
 
