@@ -574,7 +574,8 @@ def split_roofline(split_ms, batch, n, s, method):
     read = 2 * batch * n * n * 16
     write = s * batch * (2 * n * n + 4 * n * n) if method == "4m" else s * batch * 6 * n * n
     gbs = (read + write) / (split_ms * 1e-3) / 1e9 if split_ms > 0 else 0.0
-    return {"bound": "hbm", "kernel": "k_split_sm (exponent scan + INT8 digits, both operands)",
+    kname = "k_split_fast" if s <= 8 else "k_split_sm"
+    return {"bound": "hbm", "kernel": f"{kname} (exponent scan + INT8 digits, both operands, one launch)",
             "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(gbs / hbm, 4),
             "algorithmic_bytes_per_step": int(read + write), "peak_source": src}
 

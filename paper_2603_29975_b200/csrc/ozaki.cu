@@ -435,6 +435,19 @@ SplitParams split_params(const Plan &P, const Operand &op, bool sideA, int8_t *s
 // launch, CTA-pair tiles (A 128 rows, B 64 rows), s <= 8, Ozaki-I digit layout.  Returns 1 when
 // the call does not qualify (the generic k_split_sm runs), else 0 / an error code.
 // OZAKI_SPLIT=generic forces the generic kernel (A/B tests).
+// LONG form of k_split_fast: 16 rows per CTA (512 threads) for real operands, 8 for complex
+template <int S, int MA, int MB>
+void launch_split_long(dim3 grid, size_t smem, cudaStream_t st, const SplitPair &pp, int KW, int nwin) {
+    constexpr int R = (MA == SPLIT_REAL) ? 16 : 8;
+    static size_t attr = 0;
+    if (attr < smem) {
+        cudaFuncSetAttribute(k_split_fast<S, MA, MB, R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        attr = smem;
+    }
+    k_split_fast<S, MA, MB, R, true><<<grid, 32 * R, smem, st>>>(pp, KW, nwin);
+}
+
 int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b, dim3 grid, cudaStream_t st) {
     if (!b || !P.pair || P.s < 1 || P.s > 8) return 1;
     if (a.tile_h != 128 || b->tile_h != 64) return 1;
@@ -455,10 +468,31 @@ int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b,
     int RG = 4;
     if (const char *rg = getenv("OZAKI_SPLIT_ROWS"))
         if (atoi(rg) == 8) RG = 8;
-    grid.x = (unsigned)((std::max(a.rows_grid, b->rows_grid) + RG - 1) / RG);
+    // long rows (>= 3 windows): exponents first (k_split_exps), then one CTA per (row group,
+    // window) -- OZAKI_SPLIT_LONG=0 / 1 forces the single-kernel / two-kernel form
+    const int64_t kpad = fourm ? a.kh : a.KB * 32;
+    int nwin = (int)((kpad + KW - 1) / KW);
+    bool lng = nwin >= 3;
+    if (const char *lg = getenv("OZAKI_SPLIT_LONG")) lng = (atoi(lg) != 0) && nwin > 1;
+    if (lng) {   // short windows, more rows per CTA: 128-B reads per l when rows are adjacent
+        RG = real ? 16 : 8;
+        KW = 256;
+        nwin = (int)((kpad + KW - 1) / KW);
+    }
+    grid.x = (unsigned)((std::max(a.rows_grid, b->rows_grid) + RG - 1) / RG) * (lng ? nwin : 1);
     SplitPair pp;
     pp.side[0] = a;
     pp.side[1] = *b;
+    if (lng) {
+        auto ctas = [](const SplitParams &q) { return (q.rows + (q.rs == 1 ? 31 : 7)) / (q.rs == 1 ? 32 : 8); };
+        dim3 ge((unsigned)std::max<int64_t>(1, std::max(ctas(a), ctas(*b))), grid.y, 2);
+        ProfScope ps(st, PH_EXP);
+        if (real) k_split_exps<SPLIT_REAL, SPLIT_REAL><<<ge, 256, 0, st>>>(pp);
+        else if (fourm) k_split_exps<SPLIT_A4M, SPLIT_B4M><<<ge, 256, 0, st>>>(pp);
+        else k_split_exps<SPLIT_3M, SPLIT_3M><<<ge, 256, 0, st>>>(pp);
+        CUDA_TRY(cudaGetLastError());
+        g_stats.launches += 1;
+    }
     const size_t smem = (size_t)RG * (KW + (real ? 2 : 1)) * (real ? 8 : 16);
     {
         ProfScope ps(st, PH_SLICE);
@@ -470,10 +504,11 @@ int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
                 attr = smem;                                                                         \
             }                                                                                        \
-            k_split_fast<S, MA, MB, R><<<grid, 32 * R, smem, st>>>(pp, KW);                          \
+            k_split_fast<S, MA, MB, R><<<grid, 32 * R, smem, st>>>(pp, KW, nwin);                    \
         }
+#define OZK_FAST_LONG(S, MA, MB) launch_split_long<S, MA, MB>(grid, smem, st, pp, KW, nwin);
 #define OZK_FAST(S, MA, MB)                                                                          \
-        if (RG == 4) OZK_FAST_RG(S, MA, MB, 4) else OZK_FAST_RG(S, MA, MB, 8)
+        if (lng) OZK_FAST_LONG(S, MA, MB) else if (RG == 4) OZK_FAST_RG(S, MA, MB, 4) else OZK_FAST_RG(S, MA, MB, 8)
 #define OZK_FAST_S(S)                                                                                \
         case S:                                                                                      \
             if (real) OZK_FAST(S, SPLIT_REAL, SPLIT_REAL)                                            \
@@ -487,6 +522,7 @@ int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b,
 #undef OZK_FAST_S
 #undef OZK_FAST
 #undef OZK_FAST_RG
+#undef OZK_FAST_LONG
     }
     CUDA_TRY(cudaGetLastError());
     g_stats.launches += 1;

@@ -129,7 +129,13 @@ __device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
 
 // One side of the split: RG input rows r0..r0+RG-1 of batch entry b (one warp per row in
 // pass 1, 32 * RG threads); MODE and the output tile height TH are compile-time.
-template <int S, int MODE, int TH, int RG>
+//
+// LONG (rows of many windows): the exponents come from k_split_exps (already in p.exps) and
+// each CTA digitises ONE window (blockIdx.x = row group * nwin + window), so no CTA keeps a
+// long row "open" between a first and a second read -- the input is read twice from HBM, but
+// every read streams (the windowed single-kernel form re-reads each window from L2 only while
+// the open rows of all resident CTAs fit there, which long rows do not).
+template <int S, int MODE, int TH, int RG, bool LONG>
 __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, uint8_t *sbuf) {
     constexpr bool CPLX = (MODE != SPLIT_REAL);
     constexpr int NX = (MODE == SPLIT_3M) ? 3 : 1;   // operands (exponents) per row
@@ -144,7 +150,6 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t b = blockIdx.y;
-    const int64_t r0 = (int64_t)blockIdx.x * RG;
     const bool RCONTIG = (p.rs == 1);
     const int ld = KW + (16 / (int)sizeof(Elem));     // padded row stride (elements)
     Elem *slab = reinterpret_cast<Elem *>(sbuf);
@@ -152,6 +157,8 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
     constexpr bool FOURM = (MODE == SPLIT_A4M || MODE == SPLIT_B4M);
     const int64_t kpad = FOURM ? p.kh : p.KB * 32;
     const int64_t nwin = (kpad + KW - 1) / KW;
+    const int64_t r0 = (LONG ? (int64_t)blockIdx.x / nwin : (int64_t)blockIdx.x) * RG;
+    const int64_t wbeg = LONG ? (int64_t)blockIdx.x % nwin : 0, wend = LONG ? wbeg + 1 : nwin;
     const int nrows = (int)min((int64_t)RG, max((int64_t)0, p.rows - r0));
 
     auto load_window = [&](int64_t w0) {
@@ -187,6 +194,19 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
     };
 
     // ---------------- pass 1: exponents (warp = row)
+    if constexpr (LONG) {   // from k_split_exps
+        if (tid < RG * NX) {
+            const int x = tid / RG, rw = tid % RG;
+            int32_t e = 0;
+            if (rw < nrows) {
+                const int32_t *ex = p.exps + (MODE == SPLIT_3M ? x * p.x_exps : 0) + b * p.rows_out;
+                e = ex[MODE == SPLIT_B4M ? 2 * (r0 + rw) : r0 + rw];
+            }
+            s_e[x][rw] = e;
+            const int sh = P - e;
+            s_scale[x][rw] = (sh >= -1022 && sh <= 1023) ? pow2(sh) : 0.0;
+        }
+    } else {
     uint32_t hm[NX];
 #pragma unroll
     for (int x = 0; x < NX; ++x) hm[x] = 0;
@@ -244,6 +264,7 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
             s_scale[x][warp] = (sh >= -1022 && sh <= 1023) ? pow2(sh) : 0.0;
         }
     }
+    }   // !LONG
     __syncthreads();
 
     // ---------------- pass 2: digits; thread = (row, 8-value units h = h0 + HSTEP j).
@@ -273,9 +294,9 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
     }
     const bool anylive = live[0];
 
-    for (int64_t w = 0; w < nwin; ++w) {
+    for (int64_t w = wbeg; w < wend; ++w) {
         const int64_t w0 = w * KW;
-        if (nwin > 1) {
+        if (LONG || nwin > 1) {
             __syncthreads();
             load_window(w0);
             __syncthreads();
@@ -366,17 +387,121 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
 
 // Both operands of one product in ONE launch (blockIdx.z = side), A rows in 128-row tiles,
 // B rows in 64-row halves (the CTA-pair GEMM's layout).
-template <int S, int MA, int MB, int RG>
-__global__ void __launch_bounds__(32 * RG) k_split_fast(const __grid_constant__ SplitPair pp, int KW) {
+template <int S, int MA, int MB, int RG, bool LONG = false>
+__global__ void __launch_bounds__(32 * RG) k_split_fast(const __grid_constant__ SplitPair pp, int KW,
+                                                         int nwin) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     extern __shared__ __align__(16) uint8_t sbuf[];
+    const int64_t rg = LONG ? (int64_t)blockIdx.x / nwin : (int64_t)blockIdx.x;
     if (blockIdx.z == 0) {
-        if ((int64_t)blockIdx.x * RG >= pp.side[0].rows_grid) return;
-        split_fast_side<S, MA, 128, RG>(pp.side[0], KW, sbuf);
+        if (rg * RG >= pp.side[0].rows_grid) return;
+        split_fast_side<S, MA, 128, RG, LONG>(pp.side[0], KW, sbuf);
     } else {
-        if ((int64_t)blockIdx.x * RG >= pp.side[1].rows_grid) return;
-        split_fast_side<S, MB, 64, RG>(pp.side[1], KW, sbuf);
+        if (rg * RG >= pp.side[1].rows_grid) return;
+        split_fast_side<S, MB, 64, RG, LONG>(pp.side[1], KW, sbuf);
     }
+}
+
+// R3 exponents of long rows (the LONG split's first kernel): exact 64-bit max of |x| per row
+// (NX maxima for SPLIT_3M: Re, Im', fl(Re + Im')), streamed from HBM once.
+//   rows contiguous along l: one warp per row (8 rows per CTA);
+//   rows adjacent for each l (rs == 1): lane = row (32 rows per CTA), the 8 warps split l and
+//   combine through shared memory.
+template <int MODE>
+__device__ __forceinline__ void exps_side(const SplitParams &p, int64_t g, int64_t b) {
+    constexpr bool CPLX = (MODE != SPLIT_REAL);
+    constexpr int NX = (MODE == SPLIT_3M) ? 3 : 1;
+    using Elem = typename std::conditional<CPLX, double2, double>::type;
+    __shared__ uint64_t s_m[3][8][32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const Elem *X = reinterpret_cast<const Elem *>(p.X) + b * p.bstride;
+    const bool RCONTIG = (p.rs == 1);
+    auto mag = [&](const Elem v, uint64_t (&m)[NX]) {
+        if constexpr (!CPLX) {
+            const uint64_t u = (uint64_t)__double_as_longlong(v) & kAbsMask;
+            m[0] = u > m[0] ? u : m[0];
+        } else {
+            const uint64_t ur = (uint64_t)__double_as_longlong(v.x) & kAbsMask;
+            const uint64_t ui = (uint64_t)__double_as_longlong(v.y) & kAbsMask;
+            if constexpr (MODE == SPLIT_3M) {
+                const double im = p.conj ? -v.y : v.y;
+                const uint64_t us = (uint64_t)__double_as_longlong(__dadd_rn(v.x, im)) & kAbsMask;
+                m[0] = ur > m[0] ? ur : m[0];
+                m[1] = ui > m[1] ? ui : m[1];
+                m[2] = us > m[2] ? us : m[2];
+            } else {
+                const uint64_t u = ur > ui ? ur : ui;
+                m[0] = u > m[0] ? u : m[0];
+            }
+        }
+    };
+    auto finish = [&](int64_t r, const uint64_t (&m)[NX]) {
+#pragma unroll
+        for (int x = 0; x < NX; ++x) {
+            const bool nf = m[x] >= kExpInf;
+            const int32_t e = nf ? kNonFinite : exponent_from_maxbits(m[x]);
+            int32_t *ex = p.exps + (MODE == SPLIT_3M ? x * p.x_exps : 0) + b * p.rows_out;
+            if (MODE == SPLIT_B4M) {
+                ex[2 * r] = e;
+                ex[2 * r + 1] = e;
+            } else {
+                ex[r] = e;
+            }
+            if (nf) atomicAdd(p.nonfinite, 1ull);
+        }
+    };
+    uint64_t m[NX];
+#pragma unroll
+    for (int x = 0; x < NX; ++x) m[x] = 0;
+    if (!RCONTIG) {
+        const int64_t r = g * 8 + warp;
+        if (r >= p.rows) return;
+        const Elem *gp = X + r * p.rs;
+#pragma unroll 8
+        for (int64_t l = lane; l < p.k; l += 32) mag(gp[l], m);
+#pragma unroll
+        for (int x = 0; x < NX; ++x) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const uint64_t om = __shfl_xor_sync(0xffffffffu, m[x], o);
+                m[x] = om > m[x] ? om : m[x];
+            }
+        }
+        if (lane == 0) finish(r, m);
+    } else {
+        const int64_t r = g * 32 + lane;
+        if (r < p.rows) {
+            const Elem *gp = X + r + warp * p.ls;
+            const int64_t step = 8 * p.ls;
+#pragma unroll 8
+            for (int64_t l = warp; l < p.k; l += 8, gp += step) mag(*gp, m);
+        }
+#pragma unroll
+        for (int x = 0; x < NX; ++x) s_m[x][warp][lane] = m[x];
+        __syncthreads();
+        if (warp == 0 && r < p.rows) {
+#pragma unroll
+            for (int x = 0; x < NX; ++x) {
+                uint64_t v = s_m[x][0][lane];
+#pragma unroll
+                for (int w = 1; w < 8; ++w) v = s_m[x][w][lane] > v ? s_m[x][w][lane] : v;
+                m[x] = v;
+            }
+            finish(r, m);
+        }
+    }
+}
+
+// One CTA per row group of one side (blockIdx.z) and batch entry (blockIdx.y): 8 rows (rows
+// contiguous along l) or 32 rows (rows adjacent for each l).  (A persistent form over both
+// sides' groups measured slower: the long 32-row groups then run on few CTAs.)
+template <int MA, int MB>
+__global__ void __launch_bounds__(256) k_split_exps(const __grid_constant__ SplitPair pp) {
+    const SplitParams &q = pp.side[blockIdx.z];
+    const int64_t gsz = (q.rs == 1) ? 32 : 8;
+    if ((int64_t)blockIdx.x * gsz >= q.rows) return;
+    if (blockIdx.z == 0) exps_side<MA>(q, blockIdx.x, blockIdx.y);
+    else exps_side<MB>(q, blockIdx.x, blockIdx.y);
 }
 
 }  // namespace ozk

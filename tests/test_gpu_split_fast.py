@@ -7,6 +7,7 @@ shortcuts could go wrong, vs the CPU oracle bit for bit:
   low word, zero rows;
 - rows longer than one SMEM window (real k > 1024, complex k > 512) and ragged tails;
 - conjugated operands (4M A side via -scale, B side via swapped +-Im targets; 3M Im');
+- the two-kernel LONG form (exponents by k_split_exps, one CTA per (row group, window));
 - the generic kernel (OZAKI_SPLIT=generic) gives the same bits.
 The GEMM result (and the INT32 level sums) are bit-exact only if every exponent and digit is.
 """
@@ -59,6 +60,16 @@ def tricky_real(rows, k, seed):
     return X
 
 
+@pytest.fixture(params=["auto", "0", "1"])
+def split_long(request):
+    """The single-kernel form, the two-kernel LONG form (k_split_exps + one CTA per window), or
+    the automatic choice (LONG from 3 windows)."""
+    if request.param != "auto":
+        os.environ["OZAKI_SPLIT_LONG"] = request.param
+    yield request.param
+    os.environ.pop("OZAKI_SPLIT_LONG", None)
+
+
 def with_generic(fn):
     os.environ["OZAKI_SPLIT"] = "generic"
     try:
@@ -69,7 +80,7 @@ def with_generic(fn):
 
 @pytest.mark.parametrize("s", [1, 2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("shape", [(70, 50, 40), (130, 70, 1500)])
-def test_dgemm_fast_split_exponent_branches(orc, s, shape):
+def test_dgemm_fast_split_exponent_branches(orc, s, shape, split_long):
     m, n, k = shape
     A = tricky_real(m, k, seed=11 * s)
     B = tricky_real(n, k, seed=13 * s).T.copy()      # columns of B carry the tricky rows
@@ -87,7 +98,7 @@ def test_dgemm_fast_split_exponent_branches(orc, s, shape):
 
 
 @pytest.mark.parametrize("s", [2, 5, 7, 8])
-def test_level_sums_fast_split_multiwindow(orc, s):
+def test_level_sums_fast_split_multiwindow(orc, s, split_long):
     m, n, k = 65, 130, 2100                          # 3 real windows, ragged tail
     A = tricky_real(m, k, seed=s)
     B = synth.spread(k, n, seed=50 + s, phi=2.0)
@@ -100,8 +111,8 @@ def test_level_sums_fast_split_multiwindow(orc, s):
 @pytest.mark.parametrize("s", [1, 3, 4, 7, 8])
 @pytest.mark.parametrize("method", ["4m", "3m"])
 @pytest.mark.parametrize("trans", [("N", "N"), ("C", "C"), ("T", "C"), ("C", "N")])
-@pytest.mark.parametrize("k", [45, 700])
-def test_zgemm_fast_split_conj_windows(orc, s, method, trans, k):
+@pytest.mark.parametrize("k", [45, 700, 1100])
+def test_zgemm_fast_split_conj_windows(orc, s, method, trans, k, split_long):
     ta, tb = trans
     m, n = 40, 36
     seed = (s * 131 + k) % 9973

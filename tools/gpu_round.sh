@@ -13,5 +13,11 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ge
     python bench.py --steps 1 --warmup 3 --no-extras ${BENCH_ARGS} > gpurun_out/ncu_gemm_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_split -s 3 -c 1 -f -o gpurun_out/prof_split_$TAG \
     python bench.py --steps 1 --warmup 3 --no-extras ${BENCH_ARGS} > gpurun_out/ncu_slice_$TAG.log 2>&1
+for k in gemm split; do   # export the raw pages here; the reports are too big to bring back
+  [ -f gpurun_out/prof_${k}_$TAG.ncu-rep ] || continue
+  ncu -i gpurun_out/prof_${k}_$TAG.ncu-rep --page raw --csv > gpurun_out/prof_${k}_${TAG}_raw.csv 2>&1
+  ncu -i gpurun_out/prof_${k}_$TAG.ncu-rep --page details --csv > gpurun_out/prof_${k}_${TAG}_details.csv 2>&1
+  rm -f gpurun_out/prof_${k}_$TAG.ncu-rep
+done
 fi
 ls -la gpurun_out

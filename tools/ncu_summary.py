@@ -32,8 +32,12 @@ KEYS = [
 
 
 def ncu_raw(rep):
-    res = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True)
-    rows = list(csv.reader(io.StringIO(res.stdout)))
+    if rep.endswith(".csv"):   # raw page exported on the GPU box (the .ncu-rep stays there)
+        text = open(rep).read()
+    else:
+        text = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                              text=True).stdout
+    rows = list(csv.reader(io.StringIO(text)))
     if len(rows) < 3:
         return []
     hdr, units = rows[0], rows[1]
@@ -86,6 +90,8 @@ def main(tag):
     summary = {}
     for kind in ("gemm", "slice", "split"):
         rep = os.path.join(OUT, f"prof_{kind}_{tag}.ncu-rep")
+        if not os.path.exists(rep):
+            rep = os.path.join(OUT, f"prof_{kind}_{tag}_raw.csv")
         if not os.path.exists(rep):
             continue
         rows = ncu_raw(rep)
