@@ -19,7 +19,8 @@ def main(tag):
         rows.append({"file": os.path.basename(f), "workload": d.get("config", {}).get("workload", ""),
                      "s": d.get("config", {}).get("slices"), "value": d.get("value"),
                      "ms_per_step": d.get("ms_per_step"), "gemm_ms": r.get("kernel_ms_per_launch"),
-                     "gemm_frac": r.get("frac"), "split_ms": ph.get("k1_slice"),
+                     "gemm_frac": r.get("frac"),
+                     "split_ms": round(ph.get("k1_slice", 0.0) + ph.get("k1_exponent", 0.0), 5),
                      "clocks": d.get("clocks", {})})
     with open(os.path.join(ROOT, "profiles", f"{tag}_configs.json"), "w") as fh:
         json.dump(rows, fh, indent=1)
