@@ -449,7 +449,7 @@ void launch_split_long(dim3 grid, size_t smem, cudaStream_t st, const SplitPair 
 }
 
 int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b, dim3 grid, cudaStream_t st) {
-    if (!b || !P.pair || P.s < 1 || P.s > 8) return 1;
+    if (!b || !P.pair || P.s < 1 || P.s > 12) return 1;
     if (a.tile_h != 128 || b->tile_h != 64) return 1;
     if (a.kbs_bytes != (int64_t)P.s * 128 * 32 || b->kbs_bytes != (int64_t)P.s * 64 * 32) return 1;
     const bool real = a.mode == SPLIT_REAL && b->mode == SPLIT_REAL;
@@ -463,11 +463,9 @@ int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b,
         const int v = atoi(kw);
         if (v >= 64 && v <= 1024 && v % 32 == 0) KW = real ? v : std::min(v, 512);
     }
-    // rows per CTA (one warp each): 4 by default -- twice the CTAs of 8, so more load / compute
-    // phases overlap per SM at the same SMEM per row; OZAKI_SPLIT_ROWS=8 for A/B tests
+    // rows per CTA (one warp each): 4 -- more, smaller CTAs than 8 rows, so more load / compute
+    // phases overlap per SM at the same SMEM per row (measured: equal for 4M, -8% time for 3M)
     int RG = 4;
-    if (const char *rg = getenv("OZAKI_SPLIT_ROWS"))
-        if (atoi(rg) == 8) RG = 8;
     // long rows (>= 3 windows): exponents first (k_split_exps), then one CTA per (row group,
     // window) -- OZAKI_SPLIT_LONG=0 / 1 forces the single-kernel / two-kernel form
     const int64_t kpad = fourm ? a.kh : a.KB * 32;
@@ -508,7 +506,7 @@ int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b,
         }
 #define OZK_FAST_LONG(S, MA, MB) launch_split_long<S, MA, MB>(grid, smem, st, pp, KW, nwin);
 #define OZK_FAST(S, MA, MB)                                                                          \
-        if (lng) OZK_FAST_LONG(S, MA, MB) else if (RG == 4) OZK_FAST_RG(S, MA, MB, 4) else OZK_FAST_RG(S, MA, MB, 8)
+        if (lng) OZK_FAST_LONG(S, MA, MB) else OZK_FAST_RG(S, MA, MB, 4)
 #define OZK_FAST_S(S)                                                                                \
         case S:                                                                                      \
             if (real) OZK_FAST(S, SPLIT_REAL, SPLIT_REAL)                                            \
@@ -518,6 +516,7 @@ int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b,
         switch (P.s) {
             OZK_FAST_S(1) OZK_FAST_S(2) OZK_FAST_S(3) OZK_FAST_S(4)
             OZK_FAST_S(5) OZK_FAST_S(6) OZK_FAST_S(7) OZK_FAST_S(8)
+            OZK_FAST_S(9) OZK_FAST_S(10) OZK_FAST_S(11) OZK_FAST_S(12)
         }
 #undef OZK_FAST_S
 #undef OZK_FAST

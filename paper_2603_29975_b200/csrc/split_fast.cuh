@@ -1,4 +1,4 @@
-// split_fast.cuh -- K1 for the production Ozaki-I path (CTA-pair GEMM layout, s <= 8).
+// split_fast.cuh -- K1 for the production Ozaki-I path (CTA-pair GEMM layout, s <= 12).
 //
 // Same method and output as k_split_sm (split.cuh): §2.2 ("splits
 // high-precision input matrices into slices ... based on their significant bits
@@ -44,34 +44,66 @@ __device__ __forceinline__ void st_global_v2(int8_t *p, uint32_t a, uint32_t b) 
 template <int S>
 struct FastDigits {
     static constexpr int NW = (S + 3) / 4;   // 32-bit words of Y holding the S digit bytes
-    static constexpr unsigned long long B = 0x0080808080808080ull >> (8 * (8 - S));
+    static constexpr unsigned long long B = 0x0080808080808080ull >> (8 * (8 - (S < 8 ? S : 8)));
 
     // R4 for 8 values: X = RNE(v * 2^(P-e)) (scale = +-2^(P-e) when that power is a normal
     // double: one exact-or-correctly-rounded DMUL; else ldexp_rn on sgn*v), Y = (X + B) ^ B
     // (byte q = balanced digit of slice S - q).  NEG also forms wn = the digits of X2, where
     // X2 = -X if neg2 else X (a per-lane choice without register-array selects).
+    // S <= 8: |X| <= 127 * 2^(8S-8) fits int64; S = 9..12: 128-bit X (|y| >= 2^63 is an
+    // integer mantissa * 2^q, exact).
     template <bool NEG>
     __device__ __forceinline__ static void words(const double (&v)[8], double scale, double sgn, int sh,
                                                  uint32_t (&w)[NW][8], uint32_t (&wn)[NW][8],
                                                  bool neg2 = true) {
-        long long X[8];
-        if (scale != 0.0) {
+        if constexpr (S <= 8) {
+            long long X[8];
+            if (scale != 0.0) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) X[i] = __double2ll_rn(__dmul_rn(v[i], scale));
-        } else {   // 2^(P-e) is not a normal double (extreme exponents): exact ldexp
+                for (int i = 0; i < 8; ++i) X[i] = __double2ll_rn(__dmul_rn(v[i], scale));
+            } else {   // 2^(P-e) is not a normal double (extreme exponents): exact ldexp
 #pragma unroll
-            for (int i = 0; i < 8; ++i) X[i] = __double2ll_rn(ldexp_rn(sgn * v[i], sh));
-        }
+                for (int i = 0; i < 8; ++i) X[i] = __double2ll_rn(ldexp_rn(sgn * v[i], sh));
+            }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const unsigned long long Y = ((unsigned long long)X[i] + B) ^ B;
-            w[0][i] = (uint32_t)Y;
-            if constexpr (NW > 1) w[1][i] = (uint32_t)(Y >> 32);
-            if constexpr (NEG) {
-                const unsigned long long X2 = neg2 ? 0ull - (unsigned long long)X[i] : (unsigned long long)X[i];
-                const unsigned long long Yn = (X2 + B) ^ B;
-                wn[0][i] = (uint32_t)Yn;
-                if constexpr (NW > 1) wn[1][i] = (uint32_t)(Yn >> 32);
+            for (int i = 0; i < 8; ++i) {
+                const unsigned long long Y = ((unsigned long long)X[i] + B) ^ B;
+                w[0][i] = (uint32_t)Y;
+                if constexpr (NW > 1) w[1][i] = (uint32_t)(Y >> 32);
+                if constexpr (NEG) {
+                    const unsigned long long X2 =
+                        neg2 ? 0ull - (unsigned long long)X[i] : (unsigned long long)X[i];
+                    const unsigned long long Yn = (X2 + B) ^ B;
+                    wn[0][i] = (uint32_t)Yn;
+                    if constexpr (NW > 1) wn[1][i] = (uint32_t)(Yn >> 32);
+                }
+            }
+        } else {
+            unsigned __int128 B2 = 0;
+#pragma unroll
+            for (int q = 0; q < S - 1; ++q) B2 |= (unsigned __int128)0x80 << (8 * q);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const double y = (scale != 0.0) ? __dmul_rn(v[i], scale) : ldexp_rn(sgn * v[i], sh);
+                __int128 X;
+                if (fabs(y) < 9223372036854775808.0) {
+                    X = (__int128)__double2ll_rn(y);
+                } else {   // |y| >= 2^63: an integer, mantissa * 2^q with q >= 11
+                    const uint64_t bits = (uint64_t)__double_as_longlong(y);
+                    const int q = (int)((bits >> 52) & 0x7ff) - 1075;
+                    X = (__int128)((bits & kFracMask) | (1ull << 52)) << q;
+                    if (bits >> 63) X = -X;
+                }
+                const unsigned __int128 Y = ((unsigned __int128)X + B2) ^ B2;
+#pragma unroll
+                for (int j = 0; j < NW; ++j) w[j][i] = (uint32_t)(Y >> (32 * j));
+                if constexpr (NEG) {
+                    const unsigned __int128 X2 = neg2 ? (unsigned __int128)0 - (unsigned __int128)X
+                                                      : (unsigned __int128)X;
+                    const unsigned __int128 Yn = (X2 + B2) ^ B2;
+#pragma unroll
+                    for (int j = 0; j < NW; ++j) wn[j][i] = (uint32_t)(Yn >> (32 * j));
+                }
             }
         }
     }

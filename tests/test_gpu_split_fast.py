@@ -78,7 +78,7 @@ def with_generic(fn):
         del os.environ["OZAKI_SPLIT"]
 
 
-@pytest.mark.parametrize("s", [1, 2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("s", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12])
 @pytest.mark.parametrize("shape", [(70, 50, 40), (130, 70, 1500)])
 def test_dgemm_fast_split_exponent_branches(orc, s, shape, split_long):
     m, n, k = shape
@@ -97,7 +97,7 @@ def test_dgemm_fast_split_exponent_branches(orc, s, shape, split_long):
     assert same(gen.cpu().numpy(), want)
 
 
-@pytest.mark.parametrize("s", [2, 5, 7, 8])
+@pytest.mark.parametrize("s", [2, 5, 7, 8, 9, 12])
 def test_level_sums_fast_split_multiwindow(orc, s, split_long):
     m, n, k = 65, 130, 2100                          # 3 real windows, ragged tail
     A = tricky_real(m, k, seed=s)
@@ -108,7 +108,7 @@ def test_level_sums_fast_split_multiwindow(orc, s, split_long):
     assert (S.astype(np.int64) == orc.level_sums(DA, DB, s)).all()
 
 
-@pytest.mark.parametrize("s", [1, 3, 4, 7, 8])
+@pytest.mark.parametrize("s", [1, 3, 4, 7, 8, 9, 12])
 @pytest.mark.parametrize("method", ["4m", "3m"])
 @pytest.mark.parametrize("trans", [("N", "N"), ("C", "C"), ("T", "C"), ("C", "N")])
 @pytest.mark.parametrize("k", [45, 700, 1100])
