@@ -1163,6 +1163,75 @@ int crt_nu(const CrtHost &h, int64_t keff) {
     return std::min(nu, 62);
 }
 
+// K1' for Ozaki-II through k_split_fast<…, CRT>: both operands in one launch, 128-row tiles on
+// both sides, the moduli word count compile-time (n rounded up to a multiple of 4).  Returns 1
+// when OZAKI_SPLIT=generic asks for the generic k_split_sm form.
+template <int NMX>
+void launch_crt_fast(bool real, bool lng, dim3 grid, size_t smem, cudaStream_t st, const SplitPair &pp, int KW,
+                     int nwin) {
+#define OZK_CRT_K(MA, MB, R, L)                                                                      \
+    {                                                                                                \
+        static size_t attr = 0;                                                                      \
+        if (attr < smem) {                                                                           \
+            cudaFuncSetAttribute(k_split_fast<NMX, MA, MB, R, L, true>,                              \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
+            attr = smem;                                                                             \
+        }                                                                                            \
+        k_split_fast<NMX, MA, MB, R, L, true><<<grid, 32 * R, smem, st>>>(pp, KW, nwin);             \
+    }
+    if (real) {
+        if (lng) OZK_CRT_K(SPLIT_REAL, SPLIT_REAL, 16, true) else OZK_CRT_K(SPLIT_REAL, SPLIT_REAL, 4, false)
+    } else {
+        if (lng) OZK_CRT_K(SPLIT_A4M, SPLIT_B4M, 8, true) else OZK_CRT_K(SPLIT_A4M, SPLIT_B4M, 4, false)
+    }
+#undef OZK_CRT_K
+}
+
+int launch_split_fast_crt(const SplitParams &a, const SplitParams &b, int64_t batch, cudaStream_t st) {
+    if (const char *e = getenv("OZAKI_SPLIT"))
+        if (!strcmp(e, "generic")) return 1;
+    const bool real = a.mode == SPLIT_REAL;
+    const int64_t rows_grid = std::max(a.rows_grid, b.rows_grid);
+    if (rows_grid == 0) return 0;
+    int KW = real ? 1024 : 512, RG = 4;
+    const int64_t kpad = real ? a.KB * 32 : a.kh;
+    int nwin = (int)((kpad + KW - 1) / KW);
+    bool lng = nwin >= 3;
+    if (const char *lg = getenv("OZAKI_SPLIT_LONG")) lng = (atoi(lg) != 0) && nwin > 1;
+    if (lng) {
+        RG = real ? 16 : 8;
+        KW = 256;
+        nwin = (int)((kpad + KW - 1) / KW);
+    }
+    SplitPair pp;
+    pp.side[0] = a;
+    pp.side[1] = b;
+    dim3 grid((unsigned)((rows_grid + RG - 1) / RG) * (lng ? nwin : 1), (unsigned)batch, 2);
+    if (lng) {
+        auto ctas = [](const SplitParams &q) { return (q.rows + (q.rs == 1 ? 31 : 7)) / (q.rs == 1 ? 32 : 8); };
+        dim3 ge((unsigned)std::max<int64_t>(1, std::max(ctas(a), ctas(b))), (unsigned)batch, 2);
+        ProfScope ps(st, PH_EXP);
+        if (real) k_split_exps<SPLIT_REAL, SPLIT_REAL, true><<<ge, 256, 0, st>>>(pp);
+        else k_split_exps<SPLIT_A4M, SPLIT_B4M, true><<<ge, 256, 0, st>>>(pp);
+        CUDA_TRY(cudaGetLastError());
+        g_stats.launches += 1;
+    }
+    const size_t smem = (size_t)RG * (KW + (real ? 2 : 1)) * (real ? 8 : 16);
+    {
+        ProfScope ps(st, PH_SLICE);
+        switch ((a.crt.n + 3) / 4) {
+            case 1: launch_crt_fast<4>(real, lng, grid, smem, st, pp, KW, nwin); break;
+            case 2: launch_crt_fast<8>(real, lng, grid, smem, st, pp, KW, nwin); break;
+            case 3: launch_crt_fast<12>(real, lng, grid, smem, st, pp, KW, nwin); break;
+            case 4: launch_crt_fast<16>(real, lng, grid, smem, st, pp, KW, nwin); break;
+            default: launch_crt_fast<20>(real, lng, grid, smem, st, pp, KW, nwin); break;
+        }
+    }
+    CUDA_TRY(cudaGetLastError());
+    g_stats.launches += 1;
+    return 0;
+}
+
 int run_crt(const Call &c, DevState *dev, cudaStream_t st) {
     const int n = c.s;
     const CrtHost &h = crt_tables(n);
@@ -1198,7 +1267,7 @@ int run_crt(const Call &c, DevState *dev, cudaStream_t st) {
     int rc = 0;
 
     // ---- K1': R17 quantisation + R18 residues (modulus-major slices, 128-row tiles)
-    auto split = [&](const Operand &op, bool sideA, int8_t *out, int32_t *exps) -> int {
+    auto params = [&](const Operand &op, bool sideA, int8_t *out, int32_t *exps) {
         SplitParams sp{};
         sp.X = op.X;
         sp.rs = op.rs;
@@ -1214,7 +1283,7 @@ int run_crt(const Call &c, DevState *dev, cudaStream_t st) {
         sp.KB = KB;
         sp.kh = kh;
         sp.rows_out = (op.mode == SPLIT_B4M) ? 2 * op.rows : op.rows;
-        sp.rows_grid = (op.mode == SPLIT_B4M) ? sp.tiles * sp.tile_h / 2 : sp.tiles * sp.tile_h;
+        sp.rows_grid = (op.rows == 0) ? 0 : ((op.mode == SPLIT_B4M) ? sp.tiles * sp.tile_h / 2 : sp.tiles * sp.tile_h);
         sp.out = out;
         sp.exps = exps;
         sp.nonfinite = dev->nonfinite;
@@ -1222,8 +1291,11 @@ int run_crt(const Call &c, DevState *dev, cudaStream_t st) {
         sp.ss_bytes = (int64_t)KB * kCrtBlk;
         sp.crt = h.tab;
         sp.crt.nu = nu;
-        if (op.rows == 0) return 0;
-        const bool cx = op.mode != SPLIT_REAL;
+        return sp;
+    };
+    auto split = [&](const SplitParams &sp) -> int {   // generic form, one operand per launch
+        if (sp.rows == 0) return 0;
+        const bool cx = sp.mode != SPLIT_REAL;
         dim3 grid((unsigned)((sp.rows_grid + 7) / 8), (unsigned)c.batch);
         const int KW = cx ? 512 : 1024;
         const size_t smem = (size_t)8 * (KW + (cx ? 1 : 2)) * (cx ? 16 : 8);
@@ -1248,8 +1320,13 @@ int run_crt(const Call &c, DevState *dev, cudaStream_t st) {
         return 0;
     };
     const int ma = cplx ? SPLIT_A4M : SPLIT_REAL, mb = cplx ? SPLIT_B4M : SPLIT_REAL;
-    rc = split(view_A(c.A, c.ta, c.m, c.k, c.lda, c.sA, ma), true, sa, ea);
-    if (!rc) rc = split(view_B(c.B, c.tb, c.n, c.k, c.ldb, c.sB, mb), false, sb, fb);
+    const SplitParams spa = params(view_A(c.A, c.ta, c.m, c.k, c.lda, c.sA, ma), true, sa, ea);
+    const SplitParams spb = params(view_B(c.B, c.tb, c.n, c.k, c.ldb, c.sB, mb), false, sb, fb);
+    rc = launch_split_fast_crt(spa, spb, c.batch, st);
+    if (rc == 1) {
+        rc = split(spa);
+        if (!rc) rc = split(spb);
+    }
 
     // ---- K2': one INT8 GEMM per modulus, residues of the products (R19)
     if (!rc) {

@@ -33,6 +33,19 @@ __device__ __forceinline__ bool exponent_from_hi(uint32_t H, int32_t &e) {
     return true;
 }
 
+// R17 (crt_exponent) from the max high word: e = E + 1 for a normal max 1.f 2^E, plus one when
+// nu <= 52 and the top nu fraction bits are all ones.  Decided by the high word unless the max
+// is subnormal / zero or (nu > 20 and the 20 high fraction bits are all ones).
+__device__ __forceinline__ bool exponent_from_hi_crt(uint32_t H, int nu, int32_t &e) {
+    const uint32_t ex = H >> 20, f = H & 0xfffffu;
+    if (ex == 0) return false;
+    bool bump = false;
+    if (nu <= 20) bump = f >= (1u << 20) - (1u << (20 - nu));
+    else if (nu <= 52 && f == 0xfffffu) return false;
+    e = (int32_t)ex - 1022 + (bump ? 1 : 0);
+    return true;
+}
+
 __device__ __forceinline__ uint32_t hi_abs(double x) {
     return (uint32_t)__double2hiint(x) & 0x7fffffffu;
 }
@@ -126,6 +139,123 @@ struct FastDigits {
     }
 };
 
+template <int S>
+struct FastDigitsEmit : FastDigits<S> {
+    using D = FastDigits<S>;
+    // one target: the digits of X
+    template <int BLK>
+    __device__ __forceinline__ static void emit1(const double (&v)[8], double scale, double sgn, int sh,
+                                                 int8_t *p1, const SplitParams &) {
+        uint32_t w[D::NW][8], wn[D::NW][8];
+        D::template words<false>(v, scale, sgn, sh, w, wn);
+        D::template store<BLK>(w, p1);
+    }
+    // two targets: p1 <- digits of X, p2 <- digits of X2 (-X if neg2 else X)
+    template <int BLK>
+    __device__ __forceinline__ static void emit2(const double (&v)[8], double scale, double sgn, int sh,
+                                                 int8_t *p1, int8_t *p2, bool neg2, const SplitParams &) {
+        uint32_t w[D::NW][8], wn[D::NW][8];
+        D::template words<true>(v, scale, sgn, sh, w, wn, neg2);
+        D::template store<BLK>(w, p1);
+        D::template store<BLK>(wn, p2);
+    }
+};
+
+// Ozaki-II (NEXT-1) counterpart: R17 Q = RNE(v 2^(nu-e)) as int64 and the centred residues
+// of Q mod p_q for the NM moduli (R18, crt.cuh), one byte each, modulus-major (stride
+// p.ss_bytes).  Processed 4 moduli (one 32-bit word per value) at a time to bound registers.
+// NM is a multiple of 4 (the word count is compile-time); the live moduli count is prm.crt.n.
+template <int NM>
+struct FastResidues {
+    static constexpr int NW = (NM + 3) / 4;
+    __device__ __forceinline__ static void quantise(const double (&v)[8], double scale, double sgn, int sh,
+                                                    int32_t (&q2)[8], uint32_t (&q1)[8], uint32_t (&q0)[8]) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const double xs = (scale != 0.0) ? __dmul_rn(v[i], scale) : ldexp_rn(sgn * v[i], sh);
+            const long long Q = __double2ll_rn(xs);   // |Q| < 2^nu <= 2^62
+            q0[i] = (uint32_t)Q & 0x1fffffu;
+            q1[i] = (uint32_t)(Q >> 21) & 0x1fffffu;
+            q2[i] = (int32_t)(Q >> 42);
+        }
+    }
+    __device__ __forceinline__ static void store_word(const uint32_t (&w)[8], int j, int nm, int8_t *p,
+                                                      int64_t ss) {
+        uint32_t lo[4], hi[4];
+        transpose4x4(w[0], w[1], w[2], w[3], lo[0], lo[1], lo[2], lo[3]);
+        transpose4x4(w[4], w[5], w[6], w[7], hi[0], hi[1], hi[2], hi[3]);
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq)
+            if (4 * j + qq < nm) st_global_v2(p + (int64_t)(4 * j + qq) * ss, lo[qq], hi[qq]);
+    }
+    // centred residue byte of Q (R18) for modulus q: with h = floor(p/2), x = fold(Q) >= 0 and
+    // t = floor((x + h) / p), r = x - t p lies in [-h, p - 1 - h] (the centred range: symmetric
+    // for odd p, [-128, 127] for p = 256) -- the same value as centre_byte(x mod p).
+    __device__ __forceinline__ static uint32_t cres(int32_t q2, uint32_t q1, uint32_t q0, const CrtTab &t, int q) {
+        const uint32_t x = (uint32_t)(q2 * (int32_t)t.c42[q]) + q1 * t.c21[q] + q0 + t.bias28[q];
+        const uint32_t h = t.p[q] >> 1;
+        const uint32_t tq = (uint32_t)(((unsigned long long)(x + h) * t.m40[q]) >> 40);
+        return x - tq * t.p[q];   // low byte = the centred residue (two's complement)
+    }
+    // per-byte negation of 4 packed two's-complement bytes (-(-128) wraps to -128 = the centred
+    // residue of -Q for p = 256; odd p have symmetric ranges)
+    __device__ __forceinline__ static uint32_t neg4(uint32_t w) {
+        const uint32_t nw = ~w;
+        return ((nw & 0x7f7f7f7fu) + 0x01010101u) ^ (nw & 0x80808080u);
+    }
+    template <int BLK>
+    __device__ __forceinline__ static void emit1(const double (&v)[8], double scale, double sgn, int sh,
+                                                 int8_t *p1, const SplitParams &prm) {
+        int32_t q2[8];
+        uint32_t q1[8], q0[8];
+        quantise(v, scale, sgn, sh, q2, q1, q0);
+#pragma unroll
+        for (int j = 0; j < NW; ++j) {
+            uint32_t w[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[i] = 0;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                const int q = 4 * j + qq;
+                if (q < prm.crt.n) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        w[i] = __byte_perm(w[i], cres(q2[i], q1[i], q0[i], prm.crt, q), (0x3210 & ~(0xf << (4 * qq))) | (4 << (4 * qq)));
+                }
+            }
+            store_word(w, j, prm.crt.n, p1, prm.ss_bytes);
+        }
+    }
+    template <int BLK>
+    __device__ __forceinline__ static void emit2(const double (&v)[8], double scale, double sgn, int sh,
+                                                 int8_t *p1, int8_t *p2, bool neg2, const SplitParams &prm) {
+        int32_t q2[8];
+        uint32_t q1[8], q0[8];
+        quantise(v, scale, sgn, sh, q2, q1, q0);
+#pragma unroll
+        for (int j = 0; j < NW; ++j) {
+            uint32_t w[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[i] = 0;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                const int q = 4 * j + qq;
+                if (q < prm.crt.n) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        w[i] = __byte_perm(w[i], cres(q2[i], q1[i], q0[i], prm.crt, q), (0x3210 & ~(0xf << (4 * qq))) | (4 << (4 * qq)));
+                }
+            }
+            store_word(w, j, prm.crt.n, p1, prm.ss_bytes);
+            if (neg2) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) w[i] = neg4(w[i]);
+            }
+            store_word(w, j, prm.crt.n, p2, prm.ss_bytes);
+        }
+    }
+};
+
 // Exact 64-bit max |x| of row r over the valid depth, straight from global memory (rare path).
 template <bool CPLX>
 __device__ uint64_t row_max_bits_slow(const SplitParams &p, const void *Xb, int64_t r, int comp, int lane) {
@@ -167,14 +297,17 @@ __device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
 // long row "open" between a first and a second read -- the input is read twice from HBM, but
 // every read streams (the windowed single-kernel form re-reads each window from L2 only while
 // the open rows of all resident CTAs fit there, which long rows do not).
-template <int S, int MODE, int TH, int RG, bool LONG>
+//
+// CRT (Ozaki-II, NEXT-1): S is the moduli count; pass 1 takes the exact 64-bit max and the R17
+// exponent (crt_exponent), pass 2 emits residues instead of digits, modulus-major per tile.
+template <int S, int MODE, int TH, int RG, bool LONG, bool CRT = false>
 __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, uint8_t *sbuf) {
     constexpr bool CPLX = (MODE != SPLIT_REAL);
     constexpr int NX = (MODE == SPLIT_3M) ? 3 : 1;   // operands (exponents) per row
     constexpr int BLK = TH * 32;                      // bytes of one (tile, k-block, slice) block
-    constexpr int KBS = S * BLK;                      // bytes between k-blocks of one tile
-    constexpr int P = 8 * S - 1;
-    using D = FastDigits<S>;
+    constexpr int KBS = CRT ? BLK : S * BLK;          // bytes between k-blocks of one tile
+    const int P = CRT ? p.crt.nu : 8 * S - 1;         // fixed-point bits (R4) / quantisation bits (R17)
+    using D = typename std::conditional<CRT, FastResidues<S>, FastDigitsEmit<S>>::type;
     using Elem = typename std::conditional<CPLX, double2, double>::type;
 
     __shared__ int32_t s_e[3][RG];
@@ -275,9 +408,10 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
             if (H >= 0x7ff00000u) {          // an Inf / NaN in the row (R10)
                 nf = true;
                 e = kNonFinite;
-            } else if (!exponent_from_hi(H, e)) {
+            } else if (!(CRT ? exponent_from_hi_crt(H, p.crt.nu, e) : exponent_from_hi(H, e))) {
                 const int comp = (MODE == SPLIT_3M) ? x : (CPLX ? 3 : 0);
-                e = exponent_from_maxbits(row_max_bits_slow<CPLX>(p, X, r0 + warp, comp, lane));
+                const uint64_t mx = row_max_bits_slow<CPLX>(p, X, r0 + warp, comp, lane);
+                e = CRT ? crt_exponent(mx, p.crt.nu) : exponent_from_maxbits(mx);
             }
         }
         if (lane == 0) {
@@ -309,7 +443,7 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
     const int h0 = FOURM ? ((tid / RG) >> 1) : tid / RG;
     const int64_t R = (MODE == SPLIT_B4M) ? 2 * (r0 + row) : r0 + row;   // first output row
     const int64_t tile = R / TH, rr = R % TH;
-    const int64_t tile_bytes = (int64_t)KBS * p.KB;
+    const int64_t tile_bytes = (int64_t)(CRT ? p.crt.n : S) * BLK * p.KB;
     int8_t *obase = p.out + (b * p.tiles + tile) * tile_bytes + (rr >> 3) * 256 + (rr & 7) * 16 +
                     ((h0 >> 1) & 1) * 128 + (h0 & 1) * 8;
     const int64_t half_off = (p.kh >> 5) * KBS;        // 4M: the second K half (Im / Re block)
@@ -353,9 +487,7 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
 #pragma unroll
                     for (int i = 0; i < 8; ++i) v[i] = (anylive && i < nvalid) ? src[i] : 0.0;
                 }
-                uint32_t w_[D::NW][8], wn_[D::NW][8];
-                D::template words<false>(v, sc[0], sg[0], P - ex[0], w_, wn_);
-                D::template store<BLK>(w_, op);
+                D::template emit1<BLK>(v, sc[0], sg[0], P - ex[0], op, p);
             } else if constexpr (FOURM) {
                 // this lane's component of 8 complex values; Im' = conj ? -Im : Im via -scale (RNE
                 // is sign-symmetric).  A4M: row r = [Re | Im'].  B4M (R9 N side): row 2r = [Re | -Im'],
@@ -371,15 +503,12 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
                     for (int i = 0; i < 8; ++i) v[i] = (anylive && i < nvalid) ? sv[2 * i] : 0.0;
                 }
                 const bool negc = (c == 1) && p.conj;
-                uint32_t w_[D::NW][8], wn_[D::NW][8];
                 if constexpr (MODE == SPLIT_A4M) {
-                    D::template words<false>(v, negc ? -sc[0] : sc[0], negc ? -1.0 : 1.0, P - ex[0], w_, wn_);
-                    D::template store<BLK>(w_, op + (c ? half_off : 0));
+                    D::template emit1<BLK>(v, negc ? -sc[0] : sc[0], negc ? -1.0 : 1.0, P - ex[0],
+                                           op + (c ? half_off : 0), p);
                 } else {
-                    D::template words<true>(v, negc ? -sc[0] : sc[0], negc ? -1.0 : 1.0, P - ex[0], w_, wn_,
-                                            c == 1);
-                    D::template store<BLK>(w_, op + 16 * c);
-                    D::template store<BLK>(wn_, op + half_off + 16 * (1 - c));
+                    D::template emit2<BLK>(v, negc ? -sc[0] : sc[0], negc ? -1.0 : 1.0, P - ex[0], op + 16 * c,
+                                           op + half_off + 16 * (1 - c), c == 1, p);
                 }
             } else {
                 double re[8], im[8];
@@ -407,9 +536,7 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
                             const double imc = p.conj ? -im[i] : im[i];
                             v[i] = live[x] ? (x == 0 ? re[i] : (x == 1 ? im[i] : __dadd_rn(re[i], imc))) : 0.0;
                         }
-                        uint32_t w_[D::NW][8], wn_[D::NW][8];
-                        D::template words<false>(v, sc[x], sg[x], P - ex[x], w_, wn_);
-                        D::template store<BLK>(w_, op + x * p.x_bytes);
+                        D::template emit1<BLK>(v, sc[x], sg[x], P - ex[x], op + x * p.x_bytes, p);
                     }
                 }
             }
@@ -419,7 +546,7 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
 
 // Both operands of one product in ONE launch (blockIdx.z = side), A rows in 128-row tiles,
 // B rows in 64-row halves (the CTA-pair GEMM's layout).
-template <int S, int MA, int MB, int RG, bool LONG = false>
+template <int S, int MA, int MB, int RG, bool LONG = false, bool CRT = false>
 __global__ void __launch_bounds__(32 * RG) k_split_fast(const __grid_constant__ SplitPair pp, int KW,
                                                          int nwin) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -427,10 +554,10 @@ __global__ void __launch_bounds__(32 * RG) k_split_fast(const __grid_constant__ 
     const int64_t rg = LONG ? (int64_t)blockIdx.x / nwin : (int64_t)blockIdx.x;
     if (blockIdx.z == 0) {
         if (rg * RG >= pp.side[0].rows_grid) return;
-        split_fast_side<S, MA, 128, RG, LONG>(pp.side[0], KW, sbuf);
+        split_fast_side<S, MA, 128, RG, LONG, CRT>(pp.side[0], KW, sbuf);
     } else {
         if (rg * RG >= pp.side[1].rows_grid) return;
-        split_fast_side<S, MB, 64, RG, LONG>(pp.side[1], KW, sbuf);
+        split_fast_side<S, MB, CRT ? 128 : 64, RG, LONG, CRT>(pp.side[1], KW, sbuf);
     }
 }
 
@@ -439,7 +566,7 @@ __global__ void __launch_bounds__(32 * RG) k_split_fast(const __grid_constant__ 
 //   rows contiguous along l: one warp per row (8 rows per CTA);
 //   rows adjacent for each l (rs == 1): lane = row (32 rows per CTA), the 8 warps split l and
 //   combine through shared memory.
-template <int MODE>
+template <int MODE, bool CRT>
 __device__ __forceinline__ void exps_side(const SplitParams &p, int64_t g, int64_t b) {
     constexpr bool CPLX = (MODE != SPLIT_REAL);
     constexpr int NX = (MODE == SPLIT_3M) ? 3 : 1;
@@ -471,7 +598,7 @@ __device__ __forceinline__ void exps_side(const SplitParams &p, int64_t g, int64
 #pragma unroll
         for (int x = 0; x < NX; ++x) {
             const bool nf = m[x] >= kExpInf;
-            const int32_t e = nf ? kNonFinite : exponent_from_maxbits(m[x]);
+            const int32_t e = nf ? kNonFinite : (CRT ? crt_exponent(m[x], p.crt.nu) : exponent_from_maxbits(m[x]));
             int32_t *ex = p.exps + (MODE == SPLIT_3M ? x * p.x_exps : 0) + b * p.rows_out;
             if (MODE == SPLIT_B4M) {
                 ex[2 * r] = e;
@@ -527,13 +654,13 @@ __device__ __forceinline__ void exps_side(const SplitParams &p, int64_t g, int64
 // One CTA per row group of one side (blockIdx.z) and batch entry (blockIdx.y): 8 rows (rows
 // contiguous along l) or 32 rows (rows adjacent for each l).  (A persistent form over both
 // sides' groups measured slower: the long 32-row groups then run on few CTAs.)
-template <int MA, int MB>
+template <int MA, int MB, bool CRT = false>
 __global__ void __launch_bounds__(256) k_split_exps(const __grid_constant__ SplitPair pp) {
     const SplitParams &q = pp.side[blockIdx.z];
     const int64_t gsz = (q.rs == 1) ? 32 : 8;
     if ((int64_t)blockIdx.x * gsz >= q.rows) return;
-    if (blockIdx.z == 0) exps_side<MA>(q, blockIdx.x, blockIdx.y);
-    else exps_side<MB>(q, blockIdx.x, blockIdx.y);
+    if (blockIdx.z == 0) exps_side<MA, CRT>(q, blockIdx.x, blockIdx.y);
+    else exps_side<MB, CRT>(q, blockIdx.x, blockIdx.y);
 }
 
 }  // namespace ozk
