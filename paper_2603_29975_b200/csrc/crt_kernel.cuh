@@ -38,19 +38,25 @@ struct CrtParams {
 // at the precision of the result (53 bits, fewer when subnormal).
 template <int L>
 __device__ __forceinline__ double round_scaled(const uint32_t (&mag)[L], int sh) {
+    // leading limb and the two below it, selected without dynamic register indexing
     int top = -1;
+    uint32_t h0 = 0, m1 = 0, m2 = 0;
 #pragma unroll
     for (int l = 0; l < L; ++l)
-        if (mag[l]) top = l;
+        if (mag[l]) {
+            top = l;
+            h0 = mag[l];
+            m1 = l >= 1 ? mag[l >= 1 ? l - 1 : 0] : 0u;
+            m2 = l >= 2 ? mag[l >= 2 ? l - 2 : 0] : 0u;
+        }
     if (top < 0) return 0.0;
     // T = the 64 bits below and including the leading one; sticky = anything lower
-    uint64_t hi = mag[top];
+    uint64_t hi = h0;
     uint64_t T;
     bool sticky = false;
-    const int lz = __clz(mag[top]);
+    const int lz = __clz(h0);
     const int BL = 32 * top + 32 - lz;                       // bit length of mag
     {
-        const uint32_t m1 = top >= 1 ? mag[top - 1] : 0u, m2 = top >= 2 ? mag[top - 2] : 0u;
         const uint64_t w96hi = (hi << 32) | m1;              // bits [32 top - 32, 32 top + 32)
         // T = top 64 bits of (mag[top], m1, m2) left-aligned
         T = lz ? ((w96hi << lz) | ((uint64_t)m2 >> (32 - lz))) : w96hi;
@@ -83,9 +89,12 @@ __device__ __forceinline__ double round_scaled(const uint32_t (&mag)[L], int sh)
 }
 
 // One thread per (row, 4 consecutive columns): 4 lanes share one 16-byte plane
-// chunk, so a warp reads 8 rows x 16 B = 128 contiguous bytes per plane.
-template <int L>
+// chunk, so a warp reads 8 rows x 16 B = 128 contiguous bytes per plane.  The moduli
+// count N is compile-time (L = ceil(N / 4) limbs holds M for the R16 moduli): all N plane
+// words are loaded before any arithmetic, and the sum has no per-modulus branches.
+template <int N>
 __global__ void __launch_bounds__(256) k_crt(const __grid_constant__ CrtParams P) {
+    constexpr int L = (N + 3) / 4;
     const int64_t per_b = P.rows_pad * P.groups * 4;
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t b = blockIdx.y;
@@ -95,8 +104,10 @@ __global__ void __launch_bounds__(256) k_crt(const __grid_constant__ CrtParams P
     const int64_t G = rg / P.rows_pad, row = rg - G * P.rows_pad;
     const int64_t col0 = G * 16 + quad * 4;
     if (row >= P.Mp || col0 >= P.Np) return;
-    const int n = P.n;
     const int8_t *src = P.R + b * P.batch_bytes + (G * P.rows_pad + row) * 16 + quad * 4;
+    uint32_t words[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) words[q] = __ldg(reinterpret_cast<const uint32_t *>(src + (int64_t)q * P.plane_bytes));
     // S_x = sum_q u_q W_q for the 4 elements, 64-bit accumulator per limb
     unsigned long long acc[4][L];
 #pragma unroll
@@ -104,17 +115,15 @@ __global__ void __launch_bounds__(256) k_crt(const __grid_constant__ CrtParams P
 #pragma unroll
         for (int l = 0; l < L; ++l) acc[x][l] = 0;
 #pragma unroll
-    for (int q = 0; q < kMaxModuli; ++q) {
-        if (q < n) {
-            const uint32_t word = __ldg(reinterpret_cast<const uint32_t *>(src + (int64_t)q * P.plane_bytes));
-            const uint32_t p = P.p[q];
+    for (int q = 0; q < N; ++q) {
+        const uint32_t word = words[q];
+        const uint32_t p = P.p[q];
 #pragma unroll
-            for (int x = 0; x < 4; ++x) {
-                const int32_t zc = (int32_t)(int8_t)(word >> (8 * x));
-                const uint32_t u = (uint32_t)(zc < 0 ? zc + (int32_t)p : zc);
+        for (int x = 0; x < 4; ++x) {
+            const int32_t zc = (int32_t)(int8_t)(word >> (8 * x));
+            const uint32_t u = (uint32_t)zc + (p & (uint32_t)(zc >> 31));   // centred -> [0, p)
 #pragma unroll
-                for (int l = 0; l < L; ++l) acc[x][l] += (unsigned long long)u * P.W[q][l];
-            }
+            for (int l = 0; l < L; ++l) acc[x][l] += (unsigned long long)u * P.W[q][l];
         }
     }
     const int32_t e = __ldg(P.ea + b * P.Mp + row);

@@ -1402,12 +1402,15 @@ int run_crt(const Call &c, DevState *dev, cudaStream_t st) {
         dim3 grid((unsigned)((rows_pad * groups * 4 + 255) / 256), (unsigned)c.batch);
         {
             ProfScope ps(st, PH_OTHER);
-            switch (h.L) {
-                case 1: k_crt<1><<<grid, 256, 0, st>>>(Q); break;
-                case 2: k_crt<2><<<grid, 256, 0, st>>>(Q); break;
-                case 3: k_crt<3><<<grid, 256, 0, st>>>(Q); break;
-                case 4: k_crt<4><<<grid, 256, 0, st>>>(Q); break;
-                default: k_crt<5><<<grid, 256, 0, st>>>(Q); break;
+            if (h.L != (n + 3) / 4)   // k_crt<N> holds M in ceil(N / 4) limbs (true for the R16 moduli)
+                return fail(OZAKI_ERR_UNSUPPORTED, "Ozaki-II: M needs %d limbs for %d moduli", h.L, n);
+            switch (n) {
+#define OZK_CRT_N(N) case N: k_crt<N><<<grid, 256, 0, st>>>(Q); break;
+                OZK_CRT_N(1) OZK_CRT_N(2) OZK_CRT_N(3) OZK_CRT_N(4) OZK_CRT_N(5) OZK_CRT_N(6) OZK_CRT_N(7)
+                OZK_CRT_N(8) OZK_CRT_N(9) OZK_CRT_N(10) OZK_CRT_N(11) OZK_CRT_N(12) OZK_CRT_N(13)
+                OZK_CRT_N(14) OZK_CRT_N(15) OZK_CRT_N(16) OZK_CRT_N(17) OZK_CRT_N(18) OZK_CRT_N(19)
+                default: k_crt<20><<<grid, 256, 0, st>>>(Q); break;
+#undef OZK_CRT_N
             }
         }
         cudaError_t e = cudaGetLastError();
