@@ -21,13 +21,14 @@ constexpr int kMaxModuli = 20;   // M < 2^160: five 32-bit limbs (CRT kernel)
 //   c21    2^21 mod p,  c42 = 2^42 mod p,  c16 = 2^16 mod p
 //   bias28 multiple of p >= 2^28 (makes a folded sum non-negative)
 //   bias23 multiple of p >= 2^23
-//   m40    ceil(2^40 / p): floor(x m40 / 2^40) = floor(x / p) for 0 <= x < 2^31
+//   m39    ceil(2^39 / p), 32 bits for p > 128 (and 2^31 for p = 256): m39 p - 2^39 < 2^8, so
+//          floor(x m39 / 2^39) = floor(x / p) for 0 <= x < 2^31 (Granlund-Montgomery)
 struct CrtTab {
     int32_t n;        // moduli count
     int32_t nu;       // R17 quantisation bits
     uint32_t p[kMaxModuli], c21[kMaxModuli], c42[kMaxModuli], c16[kMaxModuli];
     uint32_t bias28[kMaxModuli], bias23[kMaxModuli];
-    unsigned long long m40[kMaxModuli];
+    uint32_t m39[kMaxModuli];   // ceil(2^39 / p) < 2^32: floor(x / p) = umulhi(x, m39) >> 7 for x < 2^31
 };
 
 // R17 exponent of a row / column from the bit pattern u of max|x| (finite):
@@ -51,9 +52,9 @@ __device__ __forceinline__ int32_t crt_exponent(uint64_t u, int nu) {
     return e;
 }
 
-// x mod p in [0, p) for 0 <= x < 2^31
-__device__ __forceinline__ uint32_t mod_small(uint32_t x, uint32_t p, unsigned long long m40) {
-    const uint32_t q = (uint32_t)(((unsigned long long)x * m40) >> 40);
+// x mod p in [0, p) for 0 <= x < 2^31 (m39 = ceil(2^39 / p))
+__device__ __forceinline__ uint32_t mod_small(uint32_t x, uint32_t p, uint32_t m39) {
+    const uint32_t q = __umulhi(x, m39) >> 7;
     return x - q * p;
 }
 
@@ -62,7 +63,7 @@ __device__ __forceinline__ uint32_t mod_small(uint32_t x, uint32_t p, unsigned l
 // folded to q2 c42 + q1 c21 + q0 + bias28 in [0, 2^31).
 __device__ __forceinline__ uint32_t residue_u(int32_t q2, uint32_t q1, uint32_t q0, const CrtTab &t, int i) {
     const uint32_t x = (uint32_t)(q2 * (int32_t)t.c42[i]) + q1 * t.c21[i] + q0 + t.bias28[i];
-    return mod_small(x, t.p[i], t.m40[i]);
+    return mod_small(x, t.p[i], t.m39[i]);
 }
 
 // centred representative (even p: [-p/2, p/2-1], odd p: symmetric) as a byte
@@ -74,7 +75,7 @@ __device__ __forceinline__ uint32_t centre_byte(uint32_t r, uint32_t p) {
 // v = vh 2^16 + vl with |vh| < 2^15: folded to vh c16 + vl + bias23 in [0, 2^25).
 __device__ __forceinline__ uint32_t residue_of_i32(int32_t v, const CrtTab &t, int i) {
     const uint32_t x = (uint32_t)((v >> 16) * (int32_t)t.c16[i]) + (uint32_t)(v & 0xffff) + t.bias23[i];
-    return centre_byte(mod_small(x, t.p[i], t.m40[i]), t.p[i]);
+    return centre_byte(mod_small(x, t.p[i], t.m39[i]), t.p[i]);
 }
 
 // 8 x 8 byte transpose of 8 words of 4 residue bytes each (values i, moduli

@@ -1147,7 +1147,7 @@ const CrtHost &crt_tables(int n) {
         h.tab.c16[q] = (uint32_t)((1ull << 16) % p);
         h.tab.bias28[q] = (uint32_t)(((1ull << 28) + p - 1) / p * p);
         h.tab.bias23[q] = (uint32_t)(((1ull << 23) + p - 1) / p * p);
-        h.tab.m40[q] = ((1ull << 40) + p - 1) / p;
+        h.tab.m39[q] = (uint32_t)(((1ull << 39) + p - 1) / p);
     }
     h.ready = true;
     return h;

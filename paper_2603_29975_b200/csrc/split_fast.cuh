@@ -194,7 +194,7 @@ struct FastResidues {
     __device__ __forceinline__ static uint32_t cres(int32_t q2, uint32_t q1, uint32_t q0, const CrtTab &t, int q) {
         const uint32_t x = (uint32_t)(q2 * (int32_t)t.c42[q]) + q1 * t.c21[q] + q0 + t.bias28[q];
         const uint32_t h = t.p[q] >> 1;
-        const uint32_t tq = (uint32_t)(((unsigned long long)(x + h) * t.m40[q]) >> 40);
+        const uint32_t tq = __umulhi(x + h, t.m39[q]) >> 7;   // floor((x + h) / p), x + h < 2^31
         return x - tq * t.p[q];   // low byte = the centred residue (two's complement)
     }
     // per-byte negation of 4 packed two's-complement bytes (-(-128) wraps to -128 = the centred
