@@ -164,8 +164,10 @@ def run_config(args):
     pairs = s * (s + 1) // 2
     per_launch_units = (nb if cfg["shard"] == "batch" else 1)
     if cfg["shard"] == "columns":
-        j0, j1 = zd.column_slab(n, rank, world)
-        frac_cols = (j1 - j0) / n
+        # per GEMM launch: this rank's owned columns are computed in one launch per non-empty
+        # chunk block (dist.sharded_gemm_columns, 4 chunks) -- average columns per launch / n
+        own = [b - a for a, b in zd.column_blocks(n, rank, world, 4)[1] if b > a] if world > 1 else [n]
+        frac_cols = (sum(own) / max(1, len(own))) / n
     else:
         frac_cols = 1.0
     alg_ops = 2 * pairs * (4 if cplx else 1) * m * n * k * per_launch_units * frac_cols

@@ -29,12 +29,28 @@ def batch_shard(total: int, rank: int, world: int) -> tuple[int, int]:
 
 
 def column_slab(n: int, rank: int, world: int, align: int = TILE_N) -> tuple[int, int]:
-    """Column range of C owned by `rank`: equal widths rounded up to `align`
-    (the last slab takes the remainder; trailing ranks may get an empty slab)."""
+    """Column range of C owned by `rank` with one block per rank: equal widths rounded up to
+    `align` (the last slab takes the remainder; trailing ranks may get an empty slab)."""
     width = -(-n // world)
     width = -(-width // align) * align
     j0 = min(n, rank * width)
     return j0, min(n, j0 + width)
+
+
+def column_blocks(n: int, rank: int, world: int, chunks: int = 1, align: int = TILE_N):
+    """Column ownership for the chunked (overlapped) all-gather: the n columns are cut into
+    world * chunks blocks of equal width (rounded up to `align`); block g = c * world + r
+    belongs to rank r, so chunk c = blocks [c * world, (c + 1) * world) is one contiguous
+    column range in which rank r's block sits at offset r * width.  Returns (width,
+    [(j0, j1) for each chunk c]) -- empty blocks have j0 == j1.  chunks = 1 is column_slab."""
+    nb = world * chunks
+    width = -(-n // nb)
+    width = -(-width // align) * align
+    blocks = []
+    for c in range(chunks):
+        j0 = min(n, (c * world + rank) * width)
+        blocks.append((j0, min(n, j0 + width)))
+    return width, blocks
 
 
 def max_over_ranks(value: float, device=None) -> float:
@@ -46,29 +62,53 @@ def max_over_ranks(value: float, device=None) -> float:
     return float(t.item())
 
 
-def sharded_gemm_columns(gemm, A, B, C, rank: int, world: int, device=None):
-    """C = op(A) B column-sharded: `gemm(A, B_slab, C_slab)` computes this rank's
-    slab in place, then an all-gather of the (column-major, contiguous) slabs
-    fills all of C on every rank.  A: m x k, B: k x n, C: m x n column-major
-    tensors (stride(0) == 1) on `device`.  Returns C."""
+def sharded_gemm_columns(gemm, A, B, C, rank: int, world: int, device=None, chunks: int = 4):
+    """C = op(A) B column-sharded with the all-gather overlapped with the GEMM (SURVEY.md
+    §8(e)): rank r computes its block of every chunk c (`gemm(A, B_block, C_block)` in place,
+    column_blocks), and after each chunk's GEMM an asynchronous all-gather of that chunk runs
+    on the communicator's stream while the next chunk's GEMM runs on the compute stream.
+    Chunk c's blocks are adjacent in column-major C, so with NCCL the gather is in place
+    (input = this rank's block inside the output range, no staging copies); ragged last
+    chunks and other backends go through padded staging buffers.  A: m x k, B: k x n,
+    C: m x n column-major tensors (stride(0) == 1) on `device`.  Every element is computed
+    exactly as on one GPU (per-row / per-column exponents), so the gathered C is bitwise the
+    single-GPU C.  Returns C."""
     m, n = C.shape
-    j0, j1 = column_slab(n, rank, world)
-    width = column_slab(n, 0, world)[1] - column_slab(n, 0, world)[0]
-    if j1 > j0:
-        gemm(A, B[:, j0:j1], C[:, j0:j1])
     if world == 1:
+        gemm(A, B, C)
         return C
-    # every rank contributes a padded slab of `width` columns (column-major, contiguous)
-    send = torch.zeros((width, m), dtype=C.dtype, device=C.device)
-    if j1 > j0:
-        send[: j1 - j0].copy_(C[:, j0:j1].t())
-    recv = torch.empty((world * width, m), dtype=C.dtype, device=C.device)
-    if hasattr(dist, "all_gather_into_tensor") and dist.get_backend() == "nccl":
-        dist.all_gather_into_tensor(recv, send)
-    else:
-        dist.all_gather(list(recv.chunk(world)), send)
-    for r in range(world):
-        a, b = column_slab(n, r, world)
-        if b > a:
-            C[:, a:b].copy_(recv[r * width: r * width + (b - a)].t())
+    width, blocks = column_blocks(n, rank, world, chunks)
+    nccl = dist.get_backend() == "nccl" and hasattr(dist, "all_gather_into_tensor")
+    flat = C.t().view(-1) if (C.stride(0) == 1 and C.stride(1) == m) else None
+    works = []
+    for c, (j0, j1) in enumerate(blocks):
+        c0 = c * world * width                        # first column of chunk c
+        if c0 >= n:
+            break
+        if j1 > j0:
+            gemm(A, B[:, j0:j1], C[:, j0:j1])
+        full = c0 + world * width <= n                # every rank's block of this chunk is full width
+        if nccl and full and flat is not None:
+            out = flat[c0 * m:(c0 + world * width) * m]
+            inp = out[rank * width * m:(rank + 1) * width * m]
+            works.append(dist.all_gather_into_tensor(out, inp, async_op=True))
+            continue
+        # staging path: padded blocks (ragged chunk, non-NCCL backend or strided C)
+        send = torch.zeros((width, m), dtype=C.dtype, device=C.device)
+        if j1 > j0:
+            send[: j1 - j0].copy_(C[:, j0:j1].t())
+        recv = torch.empty((world * width, m), dtype=C.dtype, device=C.device)
+        if nccl:
+            dist.all_gather_into_tensor(recv, send)
+        else:   # gloo (CPU tests, the 2-ranks-on-one-GPU hook): gather through host memory
+            rh = torch.empty((world * width, m), dtype=C.dtype)
+            dist.all_gather(list(rh.chunk(world)), send.cpu())
+            recv.copy_(rh)
+        for r in range(world):
+            a = min(n, c0 + r * width)
+            b = min(n, a + width)
+            if b > a and r != rank:
+                C[:, a:b].copy_(recv[r * width: r * width + (b - a)].t())
+    for w in works:
+        w.wait()
     return C

@@ -42,10 +42,13 @@ def _worker(rank, world, port, q):
         def gemm(At, Bt, Ct):   # oracle as the local GEMM: Ct = op(A) op(B)
             Ct.copy_(torch.from_numpy(oracle.dgemm("N", "N", 1.0, At.numpy(), Bt.numpy(), 0.0, None, s)))
 
-        Ct = torch.zeros((n, m), dtype=torch.float64).t()      # column-major m x n
-        zd.sharded_gemm_columns(gemm, torch.from_numpy(A), torch.from_numpy(B), Ct, rank, world)
         ref = oracle.dgemm("N", "N", 1.0, A, B, 0.0, None, s)
-        bitexact = bool((Ct.numpy() == ref).all())
+        bitexact = True
+        for chunks in (1, 2, 3):   # one block per rank, and the chunked (overlapped) ownership
+            Ct = torch.zeros((n, m), dtype=torch.float64).t()      # column-major m x n
+            zd.sharded_gemm_columns(gemm, torch.from_numpy(A), torch.from_numpy(B), Ct, rank, world,
+                                    chunks=chunks)
+            bitexact = bitexact and bool((Ct.numpy() == ref).all())
         # batch shards and max-over-ranks
         shards = [zd.batch_shard(30, r, world) for r in range(world)]
         mx = zd.max_over_ranks(float(rank + 1))
@@ -89,3 +92,15 @@ def test_shard_arithmetic():
                 cover[a:b] += 1
                 assert a % zd.TILE_N == 0 or a == n
             assert (cover == 1).all()
+            for chunks in (1, 2, 4):
+                cover = np.zeros(n, int)
+                for r in range(world):
+                    width, bl = zd.column_blocks(n, r, world, chunks)
+                    for c, (a, b) in enumerate(bl):
+                        cover[a:b] += 1
+                        if b > a:   # block g = c * world + r at offset r * width inside chunk c
+                            assert a == (c * world + r) * width and a % zd.TILE_N == 0
+                assert (cover == 1).all()
+                if chunks == 1:
+                    assert all(zd.column_blocks(n, r, world, 1)[1][0] == zd.column_slab(n, r, world)
+                               for r in range(world))
