@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--gamma", type=float, default=3.0)
     ap.add_argument("--no-extras", action="store_true", help="skip sweep / e2e / cpu baseline")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="headline without cross-call overlap (ozaki_set_overlap off)")
     ap.add_argument("--workload", default="c2x30", choices=["c2x30", "c1", "c2", "c3", "c4", "c5"],
                     help="c2x30 (default, the headline) or another BASELINE config (see CONFIGS)")
     return ap.parse_args()
@@ -321,6 +323,9 @@ def run_ours(args):
     def step():
         fn("N", "N", 1.0, A, B, 0.0, C, s)
 
+    # cross-call overlap (ozaki_set_overlap): each step's split starts under the previous step's
+    # GEMM (same results; the bench places nothing between the calls)
+    oz.set_overlap(not args.no_overlap)
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
@@ -398,6 +403,7 @@ def run_ours(args):
             "slices": s, "method": args.method, "m": n, "n": n, "k": n,
             "batch_per_gpu": batch, "global_batch": batch * world,
             "parallelism": f"batch-sharded x{world} (no collective)",
+            "cross_call_overlap": not args.no_overlap,
             "l2": "inputs exceed L2 (%.0f MB per GPU > 126 MB)" % (batch * 3 * n * n * 16 / 1e6),
         },
         "roofline": {

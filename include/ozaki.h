@@ -188,6 +188,22 @@ int ozaki_get_pair_set(void);
 int ozaki_set_exponent_block(int64_t kb);
 int64_t ozaki_get_exponent_block(void);
 
+/* --- cross-call overlap (performance option, thread-local, default 0) ---------
+ * on != 0: consecutive Ozaki-I DGEMM / ZGEMM (4M) calls of this thread on one
+ * stream overlap -- a call's split kernel is launched with programmatic
+ * dependent launch (PDL) right after the previous call's GEMM and fills the SMs
+ * its last wave leaves idle.  When the previous call's C overlaps neither A nor
+ * B, the split reads A / B and writes its slices before that GEMM completes
+ * (the slices alternate between two persistent workspaces owned by the thread
+ * and stream); otherwise it waits.  Each split grid completes only after the
+ * previous GEMM, so results and stream order are unchanged.  Caller's promise:
+ * no kernel launched with PDL that writes the next call's A or B is placed on
+ * the stream between two calls.  on = 0 releases the persistent workspaces.
+ * The host-pointer offload path and 3M, Ozaki-II, K-chunked and debug calls run
+ * as without it.  Returns 0.                                                 */
+int ozaki_set_overlap(int on);
+int ozaki_get_overlap(void);
+
 /* --- streams, stats, errors --------------------------------------------- */
 /* stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
  * thread-local; returns 0.                                                 */

@@ -72,6 +72,10 @@ def lib():
     L.ozaki_zgemm_strided_batched.argtypes = [c, c, i64, i64, i64, dP, p, i64, i64, p, i64, i64,
                                               dP, p, i64, i64, i64, i32]
     L.ozaki_zgemm3m_strided_batched.argtypes = L.ozaki_zgemm_strided_batched.argtypes
+    L.ozaki_set_overlap.argtypes = [i32]
+    L.ozaki_set_overlap.restype = i32
+    L.ozaki_get_overlap.argtypes = []
+    L.ozaki_get_overlap.restype = i32
     L.ozaki_set_exponent_block.argtypes = [i64]
     L.ozaki_set_exponent_block.restype = i32
     L.ozaki_get_exponent_block.argtypes = []
@@ -316,6 +320,15 @@ def set_exponent_block(kb: int) -> None:
 
 def get_exponent_block() -> int:
     return int(lib().ozaki_get_exponent_block())
+
+
+def set_overlap(on: bool) -> None:
+    """ozaki_set_overlap: overlap consecutive Ozaki-I calls on one stream (include/ozaki.h)."""
+    _check(lib().ozaki_set_overlap(1 if on else 0), "ozaki_set_overlap")
+
+
+def get_overlap() -> bool:
+    return bool(lib().ozaki_get_overlap())
 
 
 def set_stream(stream) -> None:

@@ -156,6 +156,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     // Programmatic dependent launch: the prologue above overlaps the producer kernel's tail
     // (K1); everything below reads its output (slices, exponents), so wait for its completion.
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    // ... and let a dependent launched with PDL (the next call's split, ozaki_set_overlap) start
+    // on the SMs this grid's last wave leaves idle; it orders itself after this grid (split_fast.cuh)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (warp == 0) {
         // ========================= producer (both CTAs): own A rows, own B half

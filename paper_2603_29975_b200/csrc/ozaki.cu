@@ -37,6 +37,31 @@ thread_local cudaStream_t t_stream = nullptr;
 thread_local std::string t_err;
 thread_local int t_full_pairs = 0;   // R21 pair set for Ozaki-I calls (ozaki_set_pair_set)
 thread_local int64_t t_kblock = 0;    // R22 exponent block along K (0 = per row / column)
+thread_local int t_overlap = 0;       // cross-call split / GEMM overlap (ozaki_set_overlap)
+
+// Cross-call overlap state per (thread, stream, device): two persistent slice workspaces used
+// alternately, and whether the last kernel this thread put on the stream is an Ozaki-I GEMM
+// (which triggers programmatic dependents at its start) together with the bytes it writes (C).
+struct OvState {
+    cudaStream_t st = nullptr;
+    int dev = -1;
+    void *ws[2] = {nullptr, nullptr};
+    size_t cap[2] = {0, 0};
+    int next = 0;
+    bool last_gemm = false;
+    uintptr_t c_lo = 0, c_hi = 0;
+};
+thread_local std::vector<OvState> t_ov;
+OvState &ov_state(cudaStream_t st) {
+    int d = 0;
+    cudaGetDevice(&d);
+    for (auto &o : t_ov)
+        if (o.st == st && o.dev == d) return o;
+    t_ov.emplace_back();
+    t_ov.back().st = st;
+    t_ov.back().dev = d;
+    return t_ov.back();
+}
 
 struct Stats {
     std::atomic<uint64_t> dgemm{0}, zgemm{0}, zgemm3m{0}, entries{0}, equiv{0}, macs{0},
@@ -445,10 +470,32 @@ void launch_split_long(dim3 grid, size_t smem, cudaStream_t st, const SplitPair 
                              (int)smem);
         attr = smem;
     }
-    k_split_fast<S, MA, MB, R, true><<<grid, 32 * R, smem, st>>>(pp, KW, nwin);
+    k_split_fast<S, MA, MB, R, true><<<grid, 32 * R, smem, st>>>(pp, KW, nwin, 0);
 }
 
+// cudaLaunchKernelEx with programmatic stream serialisation when `pdl` (cross-call overlap)
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+                Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+// Cross-call overlap request for the next split launch (set by run() for ozaki_set_overlap):
+// pdl = launch with PDL after the previous call's GEMM; early = may read / write before it ends.
+thread_local bool t_split_pdl = false, t_split_early = false;
+
 int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b, dim3 grid, cudaStream_t st) {
+    const bool pdl = t_split_pdl, early = t_split_early;
     if (!b || !P.pair || P.s < 1 || P.s > 12) return 1;
     if (a.tile_h != 128 || b->tile_h != 64) return 1;
     if (a.kbs_bytes != (int64_t)P.s * 128 * 32 || b->kbs_bytes != (int64_t)P.s * 64 * 32) return 1;
@@ -502,7 +549,8 @@ int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
                 attr = smem;                                                                         \
             }                                                                                        \
-            k_split_fast<S, MA, MB, R><<<grid, 32 * R, smem, st>>>(pp, KW, nwin);                    \
+            launch_pdl(k_split_fast<S, MA, MB, R>, grid, dim3(32 * R), smem, st, pdl, pp, KW, nwin,   \
+                       early ? 1 : 0);                                                               \
         }
 #define OZK_FAST_LONG(S, MA, MB) launch_split_long<S, MA, MB>(grid, smem, st, pp, KW, nwin);
 #define OZK_FAST(S, MA, MB)                                                                          \
@@ -1041,7 +1089,10 @@ int run_offload(const Call &c) {
         d.batch = nb;
         d.batched = true;
         t_stream = o->comp;
+        const int ovs = t_overlap;
+        t_overlap = 0;   // chunks are separated by event waits on the staging copies
         rc = run(d);
+        t_overlap = ovs;
         t_stream = user;
         if (rc) break;
         CUDA_TRY(cudaEventRecord(o->comp_done[set], o->comp));
@@ -1177,7 +1228,7 @@ void launch_crt_fast(bool real, bool lng, dim3 grid, size_t smem, cudaStream_t s
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
             attr = smem;                                                                             \
         }                                                                                            \
-        k_split_fast<NMX, MA, MB, R, L, true><<<grid, 32 * R, smem, st>>>(pp, KW, nwin);             \
+        k_split_fast<NMX, MA, MB, R, L, true><<<grid, 32 * R, smem, st>>>(pp, KW, nwin, 0);          \
     }
     if (real) {
         if (lng) OZK_CRT_K(SPLIT_REAL, SPLIT_REAL, 16, true) else OZK_CRT_K(SPLIT_REAL, SPLIT_REAL, 4, false)
@@ -1455,6 +1506,12 @@ int run(const Call &c0) {
     const size_t es = (c.kind == KIND_REAL) ? 8 : 16;
     const bool cplx = c.kind != KIND_REAL;
     const bool alpha0 = c.al[0] == 0.0 && c.al[1] == 0.0;
+    // cross-call overlap: whatever this call launches, the stream's last kernel is no longer a
+    // tracked GEMM unless the overlapped main path below sets it again
+    OvState *ov = t_overlap ? &ov_state(st) : nullptr;
+    const bool prev_gemm = ov && ov->last_gemm;
+    const uintptr_t pc_lo = ov ? ov->c_lo : 0, pc_hi = ov ? ov->c_hi : 0;
+    if (ov) ov->last_gemm = false;
     const bool beta1 = c.be[0] == 1.0 && c.be[1] == 0.0;
 
     // C must not alias A or B (only checked when A/B are read)
@@ -1534,8 +1591,25 @@ int run(const Call &c0) {
     if (c.kind == KIND_3M) t_bytes = al256(sizeof(double) * c.m * c.n * c.batch);
     ws += 3 * t_bytes;
 
+    // cross-call overlap (ozaki_set_overlap): one split + one GEMM launch, slices in the
+    // alternate persistent workspace; the split may start under the previous call's GEMM
+    // (PDL), and may read / write before that GEMM ends when its C overlaps neither operand
+    const bool ovl = ov && (c.kind == KIND_REAL || c.kind == KIND_4M) && !c.S_out && !P.kchunk_needed;
+    int ov_slot = 0;
     void *base = nullptr;
-    {
+    if (ovl) {
+        ov_slot = ov->next;
+        if (ov->cap[ov_slot] < ws) {   // grow (rare): the buffer may still be read by a GEMM in flight
+            CUDA_TRY(cudaStreamSynchronize(st));
+            if (ov->ws[ov_slot]) cudaFree(ov->ws[ov_slot]);
+            ov->ws[ov_slot] = nullptr;
+            ov->cap[ov_slot] = 0;
+            cudaError_t e = cudaMalloc(&ov->ws[ov_slot], ws);
+            if (e != cudaSuccess) return fail(OZAKI_ERR_ALLOC, "overlap workspace (%zu B): %s", ws, cudaGetErrorString(e));
+            ov->cap[ov_slot] = ws;
+        }
+        base = ov->ws[ov_slot];
+    } else {
         cudaError_t e = cudaMallocAsync(&base, ws, st);
         if (e != cudaSuccess) return fail(OZAKI_ERR_ALLOC, "cudaMallocAsync(%zu): %s", ws, cudaGetErrorString(e));
     }
@@ -1549,8 +1623,17 @@ int run(const Call &c0) {
     if (c.kind == KIND_REAL || c.kind == KIND_4M) {
         const int ma = (c.kind == KIND_4M) ? SPLIT_A4M : SPLIT_REAL;
         const int mb = (c.kind == KIND_4M) ? SPLIT_B4M : SPLIT_REAL;
+        if (ovl && prev_gemm) {
+            const int64_t ar = c.ta == 'N' ? c.m : c.k, ac = c.ta == 'N' ? c.k : c.m;
+            const int64_t br = c.tb == 'N' ? c.k : c.n, bc = c.tb == 'N' ? c.n : c.k;
+            const uintptr_t a0 = (uintptr_t)c.A, a1 = a0 + span_bytes(ar, ac, c.lda, c.sA, c.batch, es);
+            const uintptr_t b0 = (uintptr_t)c.B, b1 = b0 + span_bytes(br, bc, c.ldb, c.sB, c.batch, es);
+            t_split_pdl = true;
+            t_split_early = (a1 <= pc_lo || a0 >= pc_hi) && (b1 <= pc_lo || b0 >= pc_hi);
+        }
         rc = launch_split_ab(P, view_A(c.A, c.ta, c.m, c.k, c.lda, c.sA, ma), sa, ea,
                              view_B(c.B, c.tb, c.n, c.k, c.ldb, c.sB, mb), sb, fb, dev, st);
+        t_split_pdl = t_split_early = false;
         if (!rc) {
             const int epi = c.S_out ? EPI_LEVELS : (c.kind == KIND_4M ? EPI_CPLX4M : EPI_REAL);
             rc = launch_gemm(P, epi, sa, sb, ea, fb, c.C, c.ldc, c.sC, c.al, c.be, c.S_out, dev, st);
@@ -1572,7 +1655,16 @@ int run(const Call &c0) {
             g_stats.launches += 1;
         }
     }
-    cudaFreeAsync(base, st);
+    if (ovl) {
+        if (!rc) {
+            ov->next = ov_slot ^ 1;
+            ov->last_gemm = true;
+            ov->c_lo = (uintptr_t)c.C;
+            ov->c_hi = ov->c_lo + span_bytes(c.m, c.n, c.ldc, c.sC, c.batch, es);
+        }
+    } else {
+        cudaFreeAsync(base, st);
+    }
     if (rc) return rc;
 
     const uint64_t pr = c.full ? (uint64_t)c.s * c.s : (uint64_t)c.s * (c.s + 1) / 2;
@@ -1724,6 +1816,24 @@ int ozaki_set_exponent_block(int64_t kb) {
 }
 
 int64_t ozaki_get_exponent_block(void) { return t_kblock; }
+
+int ozaki_set_overlap(int on) {
+    t_overlap = on ? 1 : 0;
+    if (!on) {   // release the persistent workspaces of this thread (after their GEMMs finish)
+        for (auto &o : t_ov) {
+            int d = 0;
+            cudaGetDevice(&d);
+            if (o.dev != d) continue;
+            cudaStreamSynchronize(o.st);
+            for (int i = 0; i < 2; ++i)
+                if (o.ws[i]) cudaFree(o.ws[i]);
+        }
+        t_ov.clear();
+    }
+    return 0;
+}
+
+int ozaki_get_overlap(void) { return t_overlap; }
 
 int ozaki_set_pair_set(int full) {
     t_full_pairs = full ? 1 : 0;

@@ -546,19 +546,29 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
 
 // Both operands of one product in ONE launch (blockIdx.z = side), A rows in 128-row tiles,
 // B rows in 64-row halves (the CTA-pair GEMM's layout).
+//
+// Cross-call overlap (ozaki_set_overlap): the kernel may be launched with programmatic dependent
+// launch right after the previous call's GEMM, which triggers its dependents at its start, so
+// these CTAs fill the SMs the GEMM's last wave leaves idle.  `early` (host-decided: the previous
+// GEMM's C overlaps neither operand; the slice workspace alternates between two buffers) lets
+// the CTA read its operands and write its slices before the previous GEMM has finished;
+// otherwise it waits first.  Every CTA waits before exiting, so this grid completes only after
+// the previous GEMM -- the next GEMM's own griddepcontrol.wait then orders it after both.
+// Without the launch attribute both waits are no-ops.
 template <int S, int MA, int MB, int RG, bool LONG = false, bool CRT = false>
 __global__ void __launch_bounds__(32 * RG) k_split_fast(const __grid_constant__ SplitPair pp, int KW,
-                                                         int nwin) {
+                                                         int nwin, int early) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (!early) asm volatile("griddepcontrol.wait;" ::: "memory");
     extern __shared__ __align__(16) uint8_t sbuf[];
     const int64_t rg = LONG ? (int64_t)blockIdx.x / nwin : (int64_t)blockIdx.x;
     if (blockIdx.z == 0) {
-        if (rg * RG >= pp.side[0].rows_grid) return;
-        split_fast_side<S, MA, 128, RG, LONG, CRT>(pp.side[0], KW, sbuf);
+        if (rg * RG < pp.side[0].rows_grid) split_fast_side<S, MA, 128, RG, LONG, CRT>(pp.side[0], KW, sbuf);
     } else {
-        if (rg * RG >= pp.side[1].rows_grid) return;
-        split_fast_side<S, MB, CRT ? 128 : 64, RG, LONG, CRT>(pp.side[1], KW, sbuf);
+        if (rg * RG < pp.side[1].rows_grid)
+            split_fast_side<S, MB, CRT ? 128 : 64, RG, LONG, CRT>(pp.side[1], KW, sbuf);
     }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // R3 exponents of long rows (the LONG split's first kernel): exact 64-bit max of |x| per row
