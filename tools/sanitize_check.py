@@ -31,5 +31,25 @@ oz.set_pair_set("triangular")
 oz.set_exponent_block(32)
 oz.zgemm("N", "N", 1.0, dev(Z), dev(W), 0.0, Zc, 6)
 oz.set_exponent_block(0)
+# round-1 additions: long-row split (exponent kernel + per-window digits), s = 9..12 fast split,
+# Ozaki-II through the fast split (both operands, conj), cross-call overlap (PDL split after GEMM)
+os.environ["OZAKI_SPLIT_LONG"] = "1"
+oz.dgemm("N", "N", 1.0, dev(synth.uniform(90, 700, seed=7)), dev(synth.uniform(700, 60, seed=8)), 0.0,
+         dev(np.zeros((90, 60))), 7)
+oz.zgemm("N", "C", 1.0, dev(synth.kkr(40, 600, seed=9)), dev(synth.kkr(50, 600, seed=10)), 0.0,
+         dev(np.zeros((40, 50), np.complex128)), 6)
+oz.ozaki2_dgemm("T", "N", 1.0, dev(synth.uniform(700, 50, seed=11)), dev(synth.uniform(700, 40, seed=12)), 0.0,
+                dev(np.zeros((50, 40))), 10)
+del os.environ["OZAKI_SPLIT_LONG"]
+oz.dgemm("N", "N", 1.0, dev(A), dev(synth.uniform(70, 150, seed=13)), 0.0, C, 11)
+oz.ozaki2_zgemm("C", "N", 1.0, dev(np.conj(Z.T).copy()), dev(W), 0.0, Zc, 16)
+oz.set_overlap(True)
+Zd, Wd = dev(Z), dev(W)
+for _ in range(3):
+    oz.zgemm("N", "N", 1.0, Zd, Wd, 0.0, Zc, 7)
+Cd = dev(np.zeros((200, 150)))
+oz.dgemm("N", "N", 1.0, dev(A), dev(synth.uniform(70, 150, seed=14)), 0.0, Cd, 7)
+oz.dgemm("N", "N", 1.0, Cd, dev(synth.uniform(150, 150, seed=15)), 0.0, C, 7)
+oz.set_overlap(False)
 torch.cuda.synchronize()
 print("sanitize_check done")
