@@ -490,6 +490,55 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
     cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// Long-row split, first kernel: K-chunked exponent scan (k_split_exps) into a zeroed buffer of
+// biased per-row exponents ([NX][batch][rows] per side, freed in stream order by the caller).
+// mode: 0 real, 1 4M, 2 3M.  The digit kernel reads it back (split_fast.cuh LONG).
+int launch_exps(SplitPair &pp, unsigned batch, int nx, int mode, bool crt, cudaStream_t st, uint32_t **emax_out) {
+    const size_t na = (size_t)nx * batch * std::max<int64_t>(1, pp.side[0].rows);
+    const size_t nb = (size_t)nx * batch * std::max<int64_t>(1, pp.side[1].rows);
+    uint32_t *emax = nullptr;
+    {
+        cudaError_t e = cudaMallocAsync((void **)&emax, 4 * (na + nb), st);
+        if (e != cudaSuccess) return fail(OZAKI_ERR_ALLOC, "cudaMallocAsync(emax): %s", cudaGetErrorString(e));
+    }
+    CUDA_TRY(cudaMemsetAsync(emax, 0, 4 * (na + nb), st));
+    int64_t ctas = 1;
+    for (int sd = 0; sd < 2; ++sd) {
+        SplitParams &q = pp.side[sd];
+        q.emax = emax + (sd ? na : 0);
+        // split K only as far as needed for ~16 CTAs per SM over the side (few long row groups
+        // are the slow case: C3's 256 groups of 32 adjacent rows); chunks of >= 256 elements
+        static const int sms = [] {
+            int d = 0, v = 148;
+            cudaGetDevice(&d);
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+            return v;
+        }();
+        const int64_t groups = (q.rows + (q.rs == 1 ? 31 : 7)) / (q.rs == 1 ? 32 : 8);
+        const int64_t gb = groups * batch;
+        const int64_t want = gb < 4 * (int64_t)sms ? std::max<int64_t>(1, (16 * (int64_t)sms + gb - 1) / gb) : 1;
+        const int64_t kc = (q.k + want - 1) / want;
+        q.kchunk = (int32_t)std::max<int64_t>(256, (kc + 255) / 256 * 256);
+        ctas = std::max<int64_t>(ctas, groups * ((q.k + q.kchunk - 1) / q.kchunk));
+    }
+    dim3 ge((unsigned)ctas, batch, 2);
+    {
+        ProfScope ps(st, PH_EXP);
+        if (crt) {
+            if (mode == 0) k_split_exps<SPLIT_REAL, SPLIT_REAL, true><<<ge, 256, 0, st>>>(pp);
+            else k_split_exps<SPLIT_A4M, SPLIT_B4M, true><<<ge, 256, 0, st>>>(pp);
+        } else {
+            if (mode == 0) k_split_exps<SPLIT_REAL, SPLIT_REAL><<<ge, 256, 0, st>>>(pp);
+            else if (mode == 1) k_split_exps<SPLIT_A4M, SPLIT_B4M><<<ge, 256, 0, st>>>(pp);
+            else k_split_exps<SPLIT_3M, SPLIT_3M><<<ge, 256, 0, st>>>(pp);
+        }
+    }
+    CUDA_TRY(cudaGetLastError());
+    g_stats.launches += 1;
+    *emax_out = emax;
+    return 0;
+}
+
 // Cross-call overlap request for the next split launch (set by run() for ozaki_set_overlap):
 // pdl = launch with PDL after the previous call's GEMM; early = may read / write before it ends.
 thread_local bool t_split_pdl = false, t_split_early = false;
@@ -528,15 +577,9 @@ int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b,
     SplitPair pp;
     pp.side[0] = a;
     pp.side[1] = *b;
+    uint32_t *emax = nullptr;
     if (lng) {
-        auto ctas = [](const SplitParams &q) { return (q.rows + (q.rs == 1 ? 31 : 7)) / (q.rs == 1 ? 32 : 8); };
-        dim3 ge((unsigned)std::max<int64_t>(1, std::max(ctas(a), ctas(*b))), grid.y, 2);
-        ProfScope ps(st, PH_EXP);
-        if (real) k_split_exps<SPLIT_REAL, SPLIT_REAL><<<ge, 256, 0, st>>>(pp);
-        else if (fourm) k_split_exps<SPLIT_A4M, SPLIT_B4M><<<ge, 256, 0, st>>>(pp);
-        else k_split_exps<SPLIT_3M, SPLIT_3M><<<ge, 256, 0, st>>>(pp);
-        CUDA_TRY(cudaGetLastError());
-        g_stats.launches += 1;
+        if (int rc = launch_exps(pp, grid.y, threem ? 3 : 1, real ? 0 : (fourm ? 1 : 2), false, st, &emax)) return rc;
     }
     const size_t smem = (size_t)RG * (KW + (real ? 2 : 1)) * (real ? 8 : 16);
     {
@@ -571,6 +614,7 @@ int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b,
 #undef OZK_FAST_RG
 #undef OZK_FAST_LONG
     }
+    if (emax) cudaFreeAsync(emax, st);
     CUDA_TRY(cudaGetLastError());
     g_stats.launches += 1;
     return 0;
@@ -1258,14 +1302,9 @@ int launch_split_fast_crt(const SplitParams &a, const SplitParams &b, int64_t ba
     pp.side[0] = a;
     pp.side[1] = b;
     dim3 grid((unsigned)((rows_grid + RG - 1) / RG) * (lng ? nwin : 1), (unsigned)batch, 2);
+    uint32_t *emax = nullptr;
     if (lng) {
-        auto ctas = [](const SplitParams &q) { return (q.rows + (q.rs == 1 ? 31 : 7)) / (q.rs == 1 ? 32 : 8); };
-        dim3 ge((unsigned)std::max<int64_t>(1, std::max(ctas(a), ctas(b))), (unsigned)batch, 2);
-        ProfScope ps(st, PH_EXP);
-        if (real) k_split_exps<SPLIT_REAL, SPLIT_REAL, true><<<ge, 256, 0, st>>>(pp);
-        else k_split_exps<SPLIT_A4M, SPLIT_B4M, true><<<ge, 256, 0, st>>>(pp);
-        CUDA_TRY(cudaGetLastError());
-        g_stats.launches += 1;
+        if (int rc = launch_exps(pp, (unsigned)batch, 1, real ? 0 : 1, true, st, &emax)) return rc;
     }
     const size_t smem = (size_t)RG * (KW + (real ? 2 : 1)) * (real ? 8 : 16);
     {
@@ -1278,6 +1317,7 @@ int launch_split_fast_crt(const SplitParams &a, const SplitParams &b, int64_t ba
             default: launch_crt_fast<20>(real, lng, grid, smem, st, pp, KW, nwin); break;
         }
     }
+    if (emax) cudaFreeAsync(emax, st);
     CUDA_TRY(cudaGetLastError());
     g_stats.launches += 1;
     return 0;

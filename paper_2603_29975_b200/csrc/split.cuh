@@ -58,6 +58,8 @@ struct SplitParams {
     int64_t ss_bytes;     // bytes between slices / moduli  (Ozaki-I: blk;  Ozaki-II: KB*blk)
     int64_t x_bytes;      // SPLIT_3M: bytes between the Re / Im / Sum slice regions
     int64_t x_exps;       // SPLIT_3M: exponents between the three regions
+    uint32_t *emax;       // long-row split: per-row biased exponents [NX][batch][rows] (atomicMax)
+    int32_t kchunk;       // long-row split: depth per k_split_exps CTA
     CrtTab crt;           // Ozaki-II constants (CRT instantiation only)
 };
 

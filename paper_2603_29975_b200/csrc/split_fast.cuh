@@ -46,6 +46,8 @@ __device__ __forceinline__ bool exponent_from_hi_crt(uint32_t H, int nu, int32_t
     return true;
 }
 
+constexpr int32_t kExpBiasDef = 4096;   // long-row split: exponents stored as e + 4096 > 0
+
 __device__ __forceinline__ uint32_t hi_abs(double x) {
     return (uint32_t)__double2hiint(x) & 0x7fffffffu;
 }
@@ -359,13 +361,23 @@ __device__ __forceinline__ void split_fast_side(const SplitParams &p, int KW, ui
     };
 
     // ---------------- pass 1: exponents (warp = row)
-    if constexpr (LONG) {   // from k_split_exps
+    if constexpr (LONG) {   // from k_split_exps: biased per-row exponents (0: zero row, ~0u: Inf / NaN)
         if (tid < RG * NX) {
             const int x = tid / RG, rw = tid % RG;
             int32_t e = 0;
             if (rw < nrows) {
-                const int32_t *ex = p.exps + (MODE == SPLIT_3M ? x * p.x_exps : 0) + b * p.rows_out;
-                e = ex[MODE == SPLIT_B4M ? 2 * (r0 + rw) : r0 + rw];
+                const uint32_t v = p.emax[((int64_t)x * gridDim.y + b) * p.rows + r0 + rw];
+                e = (v == 0u) ? 0 : (v == 0xffffffffu ? kNonFinite : (int32_t)v - kExpBiasDef);
+                if (wbeg == 0) {   // one CTA per row group publishes the exponents (R3 / R17)
+                    int32_t *ex = p.exps + (MODE == SPLIT_3M ? x * p.x_exps : 0) + b * p.rows_out;
+                    if (MODE == SPLIT_B4M) {
+                        ex[2 * (r0 + rw)] = e;
+                        ex[2 * (r0 + rw) + 1] = e;
+                    } else {
+                        ex[r0 + rw] = e;
+                    }
+                    if (e == kNonFinite) atomicAdd(p.nonfinite, 1ull);
+                }
             }
             s_e[x][rw] = e;
             const int sh = P - e;
@@ -571,13 +583,17 @@ __global__ void __launch_bounds__(32 * RG) k_split_fast(const __grid_constant__ 
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
-// R3 exponents of long rows (the LONG split's first kernel): exact 64-bit max of |x| per row
-// (NX maxima for SPLIT_3M: Re, Im', fl(Re + Im')), streamed from HBM once.
+// R3 / R17 exponents of long rows (the LONG split's first kernel), split along K: each CTA
+// takes a group of rows and a K chunk of p.kchunk, forms the exact 64-bit max |x| of its part of
+// each row (NX maxima for SPLIT_3M: Re, Im', fl(Re + Im')) and folds the chunk's exponent into
+// p.emax with atomicMax.  The exponent rule is monotone in the max, so the max over chunks of
+// the chunk exponents is the exponent of the row max; zero chunks contribute nothing (the
+// buffer starts at 0), Inf / NaN chunks contribute ~0u.  Values are e + kExpBias > 0.
 //   rows contiguous along l: one warp per row (8 rows per CTA);
 //   rows adjacent for each l (rs == 1): lane = row (32 rows per CTA), the 8 warps split l and
 //   combine through shared memory.
 template <int MODE, bool CRT>
-__device__ __forceinline__ void exps_side(const SplitParams &p, int64_t g, int64_t b) {
+__device__ __forceinline__ void exps_side(const SplitParams &p, int64_t g, int64_t kc, int64_t b) {
     constexpr bool CPLX = (MODE != SPLIT_REAL);
     constexpr int NX = (MODE == SPLIT_3M) ? 3 : 1;
     using Elem = typename std::conditional<CPLX, double2, double>::type;
@@ -585,6 +601,7 @@ __device__ __forceinline__ void exps_side(const SplitParams &p, int64_t g, int64
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const Elem *X = reinterpret_cast<const Elem *>(p.X) + b * p.bstride;
     const bool RCONTIG = (p.rs == 1);
+    const int64_t l0 = kc * p.kchunk, l1 = min(p.k, l0 + p.kchunk);
     auto mag = [&](const Elem v, uint64_t (&m)[NX]) {
         if constexpr (!CPLX) {
             const uint64_t u = (uint64_t)__double_as_longlong(v) & kAbsMask;
@@ -604,19 +621,15 @@ __device__ __forceinline__ void exps_side(const SplitParams &p, int64_t g, int64
             }
         }
     };
-    auto finish = [&](int64_t r, const uint64_t (&m)[NX]) {
+    auto fold = [&](int64_t r, const uint64_t (&m)[NX]) {
 #pragma unroll
         for (int x = 0; x < NX; ++x) {
-            const bool nf = m[x] >= kExpInf;
-            const int32_t e = nf ? kNonFinite : (CRT ? crt_exponent(m[x], p.crt.nu) : exponent_from_maxbits(m[x]));
-            int32_t *ex = p.exps + (MODE == SPLIT_3M ? x * p.x_exps : 0) + b * p.rows_out;
-            if (MODE == SPLIT_B4M) {
-                ex[2 * r] = e;
-                ex[2 * r + 1] = e;
-            } else {
-                ex[r] = e;
-            }
-            if (nf) atomicAdd(p.nonfinite, 1ull);
+            if (m[x] == 0) continue;
+            const uint32_t v = (m[x] >= kExpInf)
+                                   ? 0xffffffffu
+                                   : (uint32_t)((CRT ? crt_exponent(m[x], p.crt.nu) : exponent_from_maxbits(m[x])) +
+                                                kExpBiasDef);
+            atomicMax(p.emax + ((int64_t)x * gridDim.y + b) * p.rows + r, v);
         }
     };
     uint64_t m[NX];
@@ -627,7 +640,7 @@ __device__ __forceinline__ void exps_side(const SplitParams &p, int64_t g, int64
         if (r >= p.rows) return;
         const Elem *gp = X + r * p.rs;
 #pragma unroll 8
-        for (int64_t l = lane; l < p.k; l += 32) mag(gp[l], m);
+        for (int64_t l = l0 + lane; l < l1; l += 32) mag(gp[l], m);
 #pragma unroll
         for (int x = 0; x < NX; ++x) {
 #pragma unroll
@@ -636,14 +649,14 @@ __device__ __forceinline__ void exps_side(const SplitParams &p, int64_t g, int64
                 m[x] = om > m[x] ? om : m[x];
             }
         }
-        if (lane == 0) finish(r, m);
+        if (lane == 0) fold(r, m);
     } else {
         const int64_t r = g * 32 + lane;
         if (r < p.rows) {
-            const Elem *gp = X + r + warp * p.ls;
+            const Elem *gp = X + r + (l0 + warp) * p.ls;
             const int64_t step = 8 * p.ls;
 #pragma unroll 8
-            for (int64_t l = warp; l < p.k; l += 8, gp += step) mag(*gp, m);
+            for (int64_t l = l0 + warp; l < l1; l += 8, gp += step) mag(*gp, m);
         }
 #pragma unroll
         for (int x = 0; x < NX; ++x) s_m[x][warp][lane] = m[x];
@@ -656,21 +669,22 @@ __device__ __forceinline__ void exps_side(const SplitParams &p, int64_t g, int64
                 for (int w = 1; w < 8; ++w) v = s_m[x][w][lane] > v ? s_m[x][w][lane] : v;
                 m[x] = v;
             }
-            finish(r, m);
+            fold(r, m);
         }
     }
 }
 
-// One CTA per row group of one side (blockIdx.z) and batch entry (blockIdx.y): 8 rows (rows
-// contiguous along l) or 32 rows (rows adjacent for each l).  (A persistent form over both
-// sides' groups measured slower: the long 32-row groups then run on few CTAs.)
+// One CTA per (row group, K chunk) of one side (blockIdx.z) and batch entry (blockIdx.y);
+// blockIdx.x = group * chunks + chunk.
 template <int MA, int MB, bool CRT = false>
 __global__ void __launch_bounds__(256) k_split_exps(const __grid_constant__ SplitPair pp) {
     const SplitParams &q = pp.side[blockIdx.z];
     const int64_t gsz = (q.rs == 1) ? 32 : 8;
-    if ((int64_t)blockIdx.x * gsz >= q.rows) return;
-    if (blockIdx.z == 0) exps_side<MA, CRT>(q, blockIdx.x, blockIdx.y);
-    else exps_side<MB, CRT>(q, blockIdx.x, blockIdx.y);
+    const int64_t nch = (q.k + q.kchunk - 1) / q.kchunk;
+    const int64_t g = blockIdx.x / nch, kc = blockIdx.x % nch;
+    if (g * gsz >= q.rows) return;
+    if (blockIdx.z == 0) exps_side<MA, CRT>(q, g, kc, blockIdx.y);
+    else exps_side<MB, CRT>(q, g, kc, blockIdx.y);
 }
 
 }  // namespace ozk
