@@ -361,6 +361,9 @@ def run_ours(args):
 
     # ---- timed pass 2 (same K steps): per-launch CUDA events on the launch stream give each
     # kernel's device time -> the roofline's kernel duration and the phase split
+    # the kernel's own duration: without cross-call overlap (in pass 1 the next step's split CTAs
+    # share the GEMM's last wave, which lengthens the GEMM grid while shortening the step)
+    oz.set_overlap(False)
     oz.profile_enable(True)
     oz.profile_read()
     torch.cuda.synchronize()
@@ -373,6 +376,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     prof = oz.profile_read()
     oz.profile_enable(False)
+    oz.set_overlap(not args.no_overlap)
     ms_instrumented = p0.elapsed_time(p1) / args.steps
 
     bf16_burst, bf16_sus, peak_src = peaks()
@@ -420,8 +424,8 @@ def run_ours(args):
             "kernel_ms_per_launch": round(gemm_ms, 5),
             "kernel_share_of_step": round(gemm_ms * gemm["launches"] / args.steps / max(1e-9, ms_instrumented), 4),
             "timing": ("kernel time from per-launch CUDA events on the launch stream in a second timed "
-                       "pass of the same K steps (%.4f ms/step with the events; the headline pass has "
-                       "none)" % ms_instrumented),
+                       "pass of the same K steps without cross-call overlap (%.4f ms/step with the "
+                       "events; the headline pass has none)" % ms_instrumented),
         },
         "roofline_split": split_roofline(step_phase_ms.get("k1_slice", 0.0), batch, n, s, args.method),
         "paper_context": {
