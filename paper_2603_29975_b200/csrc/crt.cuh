@@ -71,11 +71,12 @@ __device__ __forceinline__ uint32_t centre_byte(uint32_t r, uint32_t p) {
     return (r >= ((p + 1) >> 1)) ? (r - p) & 0xffu : r;
 }
 
-// R19 epilogue: (int32 sum of residue products) mod p, centred byte.
+// R19 epilogue: (int32 sum of residue products) mod p, as the byte u in [0, p) (not centred:
+// the residue planes are read only by k_crt, which needs u).
 // v = vh 2^16 + vl with |vh| < 2^15: folded to vh c16 + vl + bias23 in [0, 2^25).
 __device__ __forceinline__ uint32_t residue_of_i32(int32_t v, const CrtTab &t, int i) {
     const uint32_t x = (uint32_t)((v >> 16) * (int32_t)t.c16[i]) + (uint32_t)(v & 0xffff) + t.bias23[i];
-    return centre_byte(mod_small(x, t.p[i], t.m39[i]), t.p[i]);
+    return mod_small(x, t.p[i], t.m39[i]);   // u in [0, p): the planes feed only k_crt (p <= 256)
 }
 
 // 8 x 8 byte transpose of 8 words of 4 residue bytes each (values i, moduli

@@ -1,10 +1,10 @@
 // crt_kernel.cuh -- Ozaki-II reconstruction (NEXT-1, reading R20; PAPER.md:99
 // "uses the CRT to reconstruct the final result").
 //
-// Per output element: the n centred residues z_q (plane q) determine the
-// unique Z in (-M/2, M/2] with Z = z_q mod p_q; by the choice of nu (R17) Z is
+// Per output element: the n residues u_q in [0, p_q) (plane q) determine the
+// unique Z in (-M/2, M/2] with Z = u_q mod p_q; by the choice of nu (R17) Z is
 // the exact integer product Q_A . Q_B.  Computed exactly in 32-bit limbs:
-//   S = sum_q u_q W_q   (u_q = z_q mod p_q in [0, p_q), W_q = (M/p_q) inv_q < M)
+//   S = sum_q u_q W_q   (W_q = (M/p_q) inv_q < M)
 //   Z = S mod M  (quotient from an FP64 estimate, corrected to be exact), centred
 // then P = RNE(Z 2^(e_i + f_j - 2 nu)) with ONE rounding at the bit position
 // of the (normal or subnormal) result, and C = alpha P + beta C as R7.
@@ -117,11 +117,9 @@ __global__ void __launch_bounds__(256) k_crt(const __grid_constant__ CrtParams P
 #pragma unroll
     for (int q = 0; q < N; ++q) {
         const uint32_t word = words[q];
-        const uint32_t p = P.p[q];
 #pragma unroll
         for (int x = 0; x < 4; ++x) {
-            const int32_t zc = (int32_t)(int8_t)(word >> (8 * x));
-            const uint32_t u = (uint32_t)zc + (p & (uint32_t)(zc >> 31));   // centred -> [0, p)
+            const uint32_t u = (word >> (8 * x)) & 0xffu;   // residue planes hold u in [0, p)
 #pragma unroll
             for (int l = 0; l < L; ++l) acc[x][l] += (unsigned long long)u * P.W[q][l];
         }
