@@ -151,24 +151,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCrtThreads, 1)
                 tc_fence_after();
                 int8_t *dst = rb + (int64_t)q * P.plane_bytes;
 #pragma unroll
-                for (int gg = 0; gg < 4; ++gg) {
-                    uint32_t v[16];
-                    tmem_ld_32x32b_x16(tl + slot * 256u + (uint32_t)(16 * gg), v);
+                for (int gp = 0; gp < 2; ++gp) {   // two 16-column groups in flight per TMEM wait
+                    uint32_t v[2][16];
+                    tmem_ld_32x32b_x16(tl + slot * 256u + (uint32_t)(32 * gp), v[0]);
+                    tmem_ld_32x32b_x16(tl + slot * 256u + (uint32_t)(32 * gp + 16), v[1]);
                     tmem_wait_ld();
-                    if (gg == 3) {          // all four loads of this slot done: hand it back
+                    if (gp == 1) {          // all four loads of this slot done: hand it back
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive_cluster(slot_remote0 + 8u * slot);
                     }
-                    uint32_t w[4];
 #pragma unroll
-                    for (int x = 0; x < 4; ++x) {
-                        w[x] = residue_of_i32((int32_t)v[4 * x], P.crt, q) |
-                               (residue_of_i32((int32_t)v[4 * x + 1], P.crt, q) << 8) |
-                               (residue_of_i32((int32_t)v[4 * x + 2], P.crt, q) << 16) |
-                               (residue_of_i32((int32_t)v[4 * x + 3], P.crt, q) << 24);
+                    for (int hg = 0; hg < 2; ++hg) {
+                        const int gg = 2 * gp + hg;
+                        uint32_t w[4];
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) {
+                            w[x] = residue_of_i32((int32_t)v[hg][4 * x], P.crt, q) |
+                                   (residue_of_i32((int32_t)v[hg][4 * x + 1], P.crt, q) << 8) |
+                                   (residue_of_i32((int32_t)v[hg][4 * x + 2], P.crt, q) << 16) |
+                                   (residue_of_i32((int32_t)v[hg][4 * x + 3], P.crt, q) << 24);
+                        }
+                        *reinterpret_cast<uint4 *>(dst + (int64_t)gg * P.rows_pad * 16) =
+                            make_uint4(w[0], w[1], w[2], w[3]);
                     }
-                    *reinterpret_cast<uint4 *>(dst + (int64_t)gg * P.rows_pad * 16) = make_uint4(w[0], w[1], w[2], w[3]);
                 }
             }
         }
