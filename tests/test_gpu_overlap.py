@@ -86,3 +86,31 @@ def test_overlap_flag_thread_local_default_off():
     assert oz.get_overlap() is True
     oz.set_overlap(False)
     assert oz.get_overlap() is False
+
+
+def test_overlap_two_streams_interleaved():
+    """Calls alternating between two streams (per-stream overlap state and workspaces), each
+    stream's C reused: bitwise equal to the same calls without overlap."""
+    s = 6
+    A = [dev(synth.uniform(300, 260, seed=30 + i)) for i in range(2)]
+    B = [dev(synth.spread(260, 280, seed=40 + i, phi=1.5)) for i in range(2)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+
+    def run(overlap):
+        oz.set_overlap(overlap)
+        try:
+            C = [dev(np.zeros((300, 280))) for _ in range(2)]
+            torch.cuda.synchronize()
+            for rep in range(5):
+                for i in (0, 1):
+                    with torch.cuda.stream(streams[i]):
+                        oz.dgemm("N", "N", 1.0 + rep, A[i], B[i], 0.5, C[i], s)
+            torch.cuda.synchronize()
+            return [c.cpu().numpy() for c in C]
+        finally:
+            oz.set_overlap(False)
+
+    ref = run(False)
+    got = run(True)
+    for g, r in zip(got, ref):
+        assert np.array_equal(g, r)
