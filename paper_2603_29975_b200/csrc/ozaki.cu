@@ -1867,15 +1867,16 @@ int64_t ozaki_get_exponent_block(void) { return t_kblock; }
 
 int ozaki_set_overlap(int on) {
     t_overlap = on ? 1 : 0;
-    if (!on) {   // release the persistent workspaces of this thread (after their GEMMs finish)
+    if (!on && !t_ov.empty()) {   // release this thread's persistent workspaces once their GEMMs
+        int cur = 0;                 // finished (device-wide sync: a tracked stream may be gone)
+        cudaGetDevice(&cur);
         for (auto &o : t_ov) {
-            int d = 0;
-            cudaGetDevice(&d);
-            if (o.dev != d) continue;
-            cudaStreamSynchronize(o.st);
+            cudaSetDevice(o.dev);
+            cudaDeviceSynchronize();
             for (int i = 0; i < 2; ++i)
                 if (o.ws[i]) cudaFree(o.ws[i]);
         }
+        cudaSetDevice(cur);
         t_ov.clear();
     }
     return 0;
