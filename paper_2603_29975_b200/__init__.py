@@ -164,11 +164,39 @@ def _cuda(x, dtype, name):
     return x
 
 
-def _bind_stream(stream=None):
+def _operands(dtype, A, B, C):
+    """Type checks; resolves lazy conj / neg views of A and B (torch keeps them as a bit on the
+    tensor, the library would read the unconjugated storage); C must be a plain tensor.  All
+    three on one CUDA device, or all on the CPU (host offload).  Returns (A, B, device)."""
+    for x, nm in ((A, "A"), (B, "B"), (C, "C")):
+        _cuda(x, dtype, nm)
+    if C.is_conj() or C.is_neg():
+        raise ValueError("C must not be a lazily conjugated / negated view (resolve it first)")
+    A = A.resolve_conj().resolve_neg() if (A.is_conj() or A.is_neg()) else A
+    B = B.resolve_conj().resolve_neg() if (B.is_conj() or B.is_neg()) else B
+    devs = {x.device for x in (A, B, C)}
+    if len(devs) != 1:
+        raise ValueError(f"A, B and C must live on one device, got {sorted(map(str, devs))}")
+    return A, B, C.device
+
+
+def _on(device):
+    """Device guard for one library call: the library works on the current CUDA device."""
+    import contextlib
+    import torch
+    if device is None or device.type != "cuda":
+        return contextlib.nullcontext()
+    return torch.cuda.device(device)
+
+
+def _bind_stream(stream=None, device=None):
     import torch
     if stream is None and not torch.cuda.is_available():
         raise RuntimeError("no CUDA device: the Ozaki library has no CPU path")
-    s = stream if stream is not None else torch.cuda.current_stream()
+    if stream is None:
+        s = torch.cuda.current_stream(device if device is not None and device.type == "cuda" else None)
+    else:
+        s = stream
     lib().ozaki_set_stream(ctypes.c_void_p(s.cuda_stream))
 
 
@@ -190,28 +218,28 @@ def _cpair(z):
 def dgemm(transa, transb, alpha, A, B, beta, C, num_slices, stream=None):
     """C <- alpha op(A) op(B) + beta C, emulated with ``num_slices`` INT8 slices."""
     import torch
-    for x, nm in ((A, "A"), (B, "B"), (C, "C")):
-        _cuda(x, torch.float64, nm)
+    A, B, dev = _operands(torch.float64, A, B, C)
     m, n, k = _dims(transa, transb, A, B)
     if tuple(C.shape) != (m, n):
         raise ValueError(f"C must be {m}x{n}")
-    _bind_stream(stream)
-    rc = lib().ozaki_dgemm(_ch(transa), _ch(transb), m, n, k, float(alpha), A.data_ptr(), _ld(A),
-                           B.data_ptr(), _ld(B), float(beta), C.data_ptr(), _ld(C), int(num_slices))
+    with _on(dev):
+        _bind_stream(stream, dev)
+        rc = lib().ozaki_dgemm(_ch(transa), _ch(transb), m, n, k, float(alpha), A.data_ptr(), _ld(A),
+                               B.data_ptr(), _ld(B), float(beta), C.data_ptr(), _ld(C), int(num_slices))
     _check(rc, "ozaki_dgemm")
     return C
 
 
 def _zgemm(fn, transa, transb, alpha, A, B, beta, C, num_slices, stream):
     import torch
-    for x, nm in ((A, "A"), (B, "B"), (C, "C")):
-        _cuda(x, torch.complex128, nm)
+    A, B, dev = _operands(torch.complex128, A, B, C)
     m, n, k = _dims(transa, transb, A, B)
     if tuple(C.shape) != (m, n):
         raise ValueError(f"C must be {m}x{n}")
-    _bind_stream(stream)
-    rc = fn(_ch(transa), _ch(transb), m, n, k, _cpair(alpha), A.data_ptr(), _ld(A), B.data_ptr(),
-            _ld(B), _cpair(beta), C.data_ptr(), _ld(C), int(num_slices))
+    with _on(dev):
+        _bind_stream(stream, dev)
+        rc = fn(_ch(transa), _ch(transb), m, n, k, _cpair(alpha), A.data_ptr(), _ld(A), B.data_ptr(),
+                _ld(B), _cpair(beta), C.data_ptr(), _ld(C), int(num_slices))
     _check(rc, fn.__name__)
     return C
 
@@ -227,9 +255,8 @@ def zgemm3m(transa, transb, alpha, A, B, beta, C, num_slices, stream=None):
 
 
 def _batched(fn, dtype, transa, transb, alpha, A, B, beta, C, num_slices, stream, cplx):
-    import torch
+    A, B, dev = _operands(dtype, A, B, C)
     for x, nm in ((A, "A"), (B, "B"), (C, "C")):
-        _cuda(x, dtype, nm)
         if x.dim() != 3:
             raise ValueError(f"{nm} must be (batch, rows, cols)")
     batch = A.shape[0]
@@ -238,14 +265,15 @@ def _batched(fn, dtype, transa, transb, alpha, A, B, beta, C, num_slices, stream
     m, n, k = _dims(transa, transb, A, B)
     if tuple(C.shape[1:]) != (m, n):
         raise ValueError(f"C entries must be {m}x{n}")
-    _bind_stream(stream)
     al = _cpair(alpha) if cplx else float(alpha)
     be = _cpair(beta) if cplx else float(beta)
     sA = A.stride(0) if batch > 1 else 0
     sB = B.stride(0) if batch > 1 else 0
     sC = C.stride(0) if batch > 1 else 0
-    rc = fn(_ch(transa), _ch(transb), m, n, k, al, A.data_ptr(), _ld(A), sA, B.data_ptr(), _ld(B),
-            sB, be, C.data_ptr(), _ld(C), sC, batch, int(num_slices))
+    with _on(dev):
+        _bind_stream(stream, dev)
+        rc = fn(_ch(transa), _ch(transb), m, n, k, al, A.data_ptr(), _ld(A), sA, B.data_ptr(), _ld(B),
+                sB, be, C.data_ptr(), _ld(C), sC, batch, int(num_slices))
     _check(rc, fn.__name__)
     return C
 
@@ -272,14 +300,14 @@ def zgemm3m_strided_batched(transa, transb, alpha, A, B, beta, C, num_slices, st
 def ozaki2_dgemm(transa, transb, alpha, A, B, beta, C, num_moduli, stream=None):
     """C <- alpha op(A) op(B) + beta C via Ozaki-II with ``num_moduli`` moduli (R16..R20)."""
     import torch
-    for x, nm in ((A, "A"), (B, "B"), (C, "C")):
-        _cuda(x, torch.float64, nm)
+    A, B, dev = _operands(torch.float64, A, B, C)
     m, n, k = _dims(transa, transb, A, B)
     if tuple(C.shape) != (m, n):
         raise ValueError(f"C must be {m}x{n}")
-    _bind_stream(stream)
-    rc = lib().ozaki2_dgemm(_ch(transa), _ch(transb), m, n, k, float(alpha), A.data_ptr(), _ld(A),
-                            B.data_ptr(), _ld(B), float(beta), C.data_ptr(), _ld(C), int(num_moduli))
+    with _on(dev):
+        _bind_stream(stream, dev)
+        rc = lib().ozaki2_dgemm(_ch(transa), _ch(transb), m, n, k, float(alpha), A.data_ptr(), _ld(A),
+                                B.data_ptr(), _ld(B), float(beta), C.data_ptr(), _ld(C), int(num_moduli))
     _check(rc, "ozaki2_dgemm")
     return C
 
@@ -380,9 +408,11 @@ def debug_split(side, kind, trans, X, num_slices, stream=None):
     sl = torch.empty((s, rows_out, kdepth), dtype=torch.int8, device=X.device)
     ex = torch.empty((rows_out,), dtype=torch.int32, device=X.device)
     kd = ctypes.c_int64(0)
-    _bind_stream(stream)
-    rc = lib().ozaki_debug_split(_ch(side), _ch(kind), _ch(trans), rows, cols, X.data_ptr(), _ld(X),
-                                 s, sl.data_ptr(), ex.data_ptr(), ctypes.byref(kd))
+    X = X.resolve_conj().resolve_neg()
+    with _on(X.device):
+        _bind_stream(stream, X.device)
+        rc = lib().ozaki_debug_split(_ch(side), _ch(kind), _ch(trans), rows, cols, X.data_ptr(), _ld(X),
+                                     s, sl.data_ptr(), ex.data_ptr(), ctypes.byref(kd))
     _check(rc, "ozaki_debug_split")
     assert kd.value == kdepth
     return sl, ex
@@ -409,8 +439,9 @@ def debug_level_sums(transa, transb, A, B, num_slices, stream=None):
     s = int(num_slices)
     nlev = 2 * s - 1 if get_pair_set() == "full" else s
     S = torch.zeros((nlev, n, m), dtype=torch.int32, device=A.device)   # column-major per level
-    _bind_stream(stream)
-    rc = lib().ozaki_debug_level_sums(_ch(transa), _ch(transb), m, n, k, A.data_ptr(), _ld(A),
-                                      B.data_ptr(), _ld(B), s, S.data_ptr())
+    with _on(A.device):
+        _bind_stream(stream, A.device)
+        rc = lib().ozaki_debug_level_sums(_ch(transa), _ch(transb), m, n, k, A.data_ptr(), _ld(A),
+                                          B.data_ptr(), _ld(B), s, S.data_ptr())
     _check(rc, "ozaki_debug_level_sums")
     return S.transpose(1, 2)

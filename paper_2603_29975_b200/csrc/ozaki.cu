@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -51,16 +52,31 @@ struct OvState {
     bool last_gemm = false;
     uintptr_t c_lo = 0, c_hi = 0;
 };
-thread_local std::vector<OvState> t_ov;
+// The persistent workspaces are freed when the thread exits (or on ozaki_set_overlap(0)).
+struct OvList {
+    std::vector<OvState> v;
+    ~OvList() {
+        for (auto &o : v)
+            for (int i = 0; i < 2; ++i)
+                if (o.ws[i]) {
+                    int cur = 0;
+                    if (cudaGetDevice(&cur) != cudaSuccess) return;   // runtime already torn down
+                    cudaSetDevice(o.dev);
+                    cudaFree(o.ws[i]);
+                    cudaSetDevice(cur);
+                }
+    }
+};
+thread_local OvList t_ov_list;
 OvState &ov_state(cudaStream_t st) {
     int d = 0;
     cudaGetDevice(&d);
-    for (auto &o : t_ov)
+    for (auto &o : t_ov_list.v)
         if (o.st == st && o.dev == d) return o;
-    t_ov.emplace_back();
-    t_ov.back().st = st;
-    t_ov.back().dev = d;
-    return t_ov.back();
+    t_ov_list.v.emplace_back();
+    t_ov_list.v.back().st = st;
+    t_ov_list.v.back().dev = d;
+    return t_ov_list.v.back();
 }
 
 struct Stats {
@@ -142,13 +158,30 @@ int fail(int code, const char *fmt, ...) {
             return fail(OZAKI_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e)); \
     } while (0)
 
+// Dynamic shared memory opt-in, per device and kernel: the attribute belongs to the device
+// context, so a process that drives several GPUs sets it once on each; the cache is updated
+// under the lock together with the attribute (two threads cannot leave it claiming more than
+// the attribute holds).
+std::mutex g_attr_mu;
+std::unordered_map<const void *, size_t> g_attr[kMaxDev];
+
+cudaError_t smem_optin(const void *fn, size_t smem) {
+    if (smem <= 48 * 1024) return cudaSuccess;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    size_t &have = g_attr[dev][fn];
+    if (have >= smem) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) have = smem;
+    return e;
+}
+
 template <int BN, int EPI>
 int set_gemm_attr(size_t smem) {
-    static std::atomic<size_t> done{0};
-    if (done.load() >= smem) return 0;
-    CUDA_TRY(cudaFuncSetAttribute(k_gemm<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)std::max<size_t>(smem, 48 * 1024)));
-    done.store(smem);
+    CUDA_TRY(smem_optin((const void *)k_gemm<BN, EPI>, smem));
     return 0;
 }
 
@@ -464,12 +497,7 @@ SplitParams split_params(const Plan &P, const Operand &op, bool sideA, int8_t *s
 template <int S, int MA, int MB>
 void launch_split_long(dim3 grid, size_t smem, cudaStream_t st, const SplitPair &pp, int KW, int nwin) {
     constexpr int R = (MA == SPLIT_REAL) ? 16 : 8;
-    static size_t attr = 0;
-    if (attr < smem) {
-        cudaFuncSetAttribute(k_split_fast<S, MA, MB, R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        attr = smem;
-    }
+    smem_optin((const void *)k_split_fast<S, MA, MB, R, true>, smem);   // a failure surfaces at launch
     k_split_fast<S, MA, MB, R, true><<<grid, 32 * R, smem, st>>>(pp, KW, nwin, 0);
 }
 
@@ -590,12 +618,7 @@ int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b,
         ProfScope ps(st, PH_SLICE);
 #define OZK_FAST_RG(S, MA, MB, R)                                                                    \
         {                                                                                            \
-            static size_t attr = 0;                                                                  \
-            if (attr < smem) {                                                                       \
-                cudaFuncSetAttribute(k_split_fast<S, MA, MB, R>,                                     \
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
-                attr = smem;                                                                         \
-            }                                                                                        \
+            smem_optin((const void *)k_split_fast<S, MA, MB, R>, smem);                               \
             launch_pdl(k_split_fast<S, MA, MB, R>, grid, dim3(32 * R), smem, st, pdl, pp, KW, nwin,   \
                        early ? 1 : 0);                                                               \
         }
@@ -645,12 +668,7 @@ int launch_split_sides(const Plan &P, const SplitParams &a, const SplitParams *b
         ProfScope ps(st, PH_SLICE);
 #define OZK_SPLIT(SM, CX)                                                                           \
         {                                                                                           \
-            static size_t attr = 0;                                                                 \
-            if (attr < smem) {                                                                      \
-                cudaFuncSetAttribute(k_split_sm<SM, CX>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                     (int)smem);                                                    \
-                attr = smem;                                                                        \
-            }                                                                                       \
+            smem_optin((const void *)k_split_sm<SM, CX>, smem);                                     \
             k_split_sm<SM, CX><<<grid, 256, smem, st>>>(pp, KW);                                    \
         }
         if (P.s <= 8) {
@@ -682,12 +700,7 @@ int launch_split_ab(const Plan &P, const Operand &oa, int8_t *sa, int32_t *ea, c
 // ---------------------------------------------------------------- K2 launch
 template <int EPI>
 int launch_gemm_lv(const Plan &P, const GemmParams &gp, DevState *dev, cudaStream_t st) {
-    static std::atomic<size_t> done{0};
-    if (done.load() < P.smem) {
-        CUDA_TRY(cudaFuncSetAttribute(k_gemm_lv<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)P.smem));
-        done.store(P.smem);
-    }
+    CUDA_TRY(smem_optin((const void *)k_gemm_lv<EPI>, P.smem));
     LvParams lp{};
     lp.g = gp;
     lp.npass = P.npass;
@@ -728,12 +741,7 @@ int rows_map(CUtensorMap *m, const void *base, size_t bytes, uint32_t box_rows) 
 template <int EPI, int CHUNK = 0, bool FULL = false>
 int launch_gemm_lv2(const Plan &P, const GemmParams &gp, size_t a_avail, size_t b_avail, DevState *dev,
                     cudaStream_t st) {
-    static std::atomic<size_t> done{0};
-    if (done.load() < P.smem) {
-        CUDA_TRY(cudaFuncSetAttribute(k_gemm_lv2<EPI, CHUNK, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)P.smem));
-        done.store(P.smem);
-    }
+    CUDA_TRY(smem_optin((const void *)k_gemm_lv2<EPI, CHUNK, FULL>, P.smem));
     Lv2Params P2;
     std::memset(&P2, 0, sizeof P2);
     P2.lv.g = gp;
@@ -1074,8 +1082,13 @@ int run_offload(const Call &c) {
     const size_t es = (c.kind == KIND_REAL) ? 8 : 16;
     const int64_t ar = c.ta == 'N' ? c.m : c.k, ac = c.ta == 'N' ? c.k : c.m;
     const int64_t br = c.tb == 'N' ? c.k : c.n, bc = c.tb == 'N' ? c.n : c.k;
-    // element span of one entry (leading dimensions kept as given)
-    const int64_t spanA = (ac - 1) * c.lda + ar, spanB = (bc - 1) * c.ldb + br, spanC = (c.n - 1) * c.ldc + c.m;
+    // A and B are read only when alpha != 0 and k > 0 (else the quick return C = beta C runs on
+    // the staged C alone)
+    const bool readsAB = !(c.al[0] == 0.0 && c.al[1] == 0.0) && c.k > 0;
+    // element span of one entry (leading dimensions kept as given); C moves as m x n with pitch
+    // ldc (cudaMemcpy2DAsync), so the rows m..ldc-1 of the caller's array are never written
+    const int64_t spanA = readsAB ? (ac - 1) * c.lda + ar : 0, spanB = readsAB ? (bc - 1) * c.ldb + br : 0;
+    const int64_t spanC = (c.n - 1) * c.ldc + c.m;
     const bool readC = !(c.be[0] == 0.0 && c.be[1] == 0.0);
     const size_t per_entry = (size_t)(spanA + spanB + spanC) * es;
     size_t chunk_bytes = 32ull << 20;   // ~32 MB per chunk (measured best: 5.6 vs 5.9 ms for C2x30; OZAKI_OFFLOAD_CHUNK_MB overrides)
@@ -1117,13 +1130,16 @@ int run_offload(const Call &c) {
         double *dC = (double *)(buf[set] + (size_t)cb * (spanA + spanB) * es);
         if (ch >= 2) CUDA_TRY(cudaStreamWaitEvent(o->h2d, o->out_done[set], 0));   // buffer set reuse
         for (int64_t i = 0; i < nb; ++i) {
-            CUDA_TRY(cudaMemcpyAsync((char *)dA + (size_t)i * spanA * es, hA + (size_t)(b0 + i) * c.sA * es,
-                                     (size_t)spanA * es, cudaMemcpyHostToDevice, o->h2d));
-            CUDA_TRY(cudaMemcpyAsync((char *)dB + (size_t)i * spanB * es, hB + (size_t)(b0 + i) * c.sB * es,
-                                     (size_t)spanB * es, cudaMemcpyHostToDevice, o->h2d));
+            if (readsAB) {
+                CUDA_TRY(cudaMemcpyAsync((char *)dA + (size_t)i * spanA * es, hA + (size_t)(b0 + i) * c.sA * es,
+                                         (size_t)spanA * es, cudaMemcpyHostToDevice, o->h2d));
+                CUDA_TRY(cudaMemcpyAsync((char *)dB + (size_t)i * spanB * es, hB + (size_t)(b0 + i) * c.sB * es,
+                                         (size_t)spanB * es, cudaMemcpyHostToDevice, o->h2d));
+            }
             if (readC)
-                CUDA_TRY(cudaMemcpyAsync((char *)dC + (size_t)i * spanC * es, hC + (size_t)(b0 + i) * c.sC * es,
-                                         (size_t)spanC * es, cudaMemcpyHostToDevice, o->h2d));
+                CUDA_TRY(cudaMemcpy2DAsync((char *)dC + (size_t)i * spanC * es, (size_t)c.ldc * es,
+                                           hC + (size_t)(b0 + i) * c.sC * es, (size_t)c.ldc * es,
+                                           (size_t)c.m * es, (size_t)c.n, cudaMemcpyHostToDevice, o->h2d));
         }
         CUDA_TRY(cudaEventRecord(o->in_done[set], o->h2d));
         CUDA_TRY(cudaStreamWaitEvent(o->comp, o->in_done[set], 0));
@@ -1146,8 +1162,9 @@ int run_offload(const Call &c) {
         CUDA_TRY(cudaEventRecord(o->comp_done[set], o->comp));
         CUDA_TRY(cudaStreamWaitEvent(o->d2h, o->comp_done[set], 0));
         for (int64_t i = 0; i < nb; ++i)
-            CUDA_TRY(cudaMemcpyAsync(hC + (size_t)(b0 + i) * c.sC * es, (char *)dC + (size_t)i * spanC * es,
-                                     (size_t)spanC * es, cudaMemcpyDeviceToHost, o->d2h));
+            CUDA_TRY(cudaMemcpy2DAsync(hC + (size_t)(b0 + i) * c.sC * es, (size_t)c.ldc * es,
+                                       (char *)dC + (size_t)i * spanC * es, (size_t)c.ldc * es,
+                                       (size_t)c.m * es, (size_t)c.n, cudaMemcpyDeviceToHost, o->d2h));
         CUDA_TRY(cudaEventRecord(o->out_done[set], o->d2h));
     }
     // the caller's stream observes completion; host memory is final on return
@@ -1270,12 +1287,7 @@ void launch_crt_fast(bool real, bool lng, dim3 grid, size_t smem, cudaStream_t s
                      int nwin) {
 #define OZK_CRT_K(MA, MB, R, L)                                                                      \
     {                                                                                                \
-        static size_t attr = 0;                                                                      \
-        if (attr < smem) {                                                                           \
-            cudaFuncSetAttribute(k_split_fast<NMX, MA, MB, R, L, true>,                              \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
-            attr = smem;                                                                             \
-        }                                                                                            \
+        smem_optin((const void *)k_split_fast<NMX, MA, MB, R, L, true>, smem);                       \
         k_split_fast<NMX, MA, MB, R, L, true><<<grid, 32 * R, smem, st>>>(pp, KW, nwin, 0);          \
     }
     if (real) {
@@ -1404,12 +1416,7 @@ int run_crt(const Call &c, DevState *dev, cudaStream_t st) {
         ProfScope ps(st, PH_SLICE);
 #define OZK_SPLIT2(CX)                                                                               \
         {                                                                                            \
-            static bool attr = false;                                                                \
-            if (!attr) {                                                                             \
-                cudaFuncSetAttribute(k_split_sm<8, CX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                     (int)smem);                                                     \
-                attr = true;                                                                         \
-            }                                                                                        \
+            smem_optin((const void *)k_split_sm<8, CX, true>, smem);                                 \
             k_split_sm<8, CX, true><<<grid, 256, smem, st>>>(pp, KW);                               \
         }
         if (cx) OZK_SPLIT2(true) else OZK_SPLIT2(false)
@@ -1450,11 +1457,7 @@ int run_crt(const Call &c, DevState *dev, cudaStream_t st) {
         rc = rows_map(&G.tmA, sa, a_bytes, (uint32_t)kpp * (kCrtBlk / 256));
         if (!rc) rc = rows_map(&G.tmB, sb, b_bytes, (uint32_t)kpp * (kCrtBlk / 256));
         if (!rc) {
-            static std::atomic<size_t> done{0};
-            if (done.load() < smem) {
-                CUDA_TRY(cudaFuncSetAttribute(k_gemm_crt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                done.store(smem);
-            }
+            CUDA_TRY(smem_optin((const void *)k_gemm_crt, smem));
             const int64_t tiles = c.batch * tiles_m * tiles_n;
             const unsigned pairs = (unsigned)std::min<int64_t>(tiles, dev->sms / 2);
             {
@@ -1546,8 +1549,8 @@ int run(const Call &c0) {
         if (ka == PTR_HOST || kb == PTR_HOST || kc == PTR_HOST) {
             if (!(ka == PTR_HOST && kb == PTR_HOST && kc == PTR_HOST))
                 return fail(OZAKI_ERR_UNSUPPORTED, "A, B, C must all be device or all be host pointers");
-            if (!readsAB) return fail(OZAKI_ERR_UNSUPPORTED, "host-pointer quick return not supported");
-            return run_offload(c);
+            if (!readsAB && c.be[0] == 1.0 && c.be[1] == 0.0) return 0;   // quick return, C unchanged
+            return run_offload(c);   // (alpha == 0 or k == 0: C = beta C staged through k_scale_*)
         }
     }
     cudaStream_t st = t_stream;
@@ -1600,6 +1603,10 @@ int run(const Call &c0) {
         }
         const int64_t ew = cplx ? 2 : 1;   // doubles per element
         int rc = 0;
+        // the block calls run without cross-call overlap: the stream's last kernel is
+        // k_apply_ab (writing the user's C), never a tracked GEMM of the temporary T
+        const int ovs = t_overlap;
+        t_overlap = 0;
         for (int64_t b0 = 0; b0 < c.k && !rc; b0 += c.kblock) {
             Call cb = c;
             cb.k = std::min<int64_t>(c.kblock, c.k - b0);
@@ -1616,6 +1623,7 @@ int run(const Call &c0) {
             cb.batched = true;
             rc = run(cb);
         }
+        t_overlap = ovs;
         if (!rc) {
             dim3 grid(grid1d(c.m * c.n, dev->sms), 1, (unsigned)c.batch);
             ProfScope ps(st, PH_OTHER);
@@ -1867,17 +1875,17 @@ int64_t ozaki_get_exponent_block(void) { return t_kblock; }
 
 int ozaki_set_overlap(int on) {
     t_overlap = on ? 1 : 0;
-    if (!on && !t_ov.empty()) {   // release this thread's persistent workspaces once their GEMMs
+    if (!on && !t_ov_list.v.empty()) {   // release this thread's persistent workspaces once their GEMMs
         int cur = 0;                 // finished (device-wide sync: a tracked stream may be gone)
         cudaGetDevice(&cur);
-        for (auto &o : t_ov) {
+        for (auto &o : t_ov_list.v) {
             cudaSetDevice(o.dev);
             cudaDeviceSynchronize();
             for (int i = 0; i < 2; ++i)
                 if (o.ws[i]) cudaFree(o.ws[i]);
         }
         cudaSetDevice(cur);
-        t_ov.clear();
+        t_ov_list.v.clear();
     }
     return 0;
 }

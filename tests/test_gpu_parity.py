@@ -409,3 +409,59 @@ def test_disjoint_views_of_one_matrix(orc):
     with pytest.raises(oz.OzakiError) as ei:
         oz.zgemm("N", "N", 1.0, Xd[10:60, 10:60], Xd[10:60, 10:60], 0.0, Xd[40:90, 40:90], 7)
     assert ei.value.code == 5
+
+
+def test_host_offload_ldc_padding_and_quick_return(orc):
+    """Host offload moves C as m x n with pitch ldc: the rows m..ldc-1 of the caller's array
+    are never written, also with beta = 0; alpha = 0 / k = 0 with host pointers is
+    the BLAS quick return C = beta C (beta = 1: untouched; beta = 0: zeros, C not read)."""
+    m, n, k, ld, s = 70, 45, 33, 101, 6
+    A = synth.uniform(m, k, seed=3)
+    B = synth.uniform(k, n, seed=4)
+    C0 = synth.uniform(m, n, seed=5)
+    for beta in (0.0, -0.75):
+        big = torch.full((n, ld), 12345.0, dtype=torch.float64).pin_memory()   # column-major ld x n
+        big.t()[:m, :] = torch.from_numpy(C0)
+        Cv = big.t()[:m, :]
+        oz.dgemm("N", "N", 1.25, torch.from_numpy(np.asfortranarray(A)), torch.from_numpy(np.asfortranarray(B)),
+                 beta, Cv, s)
+        assert same(Cv.numpy(), orc.dgemm("N", "N", 1.25, A, B, beta, C0, s))
+        assert (big.t()[m:, :] == 12345.0).all(), beta
+    # quick returns on host pointers
+    for alpha, kk, beta in ((0.0, k, 0.5), (0.0, k, 0.0), (2.0, 0, -2.0), (0.0, k, 1.0)):
+        big = torch.full((n, ld), 7.0, dtype=torch.float64)
+        big.t()[:m, :] = torch.from_numpy(C0)
+        if beta == 0.0:
+            big.t()[:m, :] = float("nan")
+        Cv = big.t()[:m, :]
+        Ah = torch.from_numpy(np.asfortranarray(A[:, :kk]))
+        Bh = torch.from_numpy(np.asfortranarray(B[:kk, :]))
+        oz.dgemm("N", "N", alpha, Ah, Bh, beta, Cv, s)
+        want = orc.dgemm("N", "N", alpha, A[:, :kk], B[:kk, :], beta, None if beta == 0.0 else C0, s)
+        assert same(Cv.numpy(), want), (alpha, kk, beta)
+        assert (big.t()[m:, :] == 7.0).all()
+    # complex, batched, quick return with a complex beta on pinned host memory
+    Z0 = [synth.uniform(m, n, seed=20 + i, complex_=True) for i in range(3)]
+    tZ = torch.from_numpy(np.stack([np.asfortranarray(z).T for z in Z0])).contiguous().pin_memory().transpose(1, 2)
+    zA = torch.zeros((3, k, m), dtype=torch.complex128).transpose(1, 2)
+    zB = torch.zeros((3, n, k), dtype=torch.complex128).transpose(1, 2)
+    oz.zgemm_strided_batched("N", "N", 0.0, zA, zB, 0.5 - 0.25j, tZ, s)
+    for i in range(3):
+        assert same(tZ[i].numpy(), orc.zgemm("N", "N", 0.0, np.zeros((m, k), complex), np.zeros((k, n), complex),
+                                            0.5 - 0.25j, Z0[i], s))
+
+
+def test_lazy_conj_views(orc):
+    """torch keeps A.mH / A.conj() as a conj bit over unconjugated storage: the binding
+    resolves A and B before the call and refuses a conj-view C."""
+    A = synth.uniform(40, 30, seed=1, complex_=True)     # op(A) = A^H is 30 x 40
+    B = synth.uniform(40, 20, seed=2, complex_=True)
+    Ad = torch.from_numpy(A).to("cuda")                   # row-major: .mH is a column-major view
+    Bd = dev(B)
+    C = dev(np.zeros((30, 20), complex))
+    oz.zgemm("N", "N", 1.0, Ad.mH, Bd, 0.0, C, 7)
+    assert same(C.cpu().numpy(), orc.zgemm("C", "N", 1.0, A, B, 0.0, None, 7))
+    oz.zgemm("N", "N", 1.0, Ad.mH, Bd.conj(), 0.0, C, 7)
+    assert same(C.cpu().numpy(), orc.zgemm("C", "N", 1.0, A, np.conj(B), 0.0, None, 7))
+    with pytest.raises(ValueError):
+        oz.zgemm("N", "N", 1.0, Ad.mH, Bd, 0.0, C.conj(), 7)

@@ -401,3 +401,124 @@ def test_combine_order_golden(orc):
         Sarr = np.array(S, dtype=np.int64).reshape(s, 1, 1)
         P = orc.combine(Sarr, [e], [0], [f], [0], s)
         assert P[0, 0] == float(int(want)), ln
+
+
+# ------------------------------------------------- R9 complex embedding pins
+def _hexs(s):
+    return [float.fromhex(x) for x in s.split()]
+
+
+def test_complex_embedding_golden(orc):
+    """R9 by hand (tests/golden/complex_embedding.txt): the 4M N-side embedding and the 3M
+    combine; the A-side 4M embedding gives different bits on the same input."""
+    for ln in _golden_lines("complex_embedding.txt"):
+        meth, s_s, a_s, b_s, want_s, alt_s = [x.strip() for x in ln.split("|")]
+        ar, ai = _hexs(a_s)
+        br, bi = _hexs(b_s)
+        wr, wi = _hexs(want_s)
+        A = np.array([[complex(ar, ai)]])
+        B = np.array([[complex(br, bi)]])
+        C = orc.zgemm("N", "N", 1.0, A, B, 0.0, None, int(s_s), meth)
+        assert C[0, 0].real == wr and C[0, 0].imag == wi, (ln, C[0, 0])
+        if alt_s != "-":
+            assert C[0, 0].real != float.fromhex(alt_s)
+
+
+def _embedded_rows_nside(Aop, Bop):
+    """R9 N-side embedding written out as rational rows: A' row i = [Ar_i | Ai_i];
+    B'^T rows 2j = [Br_j | -Bi_j] (Re output), 2j+1 = [Bi_j | Br_j] (Im output)."""
+    Ar = [[Fraction(float(x.real)) for x in r] + [Fraction(float(x.imag)) for x in r] for r in Aop]
+    Bt = []
+    for j in range(Bop.shape[1]):
+        col = Bop[:, j]
+        Bt.append([Fraction(float(x.real)) for x in col] + [-Fraction(float(x.imag)) for x in col])
+        Bt.append([Fraction(float(x.imag)) for x in col] + [Fraction(float(x.real)) for x in col])
+    return Ar, Bt
+
+
+def _embedded_rows_aside(Aop, Bop):
+    """SURVEY's A-side embedding: rows [Ar | -Ai] (Re) and [Ai | Ar] (Im) against [Br; Bi]."""
+    Ar = [[Fraction(float(x.real)) for x in r] + [-Fraction(float(x.imag)) for x in r] for r in Aop]
+    Ar += [[Fraction(float(x.imag)) for x in r] + [Fraction(float(x.real)) for x in r] for r in Aop]
+    Bt = [[Fraction(float(x.real)) for x in Bop[:, j]] + [Fraction(float(x.imag)) for x in Bop[:, j]]
+          for j in range(Bop.shape[1])]
+    return Ar, Bt
+
+
+@pytest.mark.parametrize("s", [2, 3, 4])
+def test_4m_is_nside_embedding_bruteforce(orc, s):
+    """R9: the oracle's 4M product equals (within R6's 1 ulp) the exact retained sum of the
+    N-side embedding, computed by oracle/brute.py from the definitions.  Digits of -x differ
+    from -digits(x) only when a low byte of X is 0x80, so the crafted half of the inputs puts
+    X(Ai) = odd * 128 (row exponent 1): there the A-side embedding's retained sum is more
+    than 2 ulp away for some entry (the top digits of -X and X differ by the carry), so the pin tells the two readings apart."""
+    g = synth.rng(900 + s)
+    separated = 0
+    for trial in range(6):
+        m, n, k = 2, 2, int(g.integers(1, 4))
+        if trial % 2 == 0:
+            A = synth.spread(m, k, 40 * s + trial, phi=2.0, complex_=True)
+            B = synth.spread(k, n, 50 * s + trial, phi=2.0, complex_=True)
+        else:   # Ar = Br = 1 set e = f = 1, so X = x 2^(8s-2): X(Ai) = 2^(8s-3) + odd*128
+            # (low byte 0x80, a carry into the next digit), X(Bi) = odd*256 + odd
+            odd = lambda shape: 2 * g.integers(0, 32, shape) + 1  # noqa: E731
+            A = 1.0 + 1j * (0.5 + odd((m, k)) * 2.0 ** (9 - 8 * s))
+            B = 1.0 + 1j * (odd((k, n)) * 256 + odd((k, n))) * 2.0 ** (2 - 8 * s)
+        Pr, Pi = orc.zproduct(A, B, s, "4m")
+        Arn, Btn = _embedded_rows_nside(A, B)
+        Pn, *_ = brute.retained_exact(Arn, Btn, s)
+        Ara, Bta = _embedded_rows_aside(A, B)
+        Pa, *_ = brute.retained_exact(Ara, Bta, s)
+        for i in range(m):
+            for j in range(n):
+                for got, exn, exa in ((Pr[i, j], Pn[i][2 * j], Pa[i][j]),
+                                      (Pi[i, j], Pn[i][2 * j + 1], Pa[m + i][j])):
+                    u = Fraction(math.ulp(float(exn))) if exn != 0 else Fraction(0)
+                    assert abs(Fraction(got) - exn) <= u
+                    if abs(Fraction(got) - exa) > 2 * u:
+                        separated += 1
+    assert separated > 0
+
+
+# ---------------------------------------------- R7 quick return, complex beta
+@pytest.mark.parametrize("beta", [0.5 - 0.75j, -1.25 + 0.375j, 0.0 + 2.0j, -3.0 + 0.0j])
+def test_quick_complex_beta_exact(orc, beta):
+    """R7 quick return (alpha = 0 and k = 0) with a complex beta: C <- beta C.  Dyadic inputs
+    make every FP64 step of the fma shapes exact, so the result must equal the exact rational
+    product (Fraction) -- a sign or swapped index in the beta_i terms fails."""
+    g = synth.rng(77)
+    m, n = 5, 4
+    C = (g.integers(-64, 65, (m, n)) + 1j * g.integers(-64, 65, (m, n))) / 32.0
+    br, bi = Fraction(beta.real), Fraction(beta.imag)
+    want_r = [[br * Fraction(C[i, j].real) - bi * Fraction(C[i, j].imag) for j in range(n)] for i in range(m)]
+    want_i = [[br * Fraction(C[i, j].imag) + bi * Fraction(C[i, j].real) for j in range(n)] for i in range(m)]
+    A = synth.uniform(m, 3, 1, complex_=True)
+    B = synth.uniform(3, n, 2, complex_=True)
+    for out in (orc.zgemm("N", "N", 0.0, A, B, beta, C, 7, "4m"),
+                orc.zgemm("N", "N", 0.0, A, B, beta, C, 7, "3m"),
+                orc.zgemm("N", "N", 1.0 + 1.0j, A[:, :0], B[:0, :], beta, C, 7, "4m")):
+        for i in range(m):
+            for j in range(n):
+                assert Fraction(out[i, j].real) == want_r[i][j]
+                assert Fraction(out[i, j].imag) == want_i[i][j]
+
+
+def test_quick_complex_beta_rounded(orc):
+    """Non-dyadic data: each component of the quick return is within 2u (|br c| + |bi c'|) of
+    the exact beta C (R7's two fma shapes round at most twice)."""
+    m, n = 7, 6
+    C = synth.uniform(m, n, 5, complex_=True)
+    beta = 0.3 - 0.7j
+    out = orc.zgemm("N", "N", 0.0, np.zeros((m, 2), complex), np.zeros((2, n), complex), beta, C, 5)
+    br, bi = Fraction(beta.real), Fraction(beta.imag)
+    u = Fraction(2) ** -53
+    for i in range(m):
+        for j in range(n):
+            cr, ci = Fraction(C[i, j].real), Fraction(C[i, j].imag)
+            er, ei = br * cr - bi * ci, br * ci + bi * cr
+            assert abs(Fraction(out[i, j].real) - er) <= 2 * u * (abs(br * cr) + abs(bi * ci))
+            assert abs(Fraction(out[i, j].imag) - ei) <= 2 * u * (abs(br * ci) + abs(bi * cr))
+    # beta == 0: C not read (NaN-safe), zeros
+    Cn = np.full((m, n), np.nan + 1j * np.nan)
+    z = orc.zgemm("N", "N", 0.0, np.zeros((m, 2), complex), np.zeros((2, n), complex), 0.0, Cn, 5)
+    assert (z == 0).all()
