@@ -166,18 +166,20 @@ def _cuda(x, dtype, name):
 
 def _operands(dtype, A, B, C):
     """Type checks; resolves lazy conj / neg views of A and B (torch keeps them as a bit on the
-    tensor, the library would read the unconjugated storage); C must be a plain tensor.  All
-    three on one CUDA device, or all on the CPU (host offload).  Returns (A, B, device)."""
+    tensor, the library would read the unconjugated storage); C must be a plain tensor.  CUDA
+    operands share one device (all-CPU operands take the host offload).  Returns (A, B, device)."""
     for x, nm in ((A, "A"), (B, "B"), (C, "C")):
         _cuda(x, dtype, nm)
     if C.is_conj() or C.is_neg():
         raise ValueError("C must not be a lazily conjugated / negated view (resolve it first)")
-    A = A.resolve_conj().resolve_neg() if (A.is_conj() or A.is_neg()) else A
-    B = B.resolve_conj().resolve_neg() if (B.is_conj() or B.is_neg()) else B
-    devs = {x.device for x in (A, B, C)}
-    if len(devs) != 1:
-        raise ValueError(f"A, B and C must live on one device, got {sorted(map(str, devs))}")
-    return A, B, C.device
+    # (resolving materialises a copy, which torch lays out row-major: make it column-major again)
+    A = colmajor(A.resolve_conj().resolve_neg()) if (A.is_conj() or A.is_neg()) else A
+    B = colmajor(B.resolve_conj().resolve_neg()) if (B.is_conj() or B.is_neg()) else B
+    cuda = {x.device for x in (A, B, C) if x.device.type == "cuda"}
+    if len(cuda) > 1:
+        raise ValueError(f"A, B and C must live on one CUDA device, got {sorted(map(str, cuda))}")
+    # host / device mixes are refused by the library itself (OZAKI_ERR_UNSUPPORTED)
+    return A, B, (next(iter(cuda)) if cuda else C.device)
 
 
 def _on(device):
@@ -408,7 +410,8 @@ def debug_split(side, kind, trans, X, num_slices, stream=None):
     sl = torch.empty((s, rows_out, kdepth), dtype=torch.int8, device=X.device)
     ex = torch.empty((rows_out,), dtype=torch.int32, device=X.device)
     kd = ctypes.c_int64(0)
-    X = X.resolve_conj().resolve_neg()
+    if X.is_conj() or X.is_neg():
+        X = colmajor(X.resolve_conj().resolve_neg())
     with _on(X.device):
         _bind_stream(stream, X.device)
         rc = lib().ozaki_debug_split(_ch(side), _ch(kind), _ch(trans), rows, cols, X.data_ptr(), _ld(X),

@@ -1078,6 +1078,89 @@ int offload_ctx(OffloadCtx **out) {
     return 0;
 }
 
+// One large GEMM on host pointers (batch == 1): op(A) is staged once, then op(B) and C move
+// in column panels, double-buffered, so the H2D copy of panel p+1, the GEMM of panel p and the
+// D2H copy of panel p-1 overlap.  Row exponents come from full rows of op(A) and column
+// exponents are per column, so every element is computed exactly as by one call (bitwise).
+int run_offload_panels(const Call &c, int64_t panel) {
+    const size_t es = (c.kind == KIND_REAL) ? 8 : 16;
+    const int64_t ar = c.ta == 'N' ? c.m : c.k, ac = c.ta == 'N' ? c.k : c.m;
+    const int64_t spanA = (ac - 1) * c.lda + ar;
+    const bool readC = !(c.be[0] == 0.0 && c.be[1] == 0.0);
+    // one panel of op(B) columns j0..j0+w: 'N' -> w columns of B (pitch ldb, k rows each);
+    // 'T'/'C' -> w rows of B (pitch ldb, w elements each, k columns)
+    const int64_t bl = (c.tb == 'N') ? c.k : panel;   // device leading dimension of the B panel
+    const size_t bbytes = (size_t)panel * c.k * es, cbytes = (size_t)panel * c.m * es;
+    OffloadCtx *o = nullptr;
+    if (int rc = offload_ctx(&o)) return rc;
+    const size_t need = (size_t)spanA * es + 2 * (bbytes + cbytes);
+    if (o->cap < need) {
+        CUDA_TRY(cudaStreamSynchronize(o->d2h));
+        for (int i = 0; i < 2; ++i) {
+            if (o->buf[i]) cudaFree(o->buf[i]);
+            o->buf[i] = nullptr;
+        }
+        o->cap = 0;
+        cudaError_t e = cudaMalloc(&o->buf[0], need);
+        if (e != cudaSuccess) return fail(OZAKI_ERR_ALLOC, "offload staging (%zu B): %s", need, cudaGetErrorString(e));
+        o->cap = need;
+    }
+    char *base = o->buf[0];
+    double *dA = (double *)base;
+    char *pb[2] = {base + (size_t)spanA * es, base + (size_t)spanA * es + bbytes + cbytes};
+    cudaStream_t user = t_stream;
+    CUDA_TRY(cudaEventRecord(o->start, user));
+    CUDA_TRY(cudaStreamWaitEvent(o->h2d, o->start, 0));
+    CUDA_TRY(cudaMemcpyAsync(dA, c.A, (size_t)spanA * es, cudaMemcpyHostToDevice, o->h2d));
+    const int64_t np = (c.n + panel - 1) / panel;
+    int rc = 0;
+    for (int64_t p = 0; p < np && !rc; ++p) {
+        const int set = (int)(p & 1);
+        const int64_t j0 = p * panel, w = std::min<int64_t>(panel, c.n - j0);
+        double *dB = (double *)pb[set];
+        double *dC = (double *)(pb[set] + bbytes);
+        if (p >= 2) CUDA_TRY(cudaStreamWaitEvent(o->h2d, o->out_done[set], 0));   // panel set reuse
+        const char *hB = (const char *)c.B + (size_t)(c.tb == 'N' ? j0 * c.ldb : j0) * es;
+        if (c.tb == 'N')
+            CUDA_TRY(cudaMemcpy2DAsync(dB, (size_t)bl * es, hB, (size_t)c.ldb * es, (size_t)c.k * es, (size_t)w,
+                                       cudaMemcpyHostToDevice, o->h2d));
+        else
+            CUDA_TRY(cudaMemcpy2DAsync(dB, (size_t)bl * es, hB, (size_t)c.ldb * es, (size_t)w * es, (size_t)c.k,
+                                       cudaMemcpyHostToDevice, o->h2d));
+        char *hC = (char *)c.C + (size_t)j0 * c.ldc * es;
+        if (readC)
+            CUDA_TRY(cudaMemcpy2DAsync(dC, (size_t)c.m * es, hC, (size_t)c.ldc * es, (size_t)c.m * es, (size_t)w,
+                                       cudaMemcpyHostToDevice, o->h2d));
+        CUDA_TRY(cudaEventRecord(o->in_done[set], o->h2d));
+        CUDA_TRY(cudaStreamWaitEvent(o->comp, o->in_done[set], 0));
+        Call d = c;
+        d.A = dA;
+        d.B = dB;
+        d.ldb = bl;
+        d.C = dC;
+        d.ldc = c.m;
+        d.n = w;
+        d.sA = d.sB = d.sC = 0;
+        t_stream = o->comp;
+        const int ovs = t_overlap;
+        t_overlap = 0;
+        rc = run(d);
+        t_overlap = ovs;
+        t_stream = user;
+        if (rc) break;
+        CUDA_TRY(cudaEventRecord(o->comp_done[set], o->comp));
+        CUDA_TRY(cudaStreamWaitEvent(o->d2h, o->comp_done[set], 0));
+        CUDA_TRY(cudaMemcpy2DAsync(hC, (size_t)c.ldc * es, dC, (size_t)c.m * es, (size_t)c.m * es, (size_t)w,
+                                   cudaMemcpyDeviceToHost, o->d2h));
+        CUDA_TRY(cudaEventRecord(o->out_done[set], o->d2h));
+    }
+    cudaEventRecord(o->start, o->d2h);
+    cudaStreamWaitEvent(user, o->start, 0);
+    cudaError_t e = cudaStreamSynchronize(o->d2h);
+    if (!rc && e != cudaSuccess) rc = fail(OZAKI_ERR_CUDA, "offload: %s", cudaGetErrorString(e));
+    return rc;
+}
+
 int run_offload(const Call &c) {
     const size_t es = (c.kind == KIND_REAL) ? 8 : 16;
     const int64_t ar = c.ta == 'N' ? c.m : c.k, ac = c.ta == 'N' ? c.k : c.m;
@@ -1550,6 +1633,14 @@ int run(const Call &c0) {
             if (!(ka == PTR_HOST && kb == PTR_HOST && kc == PTR_HOST))
                 return fail(OZAKI_ERR_UNSUPPORTED, "A, B, C must all be device or all be host pointers");
             if (!readsAB && c.be[0] == 1.0 && c.be[1] == 0.0) return 0;   // quick return, C unchanged
+            if (readsAB && c.batch == 1) {
+                // one large GEMM: column panels of ~32 MB of op(B) (multiples of the 128-column tile)
+                const size_t es = (c.kind == KIND_REAL) ? 8 : 16;
+                int64_t panel = (int64_t)((32ull << 20) / std::max<size_t>(1, (size_t)(c.k + c.m) * es));
+                if (const char *pe = getenv("OZAKI_OFFLOAD_PANEL_COLS")) panel = atoll(pe);
+                panel = std::max<int64_t>(128, panel / 128 * 128);
+                if (c.n >= 2 * panel) return run_offload_panels(c, panel);
+            }
             return run_offload(c);   // (alpha == 0 or k == 0: C = beta C staged through k_scale_*)
         }
     }

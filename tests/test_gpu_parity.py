@@ -465,3 +465,35 @@ def test_lazy_conj_views(orc):
     assert same(C.cpu().numpy(), orc.zgemm("C", "N", 1.0, A, np.conj(B), 0.0, None, 7))
     with pytest.raises(ValueError):
         oz.zgemm("N", "N", 1.0, Ad.mH, Bd, 0.0, C.conj(), 7)
+
+
+@pytest.mark.parametrize("ta,tb", [("N", "N"), ("T", "T"), ("N", "C")])
+def test_host_offload_column_panels(orc, ta, tb, monkeypatch):
+    """One large GEMM on host pointers moves op(B) and C in column panels (H2D / GEMM / D2H
+    overlapped): forced 128-column panels (6 panels, ragged last), transposes, beta != 0 and
+    ldc > m -- bitwise equal to the oracle, padding rows of C untouched."""
+    monkeypatch.setenv("OZAKI_OFFLOAD_PANEL_COLS", "128")
+    m, n, k, ld, s = 300, 700, 90, 333, 6
+    Aop = synth.uniform(m, k, seed=31, complex_=True)
+    Bop = synth.spread(k, n, seed=32, phi=1.0, complex_=True)
+    C0 = synth.uniform(m, n, seed=33, complex_=True)
+    A = Aop if ta == "N" else (Aop.T.copy() if ta == "T" else np.conj(Aop.T).copy())
+    B = Bop if tb == "N" else (Bop.T.copy() if tb == "T" else np.conj(Bop.T).copy())
+    big = torch.full((n, ld), 5.0 + 0j, dtype=torch.complex128).pin_memory()
+    big.t()[:m, :] = torch.from_numpy(C0)
+    Cv = big.t()[:m, :]
+    hA = torch.from_numpy(np.ascontiguousarray(A.T)).t()
+    hB = torch.from_numpy(np.ascontiguousarray(B.T)).t()
+    oz.zgemm(ta, tb, 0.5 + 0.25j, hA, hB, -1.0, Cv, s)
+    assert same(Cv.numpy(), orc.zgemm("N", "N", 0.5 + 0.25j, Aop, Bop, -1.0, C0, s))
+    assert (big.t()[m:, :] == 5.0).all()
+    # real DGEMM, beta = 0 (C not read), Ozaki-II through the same panels
+    Ar, Br = Aop.real.copy(), Bop.real.copy()
+    Cr = torch.full((n, m), float("nan"), dtype=torch.float64).t()
+    oz.dgemm("N", "N", 1.0, torch.from_numpy(np.asfortranarray(Ar)), torch.from_numpy(np.asfortranarray(Br)),
+             0.0, Cr, s)
+    assert same(Cr.numpy(), orc.dgemm("N", "N", 1.0, Ar, Br, 0.0, None, s))
+    from oracle import ozaki2 as o2
+    oz.ozaki2_dgemm("N", "N", 1.0, torch.from_numpy(np.asfortranarray(Ar)), torch.from_numpy(np.asfortranarray(Br)),
+                    0.0, Cr, 14)
+    assert same(Cr.numpy()[:40], o2.dgemm("N", "N", 1.0, Ar[:40], Br, 0.0, None, 14))
