@@ -61,6 +61,16 @@ struct GemmParams {
     int32_t chunk_mode;
     double *W;
     int64_t w_lvl;
+    // Split-K for small problems: the CTA pairs run splitk work units per
+    // tile, unit u = (tile u / splitk, split q = u % splitk) over an equal share of the
+    // k-blocks; each writes its EXACT partials -- the int64 prefix of the first pass's levels
+    // (R6's exact part) to P0 and the int32 sums of the later levels to PL -- and
+    // k_splitk_combine adds them (integers: order-free) and runs the FP64 combine + store.
+    // Layout: P0[q][b][col][row], PL[q][li][b][col][row] (li = later level index).
+    int32_t splitk;
+    int32_t pk_nl;         // later levels per unit (PL planes)
+    int64_t *P0;
+    int32_t *PL;
     unsigned long long *dbg;   // optional per-CTA role timers (ozaki_debug_timing), null = off
 };
 
@@ -79,7 +89,8 @@ enum DbgSlot : int {
     DBG_EPI_FIRST_ARRIVE,// pass_full -> first slot released, first pass (warp 2)
     DBG_MMA_WAIT_FULL0,  // part of DBG_MMA_WAIT_FULL at the first k-block of a pass
     DBG_MMA_WAIT_FULLP0, // part of DBG_MMA_WAIT_FULL inside pass 0
-    DBG_NSLOT
+    DBG_TL0 = 32,        // timeline of CTA 0 (globaltimer ns): slots DBG_TL0 + event
+    DBG_NSLOT = 48
 };
 
 // debug timers (cold path): accumulate straight into the device buffer so no

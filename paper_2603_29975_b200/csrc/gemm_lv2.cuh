@@ -32,6 +32,29 @@ struct Lv2Params {
     CUtensorMap tmB[kMaxPassMaps];        // B slices (64-row tiles), box = 8 n rows
 };
 
+// Debug timeline (ozaki_debug_timing): globaltimer at fixed events of CTA 0.
+enum TlEvent : int { TL_ENTRY = 0, TL_PROLOGUE, TL_DEPWAIT, TL_TMA0, TL_FULL0, TL_MMA_PASS0, TL_MMA_END,
+                     TL_EPI_PASS0, TL_EPI_LAST, TL_EPI_STORE, TL_EXIT };
+__device__ __forceinline__ void tl_mark(const GemmParams &p, int ev) {
+    if (p.dbg && blockIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.dbg[DBG_TL0 + ev] = t;
+    }
+}
+
+// Work unit u of the persistent loop: tile u / splitk, k-blocks of split u % splitk (an equal
+// share of [kb_begin, kb_end); splitk == 1 is the whole range).
+__device__ __forceinline__ void lv2_unit(const GemmParams &p, int64_t u, int64_t &tile, int64_t &kb0,
+                                         int64_t &kb1, int &q) {
+    const int sk = p.splitk;
+    tile = u / sk;
+    q = (int)(u - tile * sk);
+    const int64_t span = p.kb_end - p.kb_begin;
+    kb0 = p.kb_begin + span * q / sk;
+    kb1 = p.kb_begin + span * (q + 1) / sk;
+}
+
 template <int S, bool FULL = false>
 __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem, uint64_t *full,
                                              uint64_t *empty, uint64_t *pass_full,
@@ -40,24 +63,28 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
     constexpr uint32_t idesc = idesc_i8(256, kLvBN);
     const LvParams &lp = P2.lv;
     const GemmParams &p = lp.g;
-    const int64_t total = p.batch * p.tiles_m * p.tiles_n;   // super-tiles (256 x 128)
+    const int64_t total = p.batch * p.tiles_m * p.tiles_n * p.splitk;   // units of super-tiles (256 x 128)
     const int Sg = p.stages;
     uint32_t stage = 0, phase = 0;
     uint32_t slot_par = (1u << kSlots) - 1u;    // bit j: parity to wait for on slot j
     const long long t_begin = p.dbg ? clock64() : 0;
     const uint64_t dA = smem_desc_kmajor_noswz(0, 128, 256);   // 128-row A operand per CTA
     const uint64_t dB = smem_desc_kmajor_noswz(0, 128, 256);   // 64-row B half per CTA
-    for (int64_t tile = blockIdx.x >> 1; tile < total; tile += gridDim.x >> 1) {
+    for (int64_t u = blockIdx.x >> 1; u < total; u += gridDim.x >> 1) {
+        int64_t tile, ub, ue;
+        int q;
+        lv2_unit(p, u, tile, ub, ue, q);
 #pragma unroll
         for (int ps = 0; ps < PP.npass; ++ps) {
             const int hi = PP.hi[ps], lo = PP.lo[ps], tlo = PP.tlo[ps], n = PP.n[ps];
             const uint32_t abytes = (uint32_t)n * kBlk, bbytes = (uint32_t)n * (kBlk / 2);
             const int kpp = lp.pass[ps].kpp;
-            for (int64_t kb0 = p.kb_begin; kb0 < p.kb_end; kb0 += kpp) {
-                const int nk = (int)min((int64_t)kpp, p.kb_end - kb0);
-                const bool kfirst = (kb0 == p.kb_begin);
+            for (int64_t kb0 = ub; kb0 < ue; kb0 += kpp) {
+                const int nk = (int)min((int64_t)kpp, ue - kb0);
+                const bool kfirst = (kb0 == ub);
                 long long w0 = p.dbg ? clock64() : 0;
                 mbar_wait(&full[stage], phase);
+                if (kfirst && ps == 0 && u == (blockIdx.x >> 1)) tl_mark(p, TL_FULL0);
                 if (p.dbg && (threadIdx.x & 31) == 0) {
                     const long long dw = clock64() - w0;
                     dbg_add(p, DBG_MMA_WAIT_FULL, dw);
@@ -105,14 +132,17 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
                 if (++stage == (uint32_t)Sg) { stage = 0; phase ^= 1; }
             }
             mma_commit_pair_elect(pass_full);
+            if (ps == 0 && u == (blockIdx.x >> 1)) tl_mark(p, TL_MMA_PASS0);
         }
     }
+    tl_mark(p, TL_MMA_END);
     if (p.dbg && (threadIdx.x & 31) == 0) dbg_add(p, DBG_MMA_TOTAL, clock64() - t_begin);
 }
 
 // CHUNK (compile time, reading R8): 0 = whole K in one INT32 accumulation;
 // 1 = first/middle K chunk (W = S or W += S, nothing stored to C);
-// 2 = last K chunk (level sum = W + S, then the FP64 combine and store).
+// 2 = last K chunk (level sum = W + S, then the FP64 combine and store);
+// 3 = split-K unit (exact partials to P0 / PL, k_splitk_combine finishes).
 // FULL (reading R21, NEXT-4): all s^2 pairs, levels 2s .. 2 (s <= 8, CHUNK 0 only).
 template <int EPI, int CHUNK, bool FULL = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
@@ -133,7 +163,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     const uint32_t rank = cluster_ctarank();
     const int s = p.s;
     const int Lmax = FULL ? 2 * s : s + 1;   // levels Lmax (least significant) .. 2 (R1 / R21)
-    const int64_t total = p.batch * p.tiles_m * p.tiles_n;
+    const int64_t total = p.batch * p.tiles_m * p.tiles_n * p.splitk;   // work units
+    if (threadIdx.x == 0) tl_mark(p, TL_ENTRY);
 
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < S; ++i) {
@@ -153,9 +184,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     cluster_sync();          // barriers of both CTAs initialised, TMEM allocated
     tc_fence_after();
     const uint32_t tbase = *tholder;
+    if (threadIdx.x == 0) tl_mark(p, TL_PROLOGUE);
     // Programmatic dependent launch: the prologue above overlaps the producer kernel's tail
     // (K1); everything below reads its output (slices, exponents), so wait for its completion.
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x == 0) tl_mark(p, TL_DEPWAIT);
     // ... and let a dependent launched with PDL (the next call's split, ozaki_set_overlap) start
     // on the SMs this grid's last wave leaves idle; it orders itself after this grid (split_fast.cuh)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -164,8 +197,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         // ========================= producer (both CTAs): own A rows, own B half
         if (lane == 0) {
             uint32_t stage = 0, phase = 0;
-            for (int64_t tile = blockIdx.x >> 1; tile < total; tile += gridDim.x >> 1) {
-                int64_t b, tm, tn;
+            for (int64_t u = blockIdx.x >> 1; u < total; u += gridDim.x >> 1) {
+                int64_t tile, ub, ue, b, tm, tn;
+                int q;
+                lv2_unit(p, u, tile, ub, ue, q);
                 decode_tile(p, tile, b, tm, tn);
                 // A tiles of 128 rows: this CTA's is 2*tm + rank;  B tiles of 64 rows: 2*tn + rank
                 const int64_t arow0 = ((b * (2 * p.tiles_m) + 2 * tm + rank) * p.KB) * (int64_t)s * (kBlk / 256);
@@ -173,8 +208,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 for (int ps = 0; ps < lp.npass; ++ps) {
                     const LvPass pa = lp.pass[ps];
                     const uint32_t abytes = (uint32_t)pa.n * kBlk, bbytes = (uint32_t)pa.n * (kBlk / 2);
-                    for (int64_t kb0 = p.kb_begin; kb0 < p.kb_end; kb0 += pa.kpp) {
-                        const int nk = (int)min((int64_t)pa.kpp, p.kb_end - kb0);
+                    for (int64_t kb0 = ub; kb0 < ue; kb0 += pa.kpp) {
+                        const int nk = (int)min((int64_t)pa.kpp, ue - kb0);
                         const long long w0 = p.dbg ? clock64() : 0;
                         mbar_wait(&empty[stage], phase ^ 1);
                         if (p.dbg) dbg_add(p, DBG_PROD_WAIT, clock64() - w0);
@@ -189,6 +224,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                             tma_load_2d_pair(dst + abytes, &P2.tmB[ps], 0, rb, leader_full);
                             dst += abytes + bbytes;
                         }
+                        if (u == (blockIdx.x >> 1) && ps == 0 && kb0 == ub) tl_mark(p, TL_TMA0);
                         if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
                     }
                 }
@@ -226,8 +262,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         const bool dbgw = p.dbg && warp == 2 && lane == 0;
         // slot_empty barriers are consecutive 8-byte words: remote address = base + 8 j
         const uint32_t slot_remote0 = mapa_shared(smem_u32(&slot_empty[0]), 0);
-        for (int64_t tile = blockIdx.x >> 1; tile < total; tile += gridDim.x >> 1) {
-            int64_t b, tm, tn;
+        for (int64_t u = blockIdx.x >> 1; u < total; u += gridDim.x >> 1) {
+            int64_t tile, ub, ue, b, tm, tn;
+            int sq;
+            lv2_unit(p, u, tile, ub, ue, sq);
             decode_tile(p, tile, b, tm, tn);
             const int64_t grow = (2 * tm + rank) * kBM + q * 32 + lane;
             const int32_t e = (grow < p.Mp) ? __ldg(p.ea + b * p.Mp + grow) : 0;
@@ -238,11 +276,86 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 const LvPass pa = lp.pass[ps];
                 long long w0 = p.dbg ? clock64() : 0;
                 mbar_wait(pass_full, pphase);
+                if (dbgw && u == (blockIdx.x >> 1)) tl_mark(p, ps == 0 ? TL_EPI_PASS0 : TL_EPI_LAST);
                 long long w1 = p.dbg ? clock64() : 0;
                 if (dbgw) dbg_add(p, DBG_EPI_WAIT, w1 - w0);
                 pphase ^= 1;
                 tc_fence_after();
-                if constexpr (CHUNK == 0 && EPI != EPI_LEVELS) {
+                if constexpr (CHUNK == 3) {
+                    // split-K unit: exact partials of this unit's k-blocks, no FP64.  Pass 0 -> the
+                    // int64 prefix X = sum_j S_j 2^(8j) of its levels (the exact part of R6, < 2^55
+                    // per unit; the units' X add exactly in int64); later levels -> int32 sums.
+                    const int nlev = pa.hi - pa.lo + 1;
+                    const int np0 = lp.pass[0].hi - lp.pass[0].lo + 1;
+                    const int64_t c0 = tn * kLvBN + half * kNC2;
+                    const bool rok = grow < p.Mp;
+                    const int64_t plane = p.batch * p.N * p.Mp;
+                    const int64_t off = (b * p.N + c0) * p.Mp + grow;
+                    uint32_t v[16];
+                    if (ps == 0) {
+                        long long t0[16], t1[16];
+                        tmem_ld_32x32b_x16(tl, v);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) t0[i] = (long long)(int)v[i];
+#pragma unroll 1
+                        for (int j = 1; j < nlev; ++j) {
+                            tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN), v);
+                            tmem_wait_ld();
+                            const int w = 1 << (8 * j);
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) t0[i] += (long long)(int)v[i] * w;
+                        }
+                        tmem_ld_32x32b_x16(tl + 16u, v);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) t1[i] = (long long)(int)v[i];
+#pragma unroll 1
+                        for (int j = 1; j < nlev; ++j) {
+                            tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + 16), v);
+                            tmem_wait_ld();
+                            const int w = 1 << (8 * j);
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) t1[i] += (long long)(int)v[i] * w;
+                        }
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0)
+                            for (int j = 0; j < nlev; ++j) mbar_arrive_cluster(slot_remote0 + 8u * (uint32_t)j);
+                        if (rok) {
+                            long long *dst = reinterpret_cast<long long *>(p.P0) + (int64_t)sq * plane + off;
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (c0 + i < p.N) dst[(int64_t)i * p.Mp] = t0[i];
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (c0 + 16 + i < p.N) dst[(int64_t)(16 + i) * p.Mp] = t1[i];
+                        }
+                    } else {
+#pragma unroll 1
+                        for (int j = 0; j < nlev; ++j) {
+                            const int li = (Lmax - np0) - (pa.hi - j);
+                            int32_t *dst = p.PL + ((int64_t)sq * p.pk_nl + li) * plane + off;
+                            tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN), v);
+                            tmem_wait_ld();
+                            if (rok) {
+#pragma unroll
+                                for (int i = 0; i < 16; ++i)
+                                    if (c0 + i < p.N) dst[(int64_t)i * p.Mp] = (int32_t)v[i];
+                            }
+                            tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + 16), v);
+                            tmem_wait_ld();
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_cluster(slot_remote0 + 8u * (uint32_t)j);
+                            if (rok) {
+#pragma unroll
+                                for (int i = 0; i < 16; ++i)
+                                    if (c0 + 16 + i < p.N) dst[(int64_t)(16 + i) * p.Mp] = (int32_t)v[i];
+                            }
+                        }
+                    }
+                } else if constexpr (CHUNK == 0 && EPI != EPI_LEVELS) {
                     // one software pipeline over the pass: chunk c = (level c/2, 16-column
                     // group c%2), the load of chunk c+1 in flight while chunk c is combined;
                     // a level's TMEM slot is released as soon as both its groups are in
@@ -374,18 +487,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 if (dbgw) dbg_add(p, DBG_EPI_DRAIN, clock64() - w1);
             }
             const long long s0 = p.dbg ? clock64() : 0;
-            if constexpr (EPI != EPI_LEVELS && CHUNK != 1)
+            if constexpr (EPI != EPI_LEVELS && CHUNK != 1 && CHUNK != 3)
                 lv_store<EPI, kNC2>(p, b, grow, e, tn * kLvBN + half * kNC2, acc, CHUNK == 0 ? -8 * (Lmax - 2) : 0);
             if (dbgw) dbg_add(p, DBG_EPI_STORE, clock64() - s0);
+            if (dbgw) tl_mark(p, TL_EPI_STORE);
         }
     }
 
     tc_fence_before();
     cluster_sync();          // all MMAs done and all TMEM reads of both CTAs finished
+    if (threadIdx.x == 0) tl_mark(p, TL_EXIT);
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc_pair(tbase, 512);
     }
+}
+
+// Split-K combine (CHUNK == 3 units wrote the partials): one thread per (row, NC = 2 product
+// columns: one complex element for 4M), warps over 32 consecutive rows (coalesced partial
+// reads), enough threads to keep the reads in flight.  The level sums are the integer sums of
+// the units' partials (order-free); acc = RNE53(X) then R6's FMAs in the pass order, exactly as
+// the unsplit epilogue, and the same store (lv_store).
+template <int EPI>
+__global__ void __launch_bounds__(128) k_splitk_combine(const __grid_constant__ GemmParams p, int Lmax, int np0) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    constexpr int NC = 2;
+    const int64_t b = blockIdx.z;
+    const int64_t grow = (int64_t)blockIdx.y * 128 + threadIdx.x;
+    const int64_t col0 = (int64_t)blockIdx.x * NC;
+    const bool rok = grow < p.Mp;
+    const int32_t e = rok ? __ldg(p.ea + b * p.Mp + grow) : 0;
+    const int64_t plane = p.batch * p.N * p.Mp;
+    const int64_t off = (b * p.N + col0) * p.Mp + grow;
+    const int sk = p.splitk, nl = p.pk_nl;
+    const bool ok0 = rok && col0 < p.N, ok1 = rok && col0 + 1 < p.N;
+    long long X0 = 0, X1 = 0;
+    {
+        const long long *x = reinterpret_cast<const long long *>(p.P0) + off;
+#pragma unroll 4
+        for (int q = 0; q < sk; ++q) {
+            if (ok0) X0 += __ldg(x + (int64_t)q * plane);
+            if (ok1) X1 += __ldg(x + (int64_t)q * plane + p.Mp);
+        }
+    }
+    double acc[NC] = {__ll2double_rn(X0), __ll2double_rn(X1)};
+    for (int li = 0; li < nl; ++li) {
+        const double sc = pow2(8 * (np0 + li));   // level L = Lmax - np0 - li weighs 2^(8(Lmax-L))
+        const int32_t *y = p.PL + (int64_t)li * plane + off;
+        uint32_t S0 = 0, S1 = 0;
+#pragma unroll 4
+        for (int q = 0; q < sk; ++q) {
+            if (ok0) S0 += (uint32_t)__ldg(y + (int64_t)q * nl * plane);
+            if (ok1) S1 += (uint32_t)__ldg(y + (int64_t)q * nl * plane + p.Mp);
+        }
+        acc[0] = __fma_rn(i32_to_f64(S0), sc, acc[0]);
+        acc[1] = __fma_rn(i32_to_f64(S1), sc, acc[1]);
+    }
+    lv_store<EPI, NC>(p, b, grow, e, col0, acc, -8 * (Lmax - 2));
 }
 
 }  // namespace ozk

@@ -220,6 +220,8 @@ int64_t rup(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 enum Kind { KIND_REAL = 0, KIND_4M = 1, KIND_3M = 2 };
 
+size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
 // ------------------------------------------------------------------- plan
 struct Plan {
     int s, BN;
@@ -241,7 +243,33 @@ struct Plan {
     int npass;
     uint32_t stage_bytes;
     LvPass pass[kMaxPass];
+    int splitk = 1;          // split-K units per tile (a7: small problems, CHUNK 3 + k_splitk_combine)
+    int pk_np = 0, pk_nl = 0;   // prefix levels (pass 0) / later levels of the split-K partials
+    size_t p0_bytes = 0, pl_bytes = 0;
 };
+
+// Split-K: when the super-tiles leave more than half of the CTA pairs idle,
+// every tile is cut into S units over equal shares of the k-blocks (>= 4 k-blocks each), so
+// up to all pairs work; the units' exact integer partials are added by k_splitk_combine.
+// OZAKI_SPLITK=n forces S (tests; 1 = off).
+void plan_splitk(Plan &P, int sms) {
+    P.splitk = 1;
+    if (!P.pair || P.kchunk_needed || P.batch == 0) return;
+    const int64_t tiles = P.batch * P.tiles_m * P.tiles_n, pairs = sms / 2;
+    int64_t S = 1;
+    if (const char *e = getenv("OZAKI_SPLITK")) {
+        S = std::max<int64_t>(1, std::min<int64_t>(atoll(e), P.KB));
+    } else if (2 * tiles <= pairs) {
+        S = std::min<int64_t>({pairs / tiles, P.KB / 4, 16});
+    }
+    if (S <= 1) return;
+    P.splitk = (int)S;
+    P.pk_np = P.pass[0].hi - P.pass[0].lo + 1;
+    P.pk_nl = (P.full ? 2 * P.s : P.s + 1) - 1 - P.pk_np;
+    const size_t elems = (size_t)P.batch * P.Mp * P.Np;
+    P.p0_bytes = al256((size_t)S * elems * 8);
+    P.pl_bytes = al256((size_t)S * P.pk_nl * elems * 4);
+}
 
 // Pass plan of the level-pass kernel: make_pass_plan (passplan.cuh, shared
 // with the device code) plus the per-pass k-blocks per stage.
@@ -276,8 +304,6 @@ int kernel_choice() {
     }
     return choice;
 }
-
-size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 int make_plan(Kind kind, int64_t m, int64_t n, int64_t k, int64_t batch, int s, Plan &P, bool full = false) {
     P.s = s;
@@ -752,7 +778,7 @@ int launch_gemm_lv2(const Plan &P, const GemmParams &gp, size_t a_avail, size_t 
         if (int rc = rows_map(&P2.tmA[q], gp.A, a_avail, (uint32_t)P.pass[q].n * (kBlk / 256))) return rc;
         if (int rc = rows_map(&P2.tmB[q], gp.B, b_avail, (uint32_t)P.pass[q].n * (kBlk / 512))) return rc;
     }
-    const int64_t tiles = gp.batch * gp.tiles_m * gp.tiles_n;
+    const int64_t tiles = gp.batch * gp.tiles_m * gp.tiles_n * gp.splitk;   // work units
     const unsigned pairs = (unsigned)std::min<int64_t>(tiles, dev->sms / 2);
     {
         ProfScope ps(st, PH_GEMM);
@@ -848,10 +874,45 @@ int launch_gemm_chunked(const Plan &P, const GemmParams &g0, int epi, int64_t kc
     return rc;
 }
 
+// Split-K launch: one GEMM over tiles x S units writing exact partials (CHUNK 3), then
+// k_splitk_combine (PDL: its launch overlaps the GEMM's tail) sums them and stores C.
+int launch_gemm_splitk(const Plan &P, GemmParams gp, int epi, int64_t *P0, int32_t *PL, DevState *dev,
+                       cudaStream_t st) {
+    gp.splitk = P.splitk;
+    gp.pk_nl = P.pk_nl;
+    gp.P0 = P0;
+    gp.PL = PL;
+    int rc = P.full ? launch_gemm_lv2<EPI_REAL, 3, true>(P, gp, P.a_bytes, P.b_bytes, dev, st)
+                    : launch_gemm_lv2<EPI_REAL, 3, false>(P, gp, P.a_bytes, P.b_bytes, dev, st);
+    if (rc) return rc;
+    const int Lmax = P.full ? 2 * P.s : P.s + 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((P.Np + 1) / 2), (unsigned)((P.Mp + 127) / 128), (unsigned)P.batch);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = getenv("OZAKI_NO_PDL") ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    {
+        ProfScope ps(st, PH_OTHER);
+        if (epi == EPI_CPLX4M)
+            CUDA_TRY(cudaLaunchKernelEx(&cfg, k_splitk_combine<EPI_CPLX4M>, gp, Lmax, P.pk_np));
+        else
+            CUDA_TRY(cudaLaunchKernelEx(&cfg, k_splitk_combine<EPI_REAL>, gp, Lmax, P.pk_np));
+    }
+    g_stats.launches += 1;
+    return 0;
+}
+
 int launch_gemm(const Plan &P, int epi, const int8_t *sa, const int8_t *sb, const int32_t *ea,
                 const int32_t *fb, double *C, int64_t ldc, int64_t strideC, const double al[2],
-                const double be[2], int32_t *S_out, DevState *dev, cudaStream_t st) {
+                const double be[2], int32_t *S_out, DevState *dev, cudaStream_t st,
+                int64_t *P0 = nullptr, int32_t *PL = nullptr) {
     GemmParams gp{};
+    gp.splitk = 1;
     gp.A = sa;
     gp.B = sb;
     gp.ea = ea;
@@ -893,6 +954,8 @@ int launch_gemm(const Plan &P, int epi, const int8_t *sa, const int8_t *sb, cons
         const int64_t kc_env = ev ? atoll(ev) : 0;
         if ((P.kchunk_needed || kc_env > 0) && epi != EPI_LEVELS)
             return launch_gemm_chunked(P, gp, epi, kc_env, dev, st);
+        if (P.splitk > 1 && epi != EPI_LEVELS && P0 && PL)
+            return launch_gemm_splitk(P, gp, epi, P0, PL, dev, st);
         if (P.full) {   // R21: all s^2 pairs (planned only without K-chunking)
             if (epi == EPI_REAL) return launch_gemm_lv2<EPI_REAL, 0, true>(P, gp, P.a_bytes, P.b_bytes, dev, st);
             if (epi == EPI_CPLX4M) return launch_gemm_lv2<EPI_CPLX4M, 0, true>(P, gp, P.a_bytes, P.b_bytes, dev, st);
@@ -1634,9 +1697,10 @@ int run(const Call &c0) {
                 return fail(OZAKI_ERR_UNSUPPORTED, "A, B, C must all be device or all be host pointers");
             if (!readsAB && c.be[0] == 1.0 && c.be[1] == 0.0) return 0;   // quick return, C unchanged
             if (readsAB && c.batch == 1) {
-                // one large GEMM: column panels of ~32 MB of op(B) (multiples of the 128-column tile)
+                // one large GEMM: column panels of ~96 MB of op(B) + C (multiples of the 128-column
+                // tile; every panel call re-splits op(A), so panels are not made smaller)
                 const size_t es = (c.kind == KIND_REAL) ? 8 : 16;
-                int64_t panel = (int64_t)((32ull << 20) / std::max<size_t>(1, (size_t)(c.k + c.m) * es));
+                int64_t panel = (int64_t)((96ull << 20) / std::max<size_t>(1, (size_t)(c.k + c.m) * es));
                 if (const char *pe = getenv("OZAKI_OFFLOAD_PANEL_COLS")) panel = atoll(pe);
                 panel = std::max<int64_t>(128, panel / 128 * 128);
                 if (c.n >= 2 * panel) return run_offload_panels(c, panel);
@@ -1733,10 +1797,11 @@ int run(const Call &c0) {
     // 3M: the three real products run as 3 x batch entries of ONE plan / split / GEMM launch
     const int64_t pbatch = (c.kind == KIND_3M) ? 3 * c.batch : c.batch;
     if (int rc = make_plan(pk, c.m, c.n, c.k, pbatch, c.s, P, c.full)) return rc;
+    if (!c.S_out) plan_splitk(P, dev->sms);
     size_t ws = plan_workspace(P);
     size_t t_bytes = 0;
     if (c.kind == KIND_3M) t_bytes = al256(sizeof(double) * c.m * c.n * c.batch);
-    ws += 3 * t_bytes;
+    ws += 3 * t_bytes + P.p0_bytes + P.pl_bytes;
 
     // cross-call overlap (ozaki_set_overlap): one split + one GEMM launch, slices in the
     // alternate persistent workspace; the split may start under the previous call's GEMM
@@ -1765,6 +1830,8 @@ int run(const Call &c0) {
     int32_t *ea = (int32_t *)(sb + P.b_bytes);
     int32_t *fb = (int32_t *)((char *)ea + P.ea_bytes);
     double *T = (double *)((char *)fb + P.fb_bytes);
+    int64_t *P0 = P.splitk > 1 ? (int64_t *)((char *)T + 3 * t_bytes) : nullptr;
+    int32_t *PL = P.splitk > 1 ? (int32_t *)((char *)P0 + P.p0_bytes) : nullptr;
     int rc = 0;
 
     if (c.kind == KIND_REAL || c.kind == KIND_4M) {
@@ -1783,14 +1850,14 @@ int run(const Call &c0) {
         t_split_pdl = t_split_early = false;
         if (!rc) {
             const int epi = c.S_out ? EPI_LEVELS : (c.kind == KIND_4M ? EPI_CPLX4M : EPI_REAL);
-            rc = launch_gemm(P, epi, sa, sb, ea, fb, c.C, c.ldc, c.sC, c.al, c.be, c.S_out, dev, st);
+            rc = launch_gemm(P, epi, sa, sb, ea, fb, c.C, c.ldc, c.sC, c.al, c.be, c.S_out, dev, st, P0, PL);
         }
     } else {   // 3M: one fused split per operand (Re, Im, fl(Re+Im) regions) and ONE GEMM launch
                // over 3 x batch entries into T = [T1 | T2 | T3], then the combine
         const double one[2] = {1.0, 0.0}, zero[2] = {0.0, 0.0};
         rc = launch_split_ab(P, view_A(c.A, c.ta, c.m, c.k, c.lda, c.sA, SPLIT_3M), sa, ea,
                              view_B(c.B, c.tb, c.n, c.k, c.ldb, c.sB, SPLIT_3M), sb, fb, dev, st, c.batch);
-        if (!rc) rc = launch_gemm(P, EPI_REAL, sa, sb, ea, fb, T, c.m, c.m * c.n, one, zero, nullptr, dev, st);
+        if (!rc) rc = launch_gemm(P, EPI_REAL, sa, sb, ea, fb, T, c.m, c.m * c.n, one, zero, nullptr, dev, st, P0, PL);
         if (!rc) {
             dim3 grid(grid1d(c.m * c.n, dev->sms), 1, (unsigned)c.batch);
             ProfScope ps(st, PH_OTHER);

@@ -1,0 +1,49 @@
+"""Timeline of CTA 0 of the pair GEMM (globaltimer ns, relative to kernel entry) for small
+problems: where the fixed per-launch time goes.  usage: python tools/gemm_timeline.py"""
+import ctypes
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+import paper_2603_29975_b200 as oz  # noqa: E402
+
+EV = ["entry", "prologue", "depwait", "tma0_issued", "full0", "mma_pass0_done", "mma_end", "epi_pass0",
+      "epi_last_pass", "epi_store_done", "exit"]
+
+
+def dev(x):
+    return oz.colmajor(torch.from_numpy(np.asfortranarray(x)).cuda())
+
+
+def timeline(name, fn):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    L = oz.lib()
+    buf = (ctypes.c_uint64 * 48)()
+    L.ozaki_debug_timing(1, buf, 48)
+    fn()
+    torch.cuda.synchronize()
+    L.ozaki_debug_timing(0, buf, 48)
+    t = [int(buf[32 + i]) for i in range(len(EV))]
+    t0 = t[0]
+    print(json.dumps({"case": name, **{e: (round((v - t0) / 1e3, 2) if v else None) for e, v in zip(EV, t)}}))
+
+
+A, B, C = dev(synth.uniform(64, 64, 1)), dev(synth.uniform(64, 64, 2)), dev(np.zeros((64, 64)))
+timeline("DGEMM 64^3 s=7", lambda: oz.dgemm("N", "N", 1.0, A, B, 0.0, C, 7))
+A, B = dev(synth.kkr(512, 512, seed=1, gamma=3.0)), dev(synth.kkr(512, 512, seed=2, gamma=3.0))
+C = dev(np.zeros((512, 512), complex))
+for sk in ("1", "4"):
+    os.environ["OZAKI_SPLITK"] = sk
+    timeline(f"ZGEMM 512^3 4M s=7 splitk={sk}", lambda: oz.zgemm("N", "N", 1.0, A, B, 0.0, C, 7))
+os.environ.pop("OZAKI_SPLITK")
+n = 2048
+A, B, C = dev(synth.uniform(n, n, 1)), dev(synth.uniform(n, n, 2)), dev(np.zeros((n, n)))
+timeline(f"DGEMM {n}^3 s=7", lambda: oz.dgemm("N", "N", 1.0, A, B, 0.0, C, 7))
