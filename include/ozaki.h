@@ -165,6 +165,34 @@ int ozaki2_zgemm_strided_batched(char transa, char transb, int64_t m, int64_t n,
                                  const double *beta, double *C, int64_t ldc, int64_t strideC,
                                  int64_t batch, int num_moduli);
 
+/* --- NEXT-4 variant: emulated triangular solve (reading R23) ----------------
+ * PAPER.md:115 (§3.2): LSMS time is "primarily the ZGEMM and ZTRSM" (> 80 %).
+ * BLAS TRSM semantics, B overwritten by X (column-major, device or host
+ * pointers like the GEMMs; host pointers are staged and the call returns when
+ * B is written back):
+ *   side 'L': op(A) X = alpha B   (A is m x m)
+ *   side 'R': X op(A) = alpha B   (A is n x n)
+ * uplo 'U'/'L' selects the referenced triangle of A, transa 'N'/'T'/'C'
+ * (real 'C' == 'T'), diag 'U' = unit diagonal (not referenced) / 'N'.
+ * Method (R23): B <- alpha B (R7's beta*C op shapes; alpha == 0: B = 0, B not
+ * read; alpha == 1: unchanged), then over blocks of nb rows (left) / columns
+ * (right) of the triangle, forward when op(A) is lower (left) / upper (right)
+ * and backward otherwise: the diagonal block is solved by FP64 substitution
+ * in the fixed op order of R23 (k_trsm_diag), and the remaining rows / columns
+ * of B are updated by the EMULATED GEMM B_R <- -T_RK X_K + B_R (left) or
+ * B_R <- -X_K T_KR + B_R (right) with num_slices slices (ozaki_dgemm /
+ * ozaki_zgemm 4M).  nb is thread-local (ozaki_set_trsm_block, default 128).
+ * Errors (nothing written): -1 side, -2 uplo, -3 transa, -4 diag, -5 m < 0,
+ * -6 n < 0, -9 lda < max(1, m or n), -11 ldb < max(1, m), -12 num_slices not
+ * in [1, 16]; OZAKI_ERR_ALIAS when A and B overlap.                          */
+int ozaki_dtrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n, double alpha,
+                const double *A, int64_t lda, double *B, int64_t ldb, int num_slices);
+int ozaki_ztrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n, const double *alpha,
+                const double *A, int64_t lda, double *B, int64_t ldb, int num_slices);
+/* nb >= 1 (returns -1 otherwise); thread-local, read at each TRSM call.      */
+int ozaki_set_trsm_block(int64_t nb);
+int64_t ozaki_get_trsm_block(void);
+
 /* --- NEXT-4 variant: the Ozaki-I pair set (reading R21) ----------------------
  * full = 0 (default): the triangular set t + u <= s + 1 of R1, s(s+1)/2 INT8
  * products.  full = 1: all s^2 slice products (levels L = 2..2s, same

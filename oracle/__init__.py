@@ -83,6 +83,10 @@ def lib():
         L.orc_emulated_product_full.argtypes = [i64, i64, i64, i32, p, p, p]
         L.orc_quick_complex.restype = None
         L.orc_quick_complex.argtypes = [i64, dbl, dbl, p, p]
+        L.orc_trsm_diag_real.restype = None
+        L.orc_trsm_diag_real.argtypes = [i32, i32, i32, i64, p, i64, p]
+        L.orc_trsm_diag_complex.restype = None
+        L.orc_trsm_diag_complex.argtypes = [i32, i32, i32, i64, p, i64, p]
         _lib = L
     return _lib
 
@@ -390,3 +394,71 @@ def fp64_product(A_op, B_op) -> np.ndarray:
 def pairs(s: int) -> int:
     """Number of retained slice pairs t+u <= s+1 (reading R1)."""
     return s * (s + 1) // 2
+
+
+# ------------------------------------------------------------ R23 emulated TRSM (NEXT-4c)
+def trsm_diag(side, lower, unit, T, X):
+    """Diagonal-block solve of R23 (orc_trsm_diag_*): side 'L' solves T x = b for every
+    column of X, 'R' solves x T = b for every row; returns the solved copy of X."""
+    T = np.asarray(T)
+    kb = T.shape[0]
+    cplx = np.iscomplexobj(T) or np.iscomplexobj(X)
+    right = side.upper() == "R"
+    vec = np.ascontiguousarray(X.T if not right else X)          # one vector per row
+    if cplx:
+        Tc = _c(np.asarray(T, dtype=np.complex128), np.complex128)
+        v = _c(vec, np.complex128).copy()
+        lib().orc_trsm_diag_complex(int(right), int(lower), int(unit), kb, _ptr(Tc), v.shape[0], _ptr(v))
+    else:
+        Tc = _c(T, np.float64)
+        v = _c(vec, np.float64).copy()
+        lib().orc_trsm_diag_real(int(right), int(lower), int(unit), kb, _ptr(Tc), v.shape[0], _ptr(v))
+    return v.T if not right else v
+
+
+def _scale_alpha(alpha, B, cplx):
+    """B <- alpha B with R7's beta*C shapes (the BLAS quick return's: real alpha b, complex
+    fma(ar, br, -(ai bi)) / fma(ar, bi, ai br); alpha == 0: zeros, B not read); alpha == 1
+    leaves B unchanged."""
+    if (complex(alpha) if cplx else float(alpha)) == 1:
+        return np.array(B, copy=True)
+    return _quick(complex(alpha) if cplx else float(alpha), B)
+
+
+def trsm(side, uplo, transa, diag, alpha, A, B, s: int, nb: int = 128, method: str = "4m"):
+    """R23 blocked TRSM: side 'L' solves op(A) X = alpha B, 'R' solves X op(A) = alpha B.
+    B <- alpha B first; then over nb-blocks of the triangle (forward for lower op(A) on the
+    left / upper on the right, backward otherwise): X_K = the R23 diagonal solve of
+    T_KK, and the remaining rows (left) / columns (right) are updated by the EMULATED GEMM
+    B_R <- -T_RK X_K + B_R (left) or B_R <- -X_K T_KR + B_R (right) with s slices (O1..O7).
+    Only the uplo triangle of A is referenced (diag 'U': its diagonal is not either).
+    Returns X (new array)."""
+    cplx = np.iscomplexobj(A) or np.iscomplexobj(B)
+    side, uplo, transa, diag = side.upper(), uplo.upper(), transa.upper(), diag.upper()
+    A = np.asarray(A, dtype=np.complex128 if cplx else np.float64)
+    dim = A.shape[0]
+    tri = np.tril(A) if uplo == "L" else np.triu(A)
+    T = op(tri, transa)                              # op(A), other triangle zero
+    lower = (uplo == "L") == (transa == "N")         # op(A) lower triangular?
+    unit = diag == "U"
+    X = _scale_alpha(alpha, np.asarray(B, dtype=A.dtype), cplx)
+    if X.size == 0 or complex(alpha) == 0:
+        return X
+    blocks = [(k0, min(dim, k0 + nb)) for k0 in range(0, dim, nb)]
+    left = side == "L"
+    forward = lower if left else not lower
+    gemm = (lambda a_, b_, c_: zgemm("N", "N", -1.0, a_, b_, 1.0, c_, s, method)) if cplx else \
+           (lambda a_, b_, c_: dgemm("N", "N", -1.0, a_, b_, 1.0, c_, s))
+    for (a, b) in (blocks if forward else blocks[::-1]):
+        Tkk = T[a:b, a:b]
+        if left:
+            X[a:b] = trsm_diag("L", lower, unit, Tkk, X[a:b])
+            r0, r1 = (b, dim) if forward else (0, a)
+            if r1 > r0:
+                X[r0:r1] = gemm(T[r0:r1, a:b], X[a:b], X[r0:r1])
+        else:
+            X[:, a:b] = trsm_diag("R", lower, unit, Tkk, X[:, a:b])
+            r0, r1 = (b, dim) if forward else (0, a)
+            if r1 > r0:
+                X[:, r0:r1] = gemm(X[:, a:b], T[a:b, r0:r1], X[:, r0:r1])
+    return X

@@ -542,3 +542,84 @@ void orc2_residue_gemm(int64_t m, int64_t n, int64_t k, const int8_t *RA, const 
             C[i * n + j] = (int32_t)r;
         }
 }
+
+/* ========================================================================= */
+/* Emulated TRSM (NEXT-4c), reading R23.  PAPER.md:115 (§3.2): */
+/* LSMS time is "primarily the ZGEMM and ZTRSM"; the paper does not say how a */
+/* TRSM is emulated, so R23 reads it as the standard blocked TRSM whose        */
+/* off-diagonal updates are the emulated GEMM and whose nb x nb diagonal      */
+/* blocks are solved in plain FP64 substitution with this fixed op order:     */
+/*   left  (T x = b), T lower: i ascending,  acc = b_i, acc = fma(-T_ij, x_j,  */
+/*         acc) for j ascending over j < i, x_i = acc / T_ii (unit: x_i=acc); */
+/*         T upper: i descending, j ascending over j > i.                     */
+/*   right (x T = b), T upper: j ascending, i ascending over i < j:          */
+/*         acc = fma(-T_ij, x_i, acc), x_j = acc / T_jj; T lower: j descending, */
+/*         i ascending over i > j.                                            */
+/* Complex: acc -= t x as acc_r = fma(-t_r, x_r, fma(t_i, x_i, acc_r)),        */
+/* acc_i = fma(-t_r, x_i, fma(-t_i, x_r, acc_i)); division a / t with          */
+/* d = fma(t_r, t_r, t_i t_i), x_r = fma(a_r, t_r, a_i t_i) / d,               */
+/* x_i = fma(a_i, t_r, -(a_r t_i)) / d.                                        */
+/* T is the nb x nb diagonal block of op(A), row-major T[i*kb + j]; X holds    */
+/* nvec vectors of length kb, vector v at X[v*kb + .] (solved in place).      */
+/* ========================================================================= */
+void orc_trsm_diag_real(int right, int lower, int unit, int64_t kb, const double *T, int64_t nvec, double *X)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t v = 0; v < nvec; ++v) {
+        double *x = X + v * kb;
+        for (int64_t s = 0; s < kb; ++s) {
+            /* left: forward over i for lower T; right: forward over j for upper T */
+            const int fwd = right ? !lower : lower;
+            const int64_t i = fwd ? s : kb - 1 - s;
+            double acc = x[i];
+            if (!right) {
+                const int64_t j0 = lower ? 0 : i + 1, j1 = lower ? i : kb;
+                for (int64_t j = j0; j < j1; ++j) acc = fma(-T[i * kb + j], x[j], acc);
+                x[i] = unit ? acc : acc / T[i * kb + i];
+            } else {
+                const int64_t j = i;            /* unknown x_j; terms x_r T_rj */
+                const int64_t r0 = lower ? j + 1 : 0, r1 = lower ? kb : j;
+                for (int64_t r = r0; r < r1; ++r) acc = fma(-T[r * kb + j], x[r], acc);
+                x[j] = unit ? acc : acc / T[j * kb + j];
+            }
+        }
+    }
+}
+
+static void cdiv_r23(double ar, double ai, double tr, double ti, double *xr, double *xi)
+{
+    const double d = fma(tr, tr, ti * ti);
+    *xr = fma(ar, tr, ai * ti) / d;
+    *xi = fma(ai, tr, -(ar * ti)) / d;
+}
+
+/* complex: T and X interleaved (re, im) */
+void orc_trsm_diag_complex(int right, int lower, int unit, int64_t kb, const double *T, int64_t nvec, double *X)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t v = 0; v < nvec; ++v) {
+        double *x = X + 2 * v * kb;
+        for (int64_t s = 0; s < kb; ++s) {
+            const int fwd = right ? !lower : lower;
+            const int64_t i = fwd ? s : kb - 1 - s;
+            double ar = x[2 * i], ai = x[2 * i + 1];
+            int64_t r0, r1;
+            if (!right) { r0 = lower ? 0 : i + 1; r1 = lower ? i : kb; }
+            else        { r0 = lower ? i + 1 : 0; r1 = lower ? kb : i; }
+            for (int64_t r = r0; r < r1; ++r) {
+                /* left: t = T_ir, x_r;  right: t = T_ri, x_r */
+                const int64_t ti_ = right ? (r * kb + i) : (i * kb + r);
+                const double tr = T[2 * ti_], tim = T[2 * ti_ + 1];
+                const double xr = x[2 * r], xi = x[2 * r + 1];
+                ar = fma(-tr, xr, fma(tim, xi, ar));
+                ai = fma(-tr, xi, fma(-tim, xr, ai));
+            }
+            if (unit) {
+                x[2 * i] = ar;
+                x[2 * i + 1] = ai;
+            } else {
+                cdiv_r23(ar, ai, T[2 * (i * kb + i)], T[2 * (i * kb + i) + 1], &x[2 * i], &x[2 * i + 1]);
+            }
+        }
+    }
+}

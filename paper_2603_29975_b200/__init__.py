@@ -20,7 +20,8 @@ __all__ = [
     "OzakiError", "lib", "dgemm", "zgemm", "zgemm3m", "dgemm_strided_batched",
     "zgemm_strided_batched", "zgemm3m_strided_batched", "set_stream", "get_stats",
     "reset_stats", "workspace_size", "debug_split", "debug_level_sums", "colmajor",
-    "version", "pairs", "LIB_PATH", "profile_enable", "profile_read",
+    "version", "pairs", "LIB_PATH", "profile_enable", "profile_read", "dtrsm", "ztrsm",
+    "set_trsm_block", "get_trsm_block",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -80,6 +81,12 @@ def lib():
     L.ozaki_set_exponent_block.restype = i32
     L.ozaki_get_exponent_block.argtypes = []
     L.ozaki_get_exponent_block.restype = i64
+    L.ozaki_dtrsm.argtypes = [c, c, c, c, i64, i64, dbl, p, i64, p, i64, i32]
+    L.ozaki_ztrsm.argtypes = [c, c, c, c, i64, i64, dP, p, i64, p, i64, i32]
+    L.ozaki_set_trsm_block.argtypes = [i64]
+    L.ozaki_set_trsm_block.restype = i32
+    L.ozaki_get_trsm_block.argtypes = []
+    L.ozaki_get_trsm_block.restype = i64
     L.ozaki_set_pair_set.argtypes = [i32]
     L.ozaki_set_pair_set.restype = i32
     L.ozaki_get_pair_set.argtypes = []
@@ -329,6 +336,54 @@ def ozaki2_zgemm_strided_batched(transa, transb, alpha, A, B, beta, C, num_modul
     import torch
     return _batched(lib().ozaki2_zgemm_strided_batched, torch.complex128, transa, transb, alpha, A,
                     B, beta, C, num_moduli, stream, True)
+
+
+# ------------------------------------------------- emulated TRSM (R23, NEXT-4c)
+def _trsm(fn, dtype, side, uplo, transa, diag, alpha, A, B, num_slices, stream, cplx):
+    import torch
+    for x, nm in ((A, "A"), (B, "B")):
+        _cuda(x, dtype, nm)
+    if B.is_conj() or B.is_neg():
+        raise ValueError("B must not be a lazily conjugated / negated view (resolve it first)")
+    if A.is_conj() or A.is_neg():
+        A = colmajor(A.resolve_conj().resolve_neg())
+    if A.device != B.device and A.device.type == "cuda" and B.device.type == "cuda":
+        raise ValueError("A and B must live on one CUDA device")
+    m, n = B.shape
+    dim = m if side.upper() == "L" else n
+    if tuple(A.shape) != (dim, dim):
+        raise ValueError(f"A must be {dim}x{dim}")
+    dev = A.device if A.device.type == "cuda" else B.device
+    with _on(dev):
+        _bind_stream(stream, dev)
+        al = _cpair(alpha) if cplx else float(alpha)
+        rc = fn(_ch(side), _ch(uplo), _ch(transa), _ch(diag), m, n, al, A.data_ptr(), _ld(A), B.data_ptr(),
+                _ld(B), int(num_slices))
+    _check(rc, fn.__name__)
+    return B
+
+
+def dtrsm(side, uplo, transa, diag, alpha, A, B, num_slices, stream=None):
+    """B <- X with op(A) X = alpha B (side 'L') or X op(A) = alpha B ('R'), emulated (R23)."""
+    import torch
+    return _trsm(lib().ozaki_dtrsm, torch.float64, side, uplo, transa, diag, alpha, A, B, num_slices,
+                 stream, False)
+
+
+def ztrsm(side, uplo, transa, diag, alpha, A, B, num_slices, stream=None):
+    """Complex emulated TRSM (R23), updates through the 4M ZGEMM."""
+    import torch
+    return _trsm(lib().ozaki_ztrsm, torch.complex128, side, uplo, transa, diag, alpha, A, B, num_slices,
+                 stream, True)
+
+
+def set_trsm_block(nb: int) -> None:
+    """Block size nb of the emulated TRSM for this thread (R23, default 128)."""
+    _check(lib().ozaki_set_trsm_block(int(nb)), "ozaki_set_trsm_block")
+
+
+def get_trsm_block() -> int:
+    return int(lib().ozaki_get_trsm_block())
 
 
 # ------------------------------------------------------------- utilities

@@ -3,7 +3,8 @@
 // The paper's deployment contract is "no code change": the application's
 // ZGEMM/DGEMM calls are redirected to the emulation underneath it (PAPER.md
 // :108-111, §3.1, SCILIB-Accel).  This library exports the reference-BLAS
-// Fortran entry points dgemm_/zgemm_ (and the no-underscore aliases) so that
+// Fortran entry points dgemm_/zgemm_ and dtrsm_/ztrsm_ (emulated TRSM, reading R23 -- the
+// paper's other hot routine) and the no-underscore aliases, so that
 //     LD_PRELOAD=.../libozaki_blas.so ./application
 // (or linking against it in place of BLAS) sends every DGEMM/ZGEMM through the
 // C ABI of include/ozaki.h.  It holds no arithmetic of its own.
@@ -45,10 +46,10 @@ bool zgemm_3m_from_env() {
     return m3;
 }
 
-void report(const char *name, int rc) {
+void report(const char *name, int rc, int slices_param = 14) {
     if (rc < 0) {
-        // reference-BLAS xerbla wording; num_slices (param 14) comes from the environment
-        if (rc == -14)
+        // reference-BLAS xerbla wording; num_slices (GEMM param 14, TRSM 12) comes from the environment
+        if (rc == -slices_param)
             std::fprintf(stderr, " ** On entry to %s, OZAKI_NUM_SLICES is out of range [1, 16]\n", name);
         else
             std::fprintf(stderr, " ** On entry to %s parameter number %2d had an illegal value\n", name, -rc);
@@ -81,9 +82,42 @@ void zgemm_impl(const char *ta, const char *tb, const int *m, const int *n, cons
     report("ZGEMM ", rc);
 }
 
+void dtrsm_impl(const char *side, const char *uplo, const char *ta, const char *diag, const int *m,
+                const int *n, const double *alpha, const double *A, const int *lda, double *B, const int *ldb) {
+    const int rc = finish(ozaki_dtrsm(*side, *uplo, *ta, *diag, *m, *n, *alpha, A, *lda, B, *ldb,
+                                      slices_from_env()));
+    report("DTRSM ", rc, 12);
+}
+
+void ztrsm_impl(const char *side, const char *uplo, const char *ta, const char *diag, const int *m,
+                const int *n, const double *alpha, const double *A, const int *lda, double *B, const int *ldb) {
+    const int rc = finish(ozaki_ztrsm(*side, *uplo, *ta, *diag, *m, *n, alpha, A, *lda, B, *ldb,
+                                      slices_from_env()));
+    report("ZTRSM ", rc, 12);
+}
+
 }  // namespace
 
 extern "C" {
+
+// Fortran: SUBROUTINE DTRSM(SIDE,UPLO,TRANSA,DIAG,M,N,ALPHA,A,LDA,B,LDB) -- emulated (R23)
+void dtrsm_(const char *side, const char *uplo, const char *ta, const char *diag, const int *m, const int *n,
+            const double *alpha, const double *A, const int *lda, double *B, const int *ldb) {
+    dtrsm_impl(side, uplo, ta, diag, m, n, alpha, A, lda, B, ldb);
+}
+void dtrsm(const char *side, const char *uplo, const char *ta, const char *diag, const int *m, const int *n,
+           const double *alpha, const double *A, const int *lda, double *B, const int *ldb) {
+    dtrsm_impl(side, uplo, ta, diag, m, n, alpha, A, lda, B, ldb);
+}
+// Fortran: SUBROUTINE ZTRSM(...) with COMPLEX*16 ALPHA, A, B (interleaved re, im); 4M updates
+void ztrsm_(const char *side, const char *uplo, const char *ta, const char *diag, const int *m, const int *n,
+            const double *alpha, const double *A, const int *lda, double *B, const int *ldb) {
+    ztrsm_impl(side, uplo, ta, diag, m, n, alpha, A, lda, B, ldb);
+}
+void ztrsm(const char *side, const char *uplo, const char *ta, const char *diag, const int *m, const int *n,
+           const double *alpha, const double *A, const int *lda, double *B, const int *ldb) {
+    ztrsm_impl(side, uplo, ta, diag, m, n, alpha, A, lda, B, ldb);
+}
 
 // Fortran: SUBROUTINE DGEMM(TRANSA,TRANSB,M,N,K,ALPHA,A,LDA,B,LDB,BETA,C,LDC)
 void dgemm_(const char *ta, const char *tb, const int *m, const int *n, const int *k,

@@ -34,7 +34,7 @@ struct Lv2Params {
 
 // Debug timeline (ozaki_debug_timing): globaltimer at fixed events of CTA 0.
 enum TlEvent : int { TL_ENTRY = 0, TL_PROLOGUE, TL_DEPWAIT, TL_TMA0, TL_FULL0, TL_MMA_PASS0, TL_MMA_END,
-                     TL_EPI_PASS0, TL_EPI_LAST, TL_EPI_STORE, TL_EXIT };
+                     TL_EPI_PASS0, TL_EPI_LAST, TL_EPI_STORE, TL_EXIT, TL_EPI_DRAINED, TL_EPI_F };
 __device__ __forceinline__ void tl_mark(const GemmParams &p, int ev) {
     if (p.dbg && blockIdx.x == 0) {
         unsigned long long t;
@@ -487,6 +487,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 if (dbgw) dbg_add(p, DBG_EPI_DRAIN, clock64() - w1);
             }
             const long long s0 = p.dbg ? clock64() : 0;
+            if (dbgw) {
+                tl_mark(p, TL_EPI_DRAINED);
+                // probe: latency of one column-exponent load and one load of C (debug timeline only)
+                const int32_t f = __ldg(p.fb + b * p.N + tn * kLvBN);
+                const double cv = *(volatile double *)(p.C + b * p.strideC);
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                if (blockIdx.x == 0) p.dbg[DBG_TL0 + TL_EPI_F] = t + (f == -123456789 ? 1 : 0) + (cv == 1.2345e300 ? 1 : 0);
+            }
             if constexpr (EPI != EPI_LEVELS && CHUNK != 1 && CHUNK != 3)
                 lv_store<EPI, kNC2>(p, b, grow, e, tn * kLvBN + half * kNC2, acc, CHUNK == 0 ? -8 * (Lmax - 2) : 0);
             if (dbgw) dbg_add(p, DBG_EPI_STORE, clock64() - s0);

@@ -29,6 +29,7 @@
 #include "ozaki.h"
 #include "split.cuh"
 #include "split_fast.cuh"
+#include "trsm.cuh"
 
 using namespace ozk;
 
@@ -39,6 +40,7 @@ thread_local std::string t_err;
 thread_local int t_full_pairs = 0;   // R21 pair set for Ozaki-I calls (ozaki_set_pair_set)
 thread_local int64_t t_kblock = 0;    // R22 exponent block along K (0 = per row / column)
 thread_local int t_overlap = 0;       // cross-call split / GEMM overlap (ozaki_set_overlap)
+thread_local int64_t t_trsm_nb = 128;  // R23 TRSM block (ozaki_set_trsm_block)
 
 // Cross-call overlap state per (thread, stream, device): two persistent slice workspaces used
 // alternately, and whether the last kernel this thread put on the stream is an Ozaki-I GEMM
@@ -1894,6 +1896,183 @@ int run(const Call &c0) {
     return 0;
 }
 
+// ============================================================ emulated TRSM (R23, NEXT-4c)
+struct TrsmCall {
+    bool cplx;
+    char side, uplo, ta, diag;
+    int64_t m, n;
+    double al[2];
+    const double *A;
+    int64_t lda;
+    double *B;
+    int64_t ldb;
+    int s;
+};
+
+int validate_trsm(const TrsmCall &c) {
+    const char sd = up(c.side), ul = up(c.uplo), dg = up(c.diag);
+    if (sd != 'L' && sd != 'R') return fail(-1, "side");
+    if (ul != 'U' && ul != 'L') return fail(-2, "uplo");
+    if (!trans_ok(c.ta)) return fail(-3, "transa");
+    if (dg != 'U' && dg != 'N') return fail(-4, "diag");
+    if (c.m < 0) return fail(-5, "m < 0");
+    if (c.n < 0) return fail(-6, "n < 0");
+    if (c.lda < std::max<int64_t>(1, sd == 'L' ? c.m : c.n)) return fail(-9, "lda too small");
+    if (c.ldb < std::max<int64_t>(1, c.m)) return fail(-11, "ldb too small");
+    if (c.s < 1 || c.s > 16) return fail(-12, "num_slices not in [1,16]");
+    return 0;
+}
+
+int run_trsm_device(const TrsmCall &c, DevState *dev, cudaStream_t st) {
+    const char sd = up(c.side), ul = up(c.uplo), dg = up(c.diag);
+    char ta = up(c.ta);
+    if (!c.cplx && ta == 'C') ta = 'T';
+    const bool left = sd == 'L';
+    const int64_t dim = left ? c.m : c.n;
+    const size_t es = c.cplx ? 16 : 8;
+    const double *A = c.A;
+    double *B = c.B;
+    // B <- alpha B with R7's quick-return op shapes (alpha == 0: zeros, B not read)
+    const bool alpha1 = c.al[0] == 1.0 && c.al[1] == 0.0;
+    if (!alpha1) {
+        dim3 grid(grid1d(c.m * c.n, dev->sms), 1, 1);
+        ProfScope ps(st, PH_OTHER);
+        if (c.cplx) k_scale_cplx<<<grid, 256, 0, st>>>(B, c.m, c.n, c.ldb, 0, c.al[0], c.al[1]);
+        else k_scale_real<<<grid, 256, 0, st>>>(B, c.m, c.n, c.ldb, 0, c.al[0]);
+        CUDA_TRY(cudaGetLastError());
+        g_stats.launches += 1;
+        if (c.al[0] == 0.0 && c.al[1] == 0.0) return 0;
+    }
+    const bool lower = (ul == 'L') == (ta == 'N');   // op(A) lower triangular
+    const bool forward = left ? lower : !lower;
+    const int64_t nb = std::max<int64_t>(1, t_trsm_nb);
+    const int64_t nblk = (dim + nb - 1) / nb;
+    const double m1[2] = {-1.0, 0.0}, p1[2] = {1.0, 0.0};
+    const int ovs = t_overlap;
+    t_overlap = 0;   // the diagonal kernels sit between the GEMMs (no PDL early reads)
+    const cudaStream_t user = t_stream;
+    t_stream = st;
+    int rc = 0;
+    for (int64_t q = 0; q < nblk && !rc; ++q) {
+        const int64_t bi = forward ? q : nblk - 1 - q;
+        const int64_t k0 = bi * nb, kb = std::min<int64_t>(nb, dim - k0);
+        TrsmDiagParams dp;
+        dp.A = A;
+        dp.lda = c.lda;
+        dp.B = B;
+        dp.ldb = c.ldb;
+        dp.k0 = k0;
+        dp.kb = (int32_t)kb;
+        dp.trans = ta == 'N' ? 0 : (ta == 'T' ? 1 : 2);
+        dp.lower = lower ? 1 : 0;
+        dp.unit = dg == 'U' ? 1 : 0;
+        dp.right = left ? 0 : 1;
+        dp.nvec = left ? c.n : c.m;
+        {
+            ProfScope ps(st, PH_OTHER);
+            const unsigned g = (unsigned)((dp.nvec + 127) / 128);
+            if (c.cplx) k_trsm_diag<true><<<g, 128, 0, st>>>(dp);
+            else k_trsm_diag<false><<<g, 128, 0, st>>>(dp);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) { rc = fail(OZAKI_ERR_CUDA, "k_trsm_diag: %s", cudaGetErrorString(e)); break; }
+            g_stats.launches += 1;
+        }
+        // remaining rows (left) / columns (right): [k0 + kb, dim) forward, [0, k0) backward
+        const int64_t r0 = forward ? k0 + kb : 0, r1 = forward ? dim : k0;
+        if (r1 <= r0) continue;
+        const int64_t nr = r1 - r0;
+        // T_{R,K} (left) or T_{K,R} (right) as an operand of op(): 'N' -> A(rows, cols) of T,
+        // 'T'/'C' -> the mirrored block of A with the same transpose flag
+        auto tblock = [&](int64_t row0, int64_t col0) {   // element (0,0) of T(row0.., col0..)
+            const int64_t r = ta == 'N' ? row0 : col0, cc = ta == 'N' ? col0 : row0;
+            return A + (c.cplx ? 2 : 1) * (r + cc * c.lda);
+        };
+        const int64_t ew = c.cplx ? 2 : 1;
+        Call g{};
+        g.kind = c.cplx ? KIND_4M : KIND_REAL;
+        g.al[0] = m1[0];
+        g.al[1] = m1[1];
+        g.be[0] = p1[0];
+        g.be[1] = p1[1];
+        g.s = c.s;
+        g.batch = 1;
+        g.batched = false;
+        g.full = t_full_pairs != 0;
+        g.kblock = t_kblock;
+        if (left) {   // B_R <- -T_{R,K} X_K + B_R
+            g.ta = ta;
+            g.tb = 'N';
+            g.m = nr;
+            g.n = c.n;
+            g.k = kb;
+            g.A = tblock(r0, k0);
+            g.lda = c.lda;
+            g.B = B + ew * k0;
+            g.ldb = c.ldb;
+            g.C = B + ew * r0;
+            g.ldc = c.ldb;
+        } else {      // B_R <- -X_K T_{K,R} + B_R
+            g.ta = 'N';
+            g.tb = ta;
+            g.m = c.m;
+            g.n = nr;
+            g.k = kb;
+            g.A = B + ew * k0 * c.ldb;
+            g.lda = c.ldb;
+            g.B = tblock(k0, r0);
+            g.ldb = c.lda;
+            g.C = B + ew * r0 * c.ldb;
+            g.ldc = c.ldb;
+        }
+        rc = run(g);
+    }
+    t_stream = user;
+    t_overlap = ovs;
+    (void)es;
+    return rc;
+}
+
+int run_trsm(const TrsmCall &c0) {
+    t_err.clear();
+    if (int rc = validate_trsm(c0)) return rc;
+    TrsmCall c = c0;
+    if (c.m == 0 || c.n == 0) return 0;
+    DevState *dev = nullptr;
+    if (int rc = device_state(&dev)) return rc;
+    const bool left = up(c.side) == 'L';
+    const int64_t dim = left ? c.m : c.n;
+    const size_t es = c.cplx ? 16 : 8;
+    const bool alpha0 = c.al[0] == 0.0 && c.al[1] == 0.0;
+    const size_t abytes = alpha0 ? 0 : es * (size_t)((dim - 1) * c.lda + dim);
+    const size_t bbytes = es * (size_t)((c.n - 1) * c.ldb + c.m);
+    if (!alpha0 && overlaps(c.A, abytes, c.B, bbytes)) return fail(OZAKI_ERR_ALIAS, "A overlaps B");
+    cudaStream_t st = t_stream;
+    const PtrKind kb_ = ptr_kind(c.B), ka = alpha0 ? kb_ : ptr_kind(c.A);
+    if (ka == PTR_DEVICE && kb_ == PTR_DEVICE) return run_trsm_device(c, dev, st);
+    if (!(ka == PTR_HOST && kb_ == PTR_HOST))
+        return fail(OZAKI_ERR_UNSUPPORTED, "A and B must both be device or both be host pointers");
+    // host pointers: stage A (dim x dim, pitch lda) and B (m x n, pitch ldb), solve, copy B back
+    char *buf = nullptr;
+    const size_t a_dev = alpha0 ? 0 : es * (size_t)dim * dim, b_dev = es * (size_t)c.m * c.n;
+    cudaError_t e = cudaMallocAsync((void **)&buf, al256(a_dev) + b_dev, st);
+    if (e != cudaSuccess) return fail(OZAKI_ERR_ALLOC, "TRSM staging: %s", cudaGetErrorString(e));
+    TrsmCall d = c;
+    d.A = (const double *)buf;
+    d.lda = std::max<int64_t>(1, dim);
+    d.B = (double *)(buf + al256(a_dev));
+    d.ldb = c.m;
+    int rc = 0;
+    if (!alpha0)
+        CUDA_TRY(cudaMemcpy2DAsync(buf, es * dim, c.A, es * c.lda, es * dim, dim, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpy2DAsync(d.B, es * c.m, c.B, es * c.ldb, es * c.m, c.n, cudaMemcpyHostToDevice, st));
+    rc = run_trsm_device(d, dev, st);
+    if (!rc) CUDA_TRY(cudaMemcpy2DAsync(c.B, es * c.ldb, d.B, es * c.m, es * c.m, c.n, cudaMemcpyDeviceToHost, st));
+    cudaFreeAsync(buf, st);
+    e = cudaStreamSynchronize(st);
+    if (!rc && e != cudaSuccess) rc = fail(OZAKI_ERR_CUDA, "TRSM: %s", cudaGetErrorString(e));
+    return rc;
+}
+
 Call make_call(Kind kind, char ta, char tb, int64_t m, int64_t n, int64_t k, const double *al,
                const double *A, int64_t lda, int64_t sA, const double *B, int64_t ldb, int64_t sB,
                const double *be, double *C, int64_t ldc, int64_t sC, int64_t batch, int s,
@@ -2022,6 +2201,26 @@ int ozaki2_zgemm_strided_batched(char transa, char transb, int64_t m, int64_t n,
     return run(make_call_crt(KIND_4M, transa, transb, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta,
                              C, ldc, strideC, batch, num_moduli, true));
 }
+
+int ozaki_dtrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n, double alpha,
+                const double *A, int64_t lda, double *B, int64_t ldb, int num_slices) {
+    TrsmCall c{false, side, uplo, transa, diag, m, n, {alpha, 0.0}, A, lda, B, ldb, num_slices};
+    return run_trsm(c);
+}
+
+int ozaki_ztrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n, const double *alpha,
+                const double *A, int64_t lda, double *B, int64_t ldb, int num_slices) {
+    TrsmCall c{true, side, uplo, transa, diag, m, n, {alpha[0], alpha[1]}, A, lda, B, ldb, num_slices};
+    return run_trsm(c);
+}
+
+int ozaki_set_trsm_block(int64_t nb) {
+    if (nb < 1) return -1;
+    t_trsm_nb = nb;
+    return 0;
+}
+
+int64_t ozaki_get_trsm_block(void) { return t_trsm_nb; }
 
 int ozaki_set_exponent_block(int64_t kb) {
     if (kb < 0) return fail(-1, "exponent block < 0");

@@ -94,3 +94,30 @@ def test_workspace_size_closed_form(L):
     assert workspace_size("d", 1, 1, 1, 1, 0) == -1
     # s*k_eff beyond the INT32 level-sum bound (reading R8) is K-chunked, not refused
     assert workspace_size("d", 8, 8, 20000, 1, 8) > 0
+
+
+def test_trsm_xerbla_codes_before_device_work():
+    """ozaki_dtrsm / ozaki_ztrsm argument checks (BLAS parameter numbers) return before any
+    device work (no GPU needed), and the block-size setter rejects nb < 1."""
+    import ctypes
+    import paper_2603_29975_b200 as oz
+    L = oz.lib()
+    buf = (ctypes.c_double * 64)()
+    z = (ctypes.c_double * 2)(1.0, 0.0)
+    p = ctypes.cast(buf, ctypes.c_void_p)
+    d = lambda *a: L.ozaki_dtrsm(*a)  # noqa: E731
+    assert d(b"X", b"L", b"N", b"N", 4, 4, 1.0, p, 4, p, 4, 7) == -1
+    assert d(b"L", b"X", b"N", b"N", 4, 4, 1.0, p, 4, p, 4, 7) == -2
+    assert d(b"L", b"L", b"X", b"N", 4, 4, 1.0, p, 4, p, 4, 7) == -3
+    assert d(b"L", b"L", b"N", b"X", 4, 4, 1.0, p, 4, p, 4, 7) == -4
+    assert d(b"L", b"L", b"N", b"N", -1, 4, 1.0, p, 4, p, 4, 7) == -5
+    assert d(b"L", b"L", b"N", b"N", 4, -1, 1.0, p, 4, p, 4, 7) == -6
+    assert d(b"L", b"L", b"N", b"N", 4, 2, 1.0, p, 3, p, 4, 7) == -9
+    assert d(b"R", b"L", b"N", b"N", 4, 2, 1.0, p, 1, p, 4, 7) == -9
+    assert d(b"L", b"L", b"N", b"N", 4, 2, 1.0, p, 4, p, 3, 7) == -11
+    assert d(b"L", b"L", b"N", b"N", 4, 2, 1.0, p, 4, p, 4, 17) == -12
+    assert L.ozaki_ztrsm(b"L", b"U", b"C", b"U", 4, 4, z, p, 4, p, 2, 7) == -11
+    assert d(b"L", b"L", b"N", b"N", 0, 4, 1.0, p, 4, p, 4, 7) == 0      # quick return, no device
+    assert L.ozaki_set_trsm_block(0) == -1
+    assert L.ozaki_set_trsm_block(64) == 0 and L.ozaki_get_trsm_block() == 64
+    L.ozaki_set_trsm_block(128)

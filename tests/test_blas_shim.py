@@ -28,7 +28,7 @@ def shim():
 
 def test_shim_exports_and_links(shim):
     out = subprocess.run(["nm", "-D", "--defined-only", shim], capture_output=True, text=True).stdout
-    for name in ("dgemm_", "dgemm", "zgemm_", "zgemm"):
+    for name in ("dgemm_", "dgemm", "zgemm_", "zgemm", "dtrsm_", "dtrsm", "ztrsm_", "ztrsm"):
         assert f" T {name}\n" in out, name
     dyn = subprocess.run(["readelf", "-d", shim], capture_output=True, text=True).stdout
     assert "libozaki.so" in dyn and "libcudart" not in dyn
@@ -139,3 +139,38 @@ def test_ld_preload_interposition(shim, tmp_path):
     A, B, C, ZA, ZB, ZC = run(preload=True)
     assert (C == oracle.dgemm("N", "N", 1.0, A, B, 0.0, None, 6)).all()
     assert (ZC == oracle.zgemm("N", "N", 1.0, ZA, ZB, 0.0, None, 6)).all()
+
+
+_TRSM = r"""
+import ctypes, sys, numpy as np
+sys.path.insert(0, %r)
+import oracle, synth
+L = ctypes.CDLL(%r)
+i = lambda v: ctypes.byref(ctypes.c_int(v))
+P = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+s, m, n = 6, 150, 37
+A = np.asfortranarray(np.tril(synth.uniform(m, m, 1, complex_=True)) * 0.2 + 2 * np.eye(m))
+B = np.asfortranarray(synth.uniform(m, n, 2, complex_=True))
+B0 = B.copy(order="F")
+al = (ctypes.c_double * 2)(0.5, -0.5)
+L.ztrsm_(b"L", b"L", b"C", b"N", i(m), i(n), al, P(A), i(m), P(B), i(m))
+ok_z = bool((B == oracle.trsm("L", "L", "C", "N", 0.5 - 0.5j, A, B0, s)).all())
+Ad = np.asfortranarray(np.triu(synth.uniform(n, n, 3)) * 0.3 + 2 * np.eye(n))
+Bd = np.asfortranarray(synth.uniform(m, n, 4))
+Bd0 = Bd.copy(order="F")
+a1 = ctypes.c_double(1.0)
+L.dtrsm_(b"R", b"U", b"N", b"U", i(m), i(n), ctypes.byref(a1), P(Ad), i(n), P(Bd), i(m))
+ok_d = bool((Bd == oracle.trsm("R", "U", "N", "U", 1.0, Ad, Bd0, s)).all())
+L.dtrsm_(b"R", b"Q", b"N", b"U", i(m), i(n), ctypes.byref(a1), P(Ad), i(n), P(Bd), i(m))
+print("OK" if ok_d and ok_z else "MISMATCH", ok_d, ok_z)
+"""
+
+
+@pytest.mark.gpu
+def test_shim_trsm_bitexact_vs_oracle(shim):
+    """ztrsm_ / dtrsm_ (Fortran ABI, host arrays) = the oracle's R23 blocked TRSM, bit for bit;
+    an invalid UPLO gets the xerbla message with parameter number 2."""
+    r = _run_py(_TRSM % (ROOT, shim), {"OZAKI_NUM_SLICES": "6"})
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.startswith("OK"), r.stdout + r.stderr[-2000:]
+    assert "On entry to DTRSM  parameter number  2 had an illegal value" in r.stderr
