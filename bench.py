@@ -920,6 +920,7 @@ def run_c3(args):
                 del Af, Bf
         out["ozaki2"] = c3_ozaki2_leg(torch, oz, A, B, C, n, stream, local, rows, cols, samples)
         out["native_fp64"] = native_gemm_leg(torch, A, B, n)
+        out["general_alpha_beta"] = general_ab_leg(torch, oz, A, B, C, n, s, stream, local, device)
         out["extra_workloads"] = {"c2x30": c2x30_leg(torch, oz, device, stream, local, args),
                                   "c4": c4_leg(torch, oz, device, stream, local)}
     out["sweep_note"] = ("per s: FP64-eq TF/s from an uninstrumented pass (5 calls, clocks of that pass); "
@@ -988,6 +989,32 @@ def c3_ozaki2_leg(torch, oz, A, B, C, n, stream, local, rows, cols, samples):
         samples[f"ozaki2_N{nmod}"] = C[torch.from_numpy(rows).to(dev)][:, torch.from_numpy(cols).to(dev)].cpu().numpy()
     return {"unit": "TFLOP/s (FP64-equivalent)", "moduli": res,
             "path": "ozaki2_dgemm (split -> k_gemm_crt -> k_crt), NEXT-1"}
+
+
+def general_ab_leg(torch, oz, A, B, C, n, s, stream, local, device):
+    """The LU trailing update's alpha = -1, beta = 1 (R7's general FMA epilogue, C read) against
+    the alpha = 1, beta = 0 store, on C3 (s = 7) and on C2 x 30 (4M, s = 7)."""
+    res = {}
+    for name, ab in (("unit", (1.0, 0.0)), ("lu_update", (-1.0, 1.0))):
+        call = lambda ab=ab: oz.dgemm("N", "N", ab[0], A, B, ab[1], C, s)   # noqa: E731
+        for _ in range(2):
+            call()
+        ms, clk = timed(torch, stream, call, 5, local)
+        res[f"c3_{name}"] = {"tflops": round(2.0 * n ** 3 / (ms * 1e-3) / 1e12, 2), "sm_mhz": clk.get("sm_mhz")}
+    batch, nz = 30, 512
+    A_h, B_h = make_inputs(batch, nz, 3.0, seed0=1000)
+    Az, Bz = to_dev_batched(torch, A_h, device), to_dev_batched(torch, B_h, device)
+    Cz = torch.zeros((batch, nz, nz), dtype=torch.complex128, device=device).transpose(1, 2)
+    for name, ab in (("unit", (1.0, 0.0)), ("lu_update", (-1.0, 1.0))):
+        call = lambda ab=ab: oz.zgemm_strided_batched("N", "N", ab[0], Az, Bz, ab[1], Cz, s)   # noqa: E731
+        for _ in range(3):
+            call()
+        ms, clk = timed(torch, stream, call, 20, local)
+        res[f"c2x30_{name}"] = {"tflops": round(fp64_equiv_flops(batch, nz) / (ms * 1e-3) / 1e12, 2),
+                                "sm_mhz": clk.get("sm_mhz")}
+    for w in ("c3", "c2x30"):
+        res[f"{w}_ratio"] = round(res[f"{w}_lu_update"]["tflops"] / res[f"{w}_unit"]["tflops"], 4)
+    return res
 
 
 def native_gemm_leg(torch, A, B, n):

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 
 __all__ = [
     "OzakiError", "lib", "dgemm", "zgemm", "zgemm3m", "dgemm_strided_batched",
@@ -189,12 +190,21 @@ def _operands(dtype, A, B, C):
     return A, B, (next(iter(cuda)) if cuda else C.device)
 
 
+_NULLCTX = None
+_bound = threading.local()      # last stream handle passed to ozaki_set_stream by this thread
+
+
 def _on(device):
-    """Device guard for one library call: the library works on the current CUDA device."""
+    """Device guard for one library call: the library works on the current CUDA device
+    (no guard when the operands already live on it)."""
+    global _NULLCTX
     import contextlib
     import torch
-    if device is None or device.type != "cuda":
-        return contextlib.nullcontext()
+    if _NULLCTX is None:
+        _NULLCTX = contextlib.nullcontext()
+    if device is None or device.type != "cuda" or device.index is None or \
+            device.index == torch.cuda.current_device():
+        return _NULLCTX
     return torch.cuda.device(device)
 
 
@@ -206,7 +216,10 @@ def _bind_stream(stream=None, device=None):
         s = torch.cuda.current_stream(device if device is not None and device.type == "cuda" else None)
     else:
         s = stream
-    lib().ozaki_set_stream(ctypes.c_void_p(s.cuda_stream))
+    h = s.cuda_stream
+    if getattr(_bound, "h", None) != h:      # the library's stream is thread-local too
+        lib().ozaki_set_stream(ctypes.c_void_p(h))
+        _bound.h = h
 
 
 def _dims(transa, transb, A, B):
@@ -417,7 +430,9 @@ def get_overlap() -> bool:
 
 
 def set_stream(stream) -> None:
-    lib().ozaki_set_stream(ctypes.c_void_p(getattr(stream, "cuda_stream", stream) or 0))
+    h = getattr(stream, "cuda_stream", stream) or 0
+    lib().ozaki_set_stream(ctypes.c_void_p(h))
+    _bound.h = h
 
 
 def get_stats() -> dict:

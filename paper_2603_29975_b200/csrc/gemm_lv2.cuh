@@ -34,7 +34,8 @@ struct Lv2Params {
 
 // Debug timeline (ozaki_debug_timing): globaltimer at fixed events of CTA 0.
 enum TlEvent : int { TL_ENTRY = 0, TL_PROLOGUE, TL_DEPWAIT, TL_TMA0, TL_FULL0, TL_MMA_PASS0, TL_MMA_END,
-                     TL_EPI_PASS0, TL_EPI_LAST, TL_EPI_STORE, TL_EXIT, TL_EPI_DRAINED, TL_EPI_F };
+                     TL_EPI_PASS0, TL_EPI_LAST, TL_EPI_STORE, TL_EXIT, TL_EPI_DRAINED, TL_EPI_F, TL_MMA_SLOT1, TL_EPI_REL0,
+                     TL_MMA_FULL1 };
 __device__ __forceinline__ void tl_mark(const GemmParams &p, int ev) {
     if (p.dbg && blockIdx.x == 0) {
         unsigned long long t;
@@ -85,6 +86,7 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
                 long long w0 = p.dbg ? clock64() : 0;
                 mbar_wait(&full[stage], phase);
                 if (kfirst && ps == 0 && u == (blockIdx.x >> 1)) tl_mark(p, TL_FULL0);
+                if (kfirst && ps == 1 && u == (blockIdx.x >> 1)) tl_mark(p, TL_MMA_FULL1);
                 if (p.dbg && (threadIdx.x & 31) == 0) {
                     const long long dw = clock64() - w0;
                     dbg_add(p, DBG_MMA_WAIT_FULL, dw);
@@ -110,6 +112,7 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
                             }
                         }
                         tc_fence_after();
+                        if (ps == 1 && u == (blockIdx.x >> 1)) tl_mark(p, TL_MMA_SLOT1);
                     }
 #pragma unroll
                     for (int r = 0; r < S; ++r) {
@@ -293,35 +296,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     const int64_t off = (b * p.N + c0) * p.Mp + grow;
                     uint32_t v[16];
                     if (ps == 0) {
+                        // level by level: both 16-column halves in flight, then the slot goes back
+                        // to the MMA issuer at once (the next pass waits for these slots)
                         long long t0[16], t1[16];
-                        tmem_ld_32x32b_x16(tl, v);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) t0[i] = (long long)(int)v[i];
+                        uint32_t v1[16];
 #pragma unroll 1
-                        for (int j = 1; j < nlev; ++j) {
+                        for (int j = 0; j < nlev; ++j) {
                             tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN), v);
+                            tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + 16), v1);
                             tmem_wait_ld();
-                            const int w = 1 << (8 * j);
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_cluster(slot_remote0 + 8u * (uint32_t)j);
+                            if (dbgw && j == 0 && u == (blockIdx.x >> 1)) tl_mark(p, TL_EPI_REL0);
+                            const long long w = 1ll << (8 * j);
 #pragma unroll
-                            for (int i = 0; i < 16; ++i) t0[i] += (long long)(int)v[i] * w;
+                            for (int i = 0; i < 16; ++i) {
+                                t0[i] = (j == 0 ? 0ll : t0[i]) + (long long)(int)v[i] * w;
+                                t1[i] = (j == 0 ? 0ll : t1[i]) + (long long)(int)v1[i] * w;
+                            }
                         }
-                        tmem_ld_32x32b_x16(tl + 16u, v);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) t1[i] = (long long)(int)v[i];
-#pragma unroll 1
-                        for (int j = 1; j < nlev; ++j) {
-                            tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + 16), v);
-                            tmem_wait_ld();
-                            const int w = 1 << (8 * j);
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) t1[i] += (long long)(int)v[i] * w;
-                        }
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0)
-                            for (int j = 0; j < nlev; ++j) mbar_arrive_cluster(slot_remote0 + 8u * (uint32_t)j);
                         if (rok) {
                             long long *dst = reinterpret_cast<long long *>(p.P0) + (int64_t)sq * plane + off;
 #pragma unroll
@@ -332,18 +326,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                                 if (c0 + 16 + i < p.N) dst[(int64_t)(16 + i) * p.Mp] = t1[i];
                         }
                     } else {
+                        uint32_t v1[16];
 #pragma unroll 1
                         for (int j = 0; j < nlev; ++j) {
                             const int li = (Lmax - np0) - (pa.hi - j);
                             int32_t *dst = p.PL + ((int64_t)sq * p.pk_nl + li) * plane + off;
                             tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN), v);
-                            tmem_wait_ld();
-                            if (rok) {
-#pragma unroll
-                                for (int i = 0; i < 16; ++i)
-                                    if (c0 + i < p.N) dst[(int64_t)i * p.Mp] = (int32_t)v[i];
-                            }
-                            tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + 16), v);
+                            tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + 16), v1);
                             tmem_wait_ld();
                             tc_fence_before();
                             __syncwarp();
@@ -351,7 +340,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                             if (rok) {
 #pragma unroll
                                 for (int i = 0; i < 16; ++i)
-                                    if (c0 + 16 + i < p.N) dst[(int64_t)(16 + i) * p.Mp] = (int32_t)v[i];
+                                    if (c0 + i < p.N) dst[(int64_t)i * p.Mp] = (int32_t)v[i];
+#pragma unroll
+                                for (int i = 0; i < 16; ++i)
+                                    if (c0 + 16 + i < p.N) dst[(int64_t)(16 + i) * p.Mp] = (int32_t)v1[i];
                             }
                         }
                     }
@@ -394,6 +386,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive_cluster(slot_remote0);
+                        if (dbgw && u == (blockIdx.x >> 1)) tl_mark(p, TL_EPI_REL0);
                         if (dbgw) dbg_add(p, DBG_EPI_FIRST_ARRIVE, clock64() - w1);
 #pragma unroll
                         for (int i = 0; i < 16; ++i) t1[i] = (long long)(int)v[i];

@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <unistd.h>
 #include <mutex>
 #include <unordered_map>
 #include <string>
@@ -41,6 +42,32 @@ thread_local int t_full_pairs = 0;   // R21 pair set for Ozaki-I calls (ozaki_se
 thread_local int64_t t_kblock = 0;    // R22 exponent block along K (0 = per row / column)
 thread_local int t_overlap = 0;       // cross-call split / GEMM overlap (ozaki_set_overlap)
 thread_local int64_t t_trsm_nb = 128;  // R23 TRSM block (ozaki_set_trsm_block)
+
+// OZAKI_* test / tuning hooks: one scan of the environment per public call
+// (env_refresh) instead of a getenv per hook per launch; ozenv() reads the snapshot.
+struct EnvSnap {
+    int n = 0;
+    std::string key[16], val[16];
+};
+thread_local EnvSnap t_envs;
+void env_refresh() {
+    EnvSnap &e = t_envs;
+    e.n = 0;
+    for (char **v = environ; v && *v; ++v) {
+        if (strncmp(*v, "OZAKI_", 6) != 0 || e.n >= 16) continue;
+        const char *eq = strchr(*v, '=');
+        if (!eq) continue;
+        e.key[e.n].assign(*v, (size_t)(eq - *v));
+        e.val[e.n].assign(eq + 1);
+        ++e.n;
+    }
+}
+const char *ozenv(const char *name) {
+    const EnvSnap &e = t_envs;
+    for (int i = 0; i < e.n; ++i)
+        if (e.key[i] == name) return e.val[i].c_str();
+    return nullptr;
+}
 
 // Cross-call overlap state per (thread, stream, device): two persistent slice workspaces used
 // alternately, and whether the last kernel this thread put on the stream is an Ozaki-I GEMM
@@ -259,7 +286,7 @@ void plan_splitk(Plan &P, int sms) {
     if (!P.pair || P.kchunk_needed || P.batch == 0) return;
     const int64_t tiles = P.batch * P.tiles_m * P.tiles_n, pairs = sms / 2;
     int64_t S = 1;
-    if (const char *e = getenv("OZAKI_SPLITK")) {
+    if (const char *e = ozenv("OZAKI_SPLITK")) {
         S = std::max<int64_t>(1, std::min<int64_t>(atoll(e), P.KB));
     } else if (2 * tiles <= pairs) {
         S = std::min<int64_t>({pairs / tiles, P.KB / 4, 16});
@@ -608,10 +635,10 @@ int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b,
     const bool fourm = a.mode == SPLIT_A4M && b->mode == SPLIT_B4M;
     const bool threem = a.mode == SPLIT_3M && b->mode == SPLIT_3M;
     if (!real && !fourm && !threem) return 1;
-    if (const char *e = getenv("OZAKI_SPLIT"))
+    if (const char *e = ozenv("OZAKI_SPLIT"))
         if (!strcmp(e, "generic")) return 1;
     int KW = real ? 1024 : 512;
-    if (const char *kw = getenv("OZAKI_SPLIT_KW")) {   // tuning hook: window elements per row
+    if (const char *kw = ozenv("OZAKI_SPLIT_KW")) {   // tuning hook: window elements per row
         const int v = atoi(kw);
         if (v >= 64 && v <= 1024 && v % 32 == 0) KW = v;
     }
@@ -622,12 +649,12 @@ int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b,
     // window) -- OZAKI_SPLIT_LONG=0 / 1 forces the single-kernel / two-kernel form
     const int64_t kpad = fourm ? a.kh : a.KB * 32;
     int nwin = (int)((kpad + KW - 1) / KW);
-    if (nwin == 2 && !getenv("OZAKI_SPLIT_KW")) {   // rows of two windows: one double window
+    if (nwin == 2 && !ozenv("OZAKI_SPLIT_KW")) {   // rows of two windows: one double window
         KW *= 2;                                   // (64 KB per 4-row CTA) beats re-reading the
         nwin = 1;                                  // row from L2 (C4: 0.64 -> 0.47 ms)
     }
     bool lng = nwin >= 3;
-    if (const char *lg = getenv("OZAKI_SPLIT_LONG")) lng = (atoi(lg) != 0) && nwin > 1;
+    if (const char *lg = ozenv("OZAKI_SPLIT_LONG")) lng = (atoi(lg) != 0) && nwin > 1;
     if (lng) {   // short windows, more rows per CTA: 128-B reads per l when rows are adjacent
         RG = real ? 16 : 8;
         KW = 256;
@@ -687,7 +714,7 @@ int launch_split_sides(const Plan &P, const SplitParams &a, const SplitParams *b
     if (int rc = launch_split_fast(P, a, b, grid, st); rc <= 0) return rc;   // production layout
     // SMEM window: 8 rows x KW elements (+ pad), 64 KB
     int KW = cplx ? 512 : 1024;
-    if (const char *kw = getenv("OZAKI_SPLIT_KW")) {   // tuning hook: window elements per row
+    if (const char *kw = ozenv("OZAKI_SPLIT_KW")) {   // tuning hook: window elements per row
         const int v = atoi(kw);
         if (v >= 64 && v <= 1024) KW = cplx ? std::min(v, 512) : v;
     }
@@ -791,7 +818,7 @@ int launch_gemm_lv2(const Plan &P, const GemmParams &gp, size_t a_avail, size_t 
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // overlap K1's tail
-        attr[0].val.programmaticStreamSerializationAllowed = getenv("OZAKI_NO_PDL") ? 0 : 1;
+        attr[0].val.programmaticStreamSerializationAllowed = ozenv("OZAKI_NO_PDL") ? 0 : 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         CUDA_TRY(cudaLaunchKernelEx(&cfg, k_gemm_lv2<EPI, CHUNK, FULL>, P2));
@@ -830,7 +857,7 @@ int launch_gemm_chunked(const Plan &P, const GemmParams &g0, int epi, int64_t kc
     int64_t panel = ((int64_t)2 << 30) / ((int64_t)s * Mp * 8);
     panel = std::max<int64_t>(kLvBN, panel / kLvBN * kLvBN);
     panel = std::min<int64_t>(panel, P.tiles_n * kLvBN);
-    if (const char *pe = getenv("OZAKI_PANEL_COLS"))     // test hook: force narrow panels
+    if (const char *pe = ozenv("OZAKI_PANEL_COLS"))     // test hook: force narrow panels
         panel = std::max<int64_t>(kLvBN, std::min<int64_t>(panel, atoll(pe) / kLvBN * kLvBN));
     double *W = nullptr;
     const size_t wbytes = (size_t)s * Mp * panel * sizeof(double);
@@ -895,7 +922,7 @@ int launch_gemm_splitk(const Plan &P, GemmParams gp, int epi, int64_t *P0, int32
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = getenv("OZAKI_NO_PDL") ? 0 : 1;
+    attr[0].val.programmaticStreamSerializationAllowed = ozenv("OZAKI_NO_PDL") ? 0 : 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     {
@@ -952,7 +979,7 @@ int launch_gemm(const Plan &P, int epi, const int8_t *sa, const int8_t *sb, cons
         gp.dbg = g_dbg;
     }
     if (P.pair) {
-        const char *ev = getenv("OZAKI_KCHUNK_KB");   // test hook: force a small K chunk
+        const char *ev = ozenv("OZAKI_KCHUNK_KB");   // test hook: force a small K chunk
         const int64_t kc_env = ev ? atoll(ev) : 0;
         if ((P.kchunk_needed || kc_env > 0) && epi != EPI_LEVELS)
             return launch_gemm_chunked(P, gp, epi, kc_env, dev, st);
@@ -1240,7 +1267,7 @@ int run_offload(const Call &c) {
     const bool readC = !(c.be[0] == 0.0 && c.be[1] == 0.0);
     const size_t per_entry = (size_t)(spanA + spanB + spanC) * es;
     size_t chunk_bytes = 32ull << 20;   // ~32 MB per chunk (measured best: 5.6 vs 5.9 ms for C2x30; OZAKI_OFFLOAD_CHUNK_MB overrides)
-    if (const char *ce = getenv("OZAKI_OFFLOAD_CHUNK_MB")) {
+    if (const char *ce = ozenv("OZAKI_OFFLOAD_CHUNK_MB")) {
         const long long v = atoll(ce);
         if (v >= 1 && v <= 4096) chunk_bytes = (size_t)v << 20;
     }
@@ -1447,7 +1474,7 @@ void launch_crt_fast(bool real, bool lng, dim3 grid, size_t smem, cudaStream_t s
 }
 
 int launch_split_fast_crt(const SplitParams &a, const SplitParams &b, int64_t batch, cudaStream_t st) {
-    if (const char *e = getenv("OZAKI_SPLIT"))
+    if (const char *e = ozenv("OZAKI_SPLIT"))
         if (!strcmp(e, "generic")) return 1;
     const bool real = a.mode == SPLIT_REAL;
     const int64_t rows_grid = std::max(a.rows_grid, b.rows_grid);
@@ -1460,7 +1487,7 @@ int launch_split_fast_crt(const SplitParams &a, const SplitParams &b, int64_t ba
         nwin = 1;
     }
     bool lng = nwin >= 3;
-    if (const char *lg = getenv("OZAKI_SPLIT_LONG")) lng = (atoi(lg) != 0) && nwin > 1;
+    if (const char *lg = ozenv("OZAKI_SPLIT_LONG")) lng = (atoi(lg) != 0) && nwin > 1;
     if (lng) {
         RG = real ? 16 : 8;
         KW = 256;
@@ -1703,7 +1730,7 @@ int run(const Call &c0) {
                 // tile; every panel call re-splits op(A), so panels are not made smaller)
                 const size_t es = (c.kind == KIND_REAL) ? 8 : 16;
                 int64_t panel = (int64_t)((96ull << 20) / std::max<size_t>(1, (size_t)(c.k + c.m) * es));
-                if (const char *pe = getenv("OZAKI_OFFLOAD_PANEL_COLS")) panel = atoll(pe);
+                if (const char *pe = ozenv("OZAKI_OFFLOAD_PANEL_COLS")) panel = atoll(pe);
                 panel = std::max<int64_t>(128, panel / 128 * 128);
                 if (c.n >= 2 * panel) return run_offload_panels(c, panel);
             }
@@ -2034,6 +2061,7 @@ int run_trsm_device(const TrsmCall &c, DevState *dev, cudaStream_t st) {
 
 int run_trsm(const TrsmCall &c0) {
     t_err.clear();
+    env_refresh();
     if (int rc = validate_trsm(c0)) return rc;
     TrsmCall c = c0;
     if (c.m == 0 || c.n == 0) return 0;
@@ -2077,6 +2105,7 @@ Call make_call(Kind kind, char ta, char tb, int64_t m, int64_t n, int64_t k, con
                const double *A, int64_t lda, int64_t sA, const double *B, int64_t ldb, int64_t sB,
                const double *be, double *C, int64_t ldc, int64_t sC, int64_t batch, int s,
                bool batched) {
+    env_refresh();
     Call c{};
     c.kind = kind;
     c.ta = ta;
@@ -2364,6 +2393,7 @@ const char *ozaki_version(void) { return "ozaki-b200 0.1 (sm_100a, tcgen05 kind:
 int ozaki_debug_split(char side, char kind, char trans, int64_t rows, int64_t cols,
                       const double *X, int64_t ldx, int num_slices, int8_t *slices_out,
                       int32_t *exps_out, int64_t *kdepth_out) {
+    env_refresh();
     t_err.clear();
     side = up(side);
     trans = up(trans);

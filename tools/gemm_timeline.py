@@ -14,7 +14,7 @@ import synth  # noqa: E402
 import paper_2603_29975_b200 as oz  # noqa: E402
 
 EV = ["entry", "prologue", "depwait", "tma0_issued", "full0", "mma_pass0_done", "mma_end", "epi_pass0",
-      "epi_last_pass", "epi_store_done", "exit", "epi_drained", "epi_probe_loads"]
+      "epi_last_pass", "epi_store_done", "exit", "epi_drained", "epi_probe_loads", "mma_slots_pass1", "epi_release_slot0", "mma_full_pass1"]
 
 
 def dev(x):

@@ -47,6 +47,30 @@ for n in (1024, 2048):
     C = dev(np.zeros((n, n)))
     cases.append((f"DGEMM {n}^3 s=7", 2 * n ** 3, lambda A=A, B=B, C=C: oz.dgemm("N", "N", 1.0, A, B, 0.0, C, 7)))
 
+# raw C-ABI calls (arguments marshalled once): the library's own host time per call
+import ctypes  # noqa: E402
+L = oz.lib()
+L.ozaki_set_stream(ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+Ar = dev(synth.kkr(512, 512, seed=1000, gamma=3.0))
+Br = dev(synth.kkr(512, 512, seed=1001, gamma=3.0))
+Cr = dev(np.zeros((512, 512), complex))
+one, zero = (ctypes.c_double * 2)(1.0, 0.0), (ctypes.c_double * 2)(0.0, 0.0)
+raw_args = (b"N", b"N", 512, 512, 512, one, Ar.data_ptr(), 512, Br.data_ptr(), 512, zero, Cr.data_ptr(), 512, 7)
+a64, b64, c64 = dev(synth.uniform(64, 64, 1)), dev(synth.uniform(64, 64, 2)), dev(np.zeros((64, 64)))
+raw64 = (b"N", b"N", 64, 64, 64, 1.0, a64.data_ptr(), 64, b64.data_ptr(), 64, 0.0, c64.data_ptr(), 64, 7)
+for nm, f, args in (("raw ozaki_zgemm 512^3 s=7", L.ozaki_zgemm, raw_args), ("raw ozaki_dgemm 64^3 s=7", L.ozaki_dgemm, raw64)):
+    for _ in range(5):
+        f(*args)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(a.reps):
+        f(*args)
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    print(json.dumps({"case": nm, "splitk": a.splitk, "host_us_per_call": round((t1 - t0) / a.reps * 1e6, 2),
+                      "wall_us_per_call_incl_drain": round((t2 - t0) / a.reps * 1e6, 2)}), flush=True)
+
 st = torch.cuda.current_stream()
 for name, flops, fn in cases:
     for _ in range(5):
