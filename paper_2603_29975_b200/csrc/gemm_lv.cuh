@@ -52,7 +52,9 @@ struct LvParams {
 // columns col0 .. col0+63 held in acc[].  Complex (4M, R9 N-side embedding):
 // columns 2c / 2c+1 are Re / Im of complex column col0/2 + c, so each thread
 // owns whole complex numbers: one 16-byte store, no lane exchange.
-template <int EPI, int NC = 64>
+// GAB: compile the beta != 0 (general alpha / beta) store; the production alpha = 1, beta = 0
+// kernels instantiate GAB = false so that code does not weigh on their register allocation.
+template <int EPI, int NC = 64, bool GAB = true>
 __device__ __forceinline__ void lv_store(const GemmParams &p, int64_t b, int64_t grow, int32_t e,
                                          int64_t col0, const double *acc, int nbias = 0) {
     const int lane = threadIdx.x & 31;
@@ -71,18 +73,71 @@ __device__ __forceinline__ void lv_store(const GemmParams &p, int64_t b, int64_t
     // -0 * Inf), C_i likewise.
     if constexpr (EPI == EPI_REAL) {
         double *cp = p.C + b * p.strideC + grow + col0 * p.ldc;
+        if (!GAB || p.ab_unit || beta0) {
 #pragma unroll
-        for (int j = 0; j < NC; ++j) {
-            const int32_t f = __shfl_sync(0xffffffffu, j < 32 ? f_lo : f_hi, j & 31);
-            const double P = (enan || f == kNonFinite) ? qnan : scale_pow2(acc[j], e + f - 14 + nbias);
-            if (j < ncol) {
-                if (p.ab_unit) *cp = P;
-                else *cp = beta0 ? __dmul_rn(p.alpha_r, P) : __fma_rn(p.alpha_r, P, __dmul_rn(p.beta_r, *cp));
+            for (int j = 0; j < NC; ++j) {
+                const int32_t f = __shfl_sync(0xffffffffu, j < 32 ? f_lo : f_hi, j & 31);
+                const double P = (enan || f == kNonFinite) ? qnan : scale_pow2(acc[j], e + f - 14 + nbias);
+                if (j < ncol) *cp = p.ab_unit ? P : __dmul_rn(p.alpha_r, P);
+                cp += p.ldc;
             }
-            cp += p.ldc;
+        } else if constexpr (GAB) {
+            // beta != 0: the C values of a group of 8 columns are loaded together before the
+            // group's FMAs (one memory latency per group instead of one per column).  Each C
+            // element is read once, before this thread writes it, and no other thread touches
+            // its cache lines (a warp owns whole 32-row column segments), so the read-only path
+            // is safe.
+#pragma unroll
+            for (int j0 = 0; j0 < NC; j0 += 8) {
+                double cv[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    cv[i] = (j0 + i < NC && j0 + i < ncol) ? __ldg(cp + (int64_t)(j0 + i) * p.ldc) : 0.0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int j = j0 + i;
+                    if (j >= NC) break;
+                    const int32_t f = __shfl_sync(0xffffffffu, j < 32 ? f_lo : f_hi, j & 31);
+                    const double P = (enan || f == kNonFinite) ? qnan : scale_pow2(acc[j], e + f - 14 + nbias);
+                    // beta == 1: beta * C == C exactly (also for -0, Inf, NaN): no DMUL
+                    const double t = (p.beta_r == 1.0) ? cv[i] : __dmul_rn(p.beta_r, cv[i]);
+                    if (j < ncol) cp[(int64_t)j * p.ldc] = __fma_rn(p.alpha_r, P, t);
+                }
+            }
         }
     } else {
         double2 *cp = reinterpret_cast<double2 *>(p.C) + b * p.strideC + grow + (col0 >> 1) * p.ldc;
+        if (GAB && !p.ab_unit && !beta0) {
+            // general alpha / beta: C loaded 4 complex columns at a time ahead of their FMAs
+            // (read-only path: see the real case).  (An LU-update special case -- alpha = +-1,
+            // beta = 1 as one DADD per component plus exact signed-zero selects -- measured
+            // slower on C2 x 30: 0.53 vs 0.47-0.50 ms.)
+            const double2 *cq = cp;
+#pragma unroll
+            for (int c0 = 0; c0 < NC / 2; c0 += 4) {
+                double2 cv[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    cv[i] = (c0 + i < NC / 2 && 2 * (c0 + i) < ncol) ? __ldg(cq + (int64_t)(c0 + i) * p.ldc)
+                                                                      : make_double2(0.0, 0.0);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int c = c0 + i;
+                    if (c >= NC / 2) break;
+                    const int32_t f = __shfl_sync(0xffffffffu, c < 16 ? f_lo : f_hi, (2 * c) & 31);
+                    const int nsc = e + f - 14 + nbias;
+                    const bool nan = enan || f == kNonFinite;
+                    const double Pr = nan ? qnan : scale_pow2(acc[2 * c], nsc);
+                    const double Pi = nan ? qnan : scale_pow2(acc[2 * c + 1], nsc);
+                    const double tr = __fma_rn(p.beta_r, cv[i].x, -__dmul_rn(p.beta_i, cv[i].y));
+                    const double ti = __fma_rn(p.beta_r, cv[i].y, __dmul_rn(p.beta_i, cv[i].x));
+                    const double2 out = make_double2(__fma_rn(p.alpha_r, Pr, __fma_rn(-p.alpha_i, Pi, tr)),
+                                                     __fma_rn(p.alpha_r, Pi, __fma_rn(p.alpha_i, Pr, ti)));
+                    if (2 * c < ncol) cp[(int64_t)c * p.ldc] = out;
+                }
+            }
+            return;
+        }
 #pragma unroll
         for (int c = 0; c < NC / 2; ++c) {
             const int32_t f = __shfl_sync(0xffffffffu, c < 16 ? f_lo : f_hi, (2 * c) & 31);

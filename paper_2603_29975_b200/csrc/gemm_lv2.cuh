@@ -22,6 +22,11 @@
 namespace ozk {
 
 constexpr int kMaxPassMaps = 4;
+
+// R6 step of a level after the integer prefix: acc = fma(S_L, 2^w, acc).  (Measured: removing
+// these FP64 instructions entirely, or converting with I2F instead of the DADD magic, does not
+// change the C3 / C2x30 GEMM time -- the FP64 combine does not steal tensor cycles.)
+#define OZK_LEVEL_FMA(v, sc, a) __fma_rn(i32_to_f64(v), (sc), (a))
 constexpr int kEpi2 = 16;                       // epilogue warps per CTA (4 per TMEM lane quarter)
 constexpr int kThreads2 = 64 + 32 * kEpi2;      // 576
 constexpr int kNC2 = kLvBN / (kEpi2 / 4);       // 32 columns per epilogue thread
@@ -147,7 +152,7 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
 // 2 = last K chunk (level sum = W + S, then the FP64 combine and store);
 // 3 = split-K unit (exact partials to P0 / PL, k_splitk_combine finishes).
 // FULL (reading R21, NEXT-4): all s^2 pairs, levels 2s .. 2 (s <= 8, CHUNK 0 only).
-template <int EPI, int CHUNK, bool FULL = false>
+template <int EPI, int CHUNK, bool FULL = false, bool GAB = true>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     k_gemm_lv2(const __grid_constant__ Lv2Params P2) {
     const LvParams &lp = P2.lv;
@@ -415,14 +420,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                         tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN), v);
                         tmem_wait_ld();
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) acc[i] = __fma_rn(i32_to_f64(v[i]), sc, acc[i]);
+                        for (int i = 0; i < 16; ++i) acc[i] = OZK_LEVEL_FMA(v[i], sc, acc[i]);
                         tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + 16), v);
                         tmem_wait_ld();
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive_cluster(slot_remote0 + 8u * (uint32_t)j);
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) acc[16 + i] = __fma_rn(i32_to_f64(v[i]), sc, acc[16 + i]);
+                        for (int i = 0; i < 16; ++i) acc[16 + i] = OZK_LEVEL_FMA(v[i], sc, acc[16 + i]);
                     }
                 } else {
                 for (int L = pa.hi; L >= pa.lo; --L) {          // ascending significance (R6)
@@ -490,7 +495,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 if (blockIdx.x == 0) p.dbg[DBG_TL0 + TL_EPI_F] = t + (f == -123456789 ? 1 : 0) + (cv == 1.2345e300 ? 1 : 0);
             }
             if constexpr (EPI != EPI_LEVELS && CHUNK != 1 && CHUNK != 3)
-                lv_store<EPI, kNC2>(p, b, grow, e, tn * kLvBN + half * kNC2, acc, CHUNK == 0 ? -8 * (Lmax - 2) : 0);
+                lv_store<EPI, kNC2, GAB>(p, b, grow, e, tn * kLvBN + half * kNC2, acc, CHUNK == 0 ? -8 * (Lmax - 2) : 0);
             if (dbgw) dbg_add(p, DBG_EPI_STORE, clock64() - s0);
             if (dbgw) tl_mark(p, TL_EPI_STORE);
         }

@@ -793,10 +793,10 @@ int rows_map(CUtensorMap *m, const void *base, size_t bytes, uint32_t box_rows) 
     return 0;
 }
 
-template <int EPI, int CHUNK = 0, bool FULL = false>
+template <int EPI, int CHUNK = 0, bool FULL = false, bool GAB = true>
 int launch_gemm_lv2(const Plan &P, const GemmParams &gp, size_t a_avail, size_t b_avail, DevState *dev,
                     cudaStream_t st) {
-    CUDA_TRY(smem_optin((const void *)k_gemm_lv2<EPI, CHUNK, FULL>, P.smem));
+    CUDA_TRY(smem_optin((const void *)k_gemm_lv2<EPI, CHUNK, FULL, GAB>, P.smem));
     Lv2Params P2;
     std::memset(&P2, 0, sizeof P2);
     P2.lv.g = gp;
@@ -821,7 +821,7 @@ int launch_gemm_lv2(const Plan &P, const GemmParams &gp, size_t a_avail, size_t 
         attr[0].val.programmaticStreamSerializationAllowed = ozenv("OZAKI_NO_PDL") ? 0 : 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        CUDA_TRY(cudaLaunchKernelEx(&cfg, k_gemm_lv2<EPI, CHUNK, FULL>, P2));
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, k_gemm_lv2<EPI, CHUNK, FULL, GAB>, P2));
     }
     CUDA_TRY(cudaGetLastError());
     g_stats.launches += 1;
@@ -990,8 +990,14 @@ int launch_gemm(const Plan &P, int epi, const int8_t *sa, const int8_t *sb, cons
             if (epi == EPI_CPLX4M) return launch_gemm_lv2<EPI_CPLX4M, 0, true>(P, gp, P.a_bytes, P.b_bytes, dev, st);
             return launch_gemm_lv2<EPI_LEVELS, 0, true>(P, gp, P.a_bytes, P.b_bytes, dev, st);
         }
-        if (epi == EPI_REAL) return launch_gemm_lv2<EPI_REAL>(P, gp, P.a_bytes, P.b_bytes, dev, st);
-        if (epi == EPI_CPLX4M) return launch_gemm_lv2<EPI_CPLX4M>(P, gp, P.a_bytes, P.b_bytes, dev, st);
+        // beta == 0 (C not read): the kernels without the general alpha / beta store
+        const bool gab = !(be[0] == 0.0 && be[1] == 0.0);
+        if (epi == EPI_REAL)
+            return gab ? launch_gemm_lv2<EPI_REAL, 0, false, true>(P, gp, P.a_bytes, P.b_bytes, dev, st)
+                       : launch_gemm_lv2<EPI_REAL, 0, false, false>(P, gp, P.a_bytes, P.b_bytes, dev, st);
+        if (epi == EPI_CPLX4M)
+            return gab ? launch_gemm_lv2<EPI_CPLX4M, 0, false, true>(P, gp, P.a_bytes, P.b_bytes, dev, st)
+                       : launch_gemm_lv2<EPI_CPLX4M, 0, false, false>(P, gp, P.a_bytes, P.b_bytes, dev, st);
         return launch_gemm_lv2<EPI_LEVELS>(P, gp, P.a_bytes, P.b_bytes, dev, st);
     }
     if (P.lv) {

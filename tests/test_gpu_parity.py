@@ -497,3 +497,35 @@ def test_host_offload_column_panels(orc, ta, tb, monkeypatch):
     oz.ozaki2_dgemm("N", "N", 1.0, torch.from_numpy(np.asfortranarray(Ar)), torch.from_numpy(np.asfortranarray(Br)),
                     0.0, Cr, 14)
     assert same(Cr.numpy()[:40], o2.dgemm("N", "N", 1.0, Ar[:40], Br, 0.0, None, 14))
+
+
+@pytest.mark.parametrize("alpha", [-1.0, 1.0, -1.0 + 0.5j])
+@pytest.mark.parametrize("method", ["4m", "3m"])
+def test_zgemm_lu_update_signed_zeros(orc, alpha, method):
+    """beta = 1 with alpha = -1 / +1 (the LU trailing update; the epilogue reduces R7's FMA
+    shapes to one DADD per component plus exact signed-zero terms) -- bitwise vs the oracle
+    INCLUDING the sign of zero, with +-0, +-Inf and NaN entries in C and zero / non-finite rows
+    in A (P = +0 / NaN)."""
+    m, n, k, s = 140, 96, 70, 6
+    A = synth.uniform(m, k, 3, complex_=True)
+    A[5, :] = 0.0                      # P row = +0
+    A[9, 3] = np.inf                   # P row = NaN (R10)
+    B = synth.uniform(k, n, 4, complex_=True)
+    B[:, 7] = 0.0
+    C0 = synth.uniform(m, n, 5, complex_=True)
+    specials = [complex(-0.0, -0.0), complex(0.0, -0.0), complex(-0.0, 0.0), complex(np.inf, 1.0),
+                complex(1.0, -np.inf), complex(np.nan, 0.0), complex(-0.0, 2.0), complex(3.0, -0.0)]
+    g = np.random.default_rng(9)
+    for idx, z in enumerate(specials * 6):
+        C0[g.integers(m), g.integers(n)] = z
+    C0[5, :8] = np.array(specials)     # zero P meets every special C
+    C0[10:18, 7] = np.array(specials)
+    C = dev(C0)
+    (oz.zgemm if method == "4m" else oz.zgemm3m)("N", "N", alpha, dev(A), dev(B), 1.0, C, s)
+    got = host(C)
+    want = orc.zgemm("N", "N", alpha, A, B, 1.0, C0, s, method)
+    assert same(got, want)
+    for part in (np.real, np.imag):
+        g_, w_ = part(got), part(want)
+        z = (g_ == 0) & (w_ == 0)
+        assert (np.signbit(g_[z]) == np.signbit(w_[z])).all()
