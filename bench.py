@@ -945,8 +945,9 @@ def hbm_peak():
 
 def c3_e2e_leg(torch, oz, A_h, B_h, n, s, device, rank, world, args):
     """End to end through the public API with pinned HOST buffers: ozaki_dgemm on host pointers
-    (the library's offload path: H2D of A and of B's column panels, GEMM panels and D2H of C's
-    panels overlapped on three streams) -- with N ranks each rank runs its column slab of C."""
+    (the library's offload path: row panels of A and column panels of B moved once each, block
+    (i, j) of C computed and copied back as soon as its panels are in, H2D / GEMM / D2H on three
+    streams) -- with N ranks each rank runs its column slab of C."""
     import torch.distributed as dist
     from paper_2603_29975_b200 import dist as zd
     j0, j1 = zd.column_slab(n, rank, world)
@@ -969,7 +970,7 @@ def c3_e2e_leg(torch, oz, A_h, B_h, n, s, device, rank, world, args):
             "ms_per_step": round(ms, 3),
             "h2d_bytes_per_step": int((Ap.numel() + Bp.numel()) * 8 * world),
             "d2h_bytes_per_step": int(Cp.numel() * 8 * world),
-            "path": "ozaki_dgemm on pinned HOST tensors (library offload path), "
+            "path": "ozaki_dgemm on pinned HOST tensors (library 2-D block offload), "
                     + ("column slab per rank" if world > 1 else "one call per step")}
 
 

@@ -774,7 +774,24 @@ int launch_gemm_lv(const Plan &P, const GemmParams &gp, DevState *dev, cudaStrea
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
+// Encoded maps are cached per thread by (base, bytes, box): the workspaces come back at the
+// same addresses (stream-ordered pool, persistent overlap buffers), and an encode is ~1 µs of
+// host time per map (2 x passes maps per GEMM launch).
+struct MapCacheEntry {
+    const void *base = nullptr;
+    size_t bytes = 0;
+    uint32_t box = 0;
+    CUtensorMap map;
+};
+thread_local MapCacheEntry t_maps[32];
+thread_local unsigned t_maps_next = 0;
+
 int rows_map(CUtensorMap *m, const void *base, size_t bytes, uint32_t box_rows) {
+    for (const MapCacheEntry &c : t_maps)
+        if (c.base == base && c.bytes == bytes && c.box == box_rows) {
+            *m = c.map;
+            return 0;
+        }
     if (!g_encode) {
         cudaDriverEntryPointQueryResult q;
         void *fn = nullptr;
@@ -790,6 +807,11 @@ int rows_map(CUtensorMap *m, const void *base, size_t bytes, uint32_t box_rows) 
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(OZAKI_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    MapCacheEntry &c = t_maps[t_maps_next++ % 32];
+    c.base = base;
+    c.bytes = bytes;
+    c.box = box_rows;
+    c.map = *m;
     return 0;
 }
 
@@ -1176,85 +1198,109 @@ int offload_ctx(OffloadCtx **out) {
     return 0;
 }
 
-// One large GEMM on host pointers (batch == 1): op(A) is staged once, then op(B) and C move
-// in column panels, double-buffered, so the H2D copy of panel p+1, the GEMM of panel p and the
-// D2H copy of panel p-1 overlap.  Row exponents come from full rows of op(A) and column
-// exponents are per column, so every element is computed exactly as by one call (bitwise).
-int run_offload_panels(const Call &c, int64_t panel) {
+// One large GEMM on host pointers (batch == 1), in 2-D blocks: op(A) moves in row blocks and
+// op(B) in column blocks, each ONCE (they stay resident), and block (i, j) of C is computed as
+// soon as A_i and B_j have arrived, so the D2H copies of C start after the first block instead
+// of after all of op(A) (PCIe runs both directions at once).  Order: A_0, B_0, B_1, ..., then
+// A_1, A_2, ...  Row exponents come from full rows of op(A) and column exponents are per column,
+// so every element is computed exactly as by one call (bitwise).
+int run_offload_blocks(const Call &c, int64_t rb, int64_t cb) {
     const size_t es = (c.kind == KIND_REAL) ? 8 : 16;
-    const int64_t ar = c.ta == 'N' ? c.m : c.k, ac = c.ta == 'N' ? c.k : c.m;
-    const int64_t spanA = (ac - 1) * c.lda + ar;
+    const int64_t ew = (c.kind == KIND_REAL) ? 1 : 2;      // doubles per element
+    const bool an = c.ta == 'N', bn = c.tb == 'N';
+    const int64_t ar = an ? c.m : c.k, br = bn ? c.k : c.n;  // device leading dimensions (packed)
     const bool readC = !(c.be[0] == 0.0 && c.be[1] == 0.0);
-    // one panel of op(B) columns j0..j0+w: 'N' -> w columns of B (pitch ldb, k rows each);
-    // 'T'/'C' -> w rows of B (pitch ldb, w elements each, k columns)
-    const int64_t bl = (c.tb == 'N') ? c.k : panel;   // device leading dimension of the B panel
-    const size_t bbytes = (size_t)panel * c.k * es, cbytes = (size_t)panel * c.m * es;
+    const int64_t I = (c.m + rb - 1) / rb, J = (c.n + cb - 1) / cb;
     OffloadCtx *o = nullptr;
     if (int rc = offload_ctx(&o)) return rc;
-    const size_t need = (size_t)spanA * es + 2 * (bbytes + cbytes);
+    const size_t abytes = al256((size_t)c.m * c.k * es), bbytes = al256((size_t)c.k * c.n * es);
+    const size_t need = abytes + bbytes + (size_t)c.m * c.n * es;
     if (o->cap < need) {
         CUDA_TRY(cudaStreamSynchronize(o->d2h));
-        for (int i = 0; i < 2; ++i) {
-            if (o->buf[i]) cudaFree(o->buf[i]);
-            o->buf[i] = nullptr;
+        for (int q = 0; q < 2; ++q) {
+            if (o->buf[q]) cudaFree(o->buf[q]);
+            o->buf[q] = nullptr;
         }
         o->cap = 0;
         cudaError_t e = cudaMalloc(&o->buf[0], need);
         if (e != cudaSuccess) return fail(OZAKI_ERR_ALLOC, "offload staging (%zu B): %s", need, cudaGetErrorString(e));
         o->cap = need;
     }
-    char *base = o->buf[0];
-    double *dA = (double *)base;
-    char *pb[2] = {base + (size_t)spanA * es, base + (size_t)spanA * es + bbytes + cbytes};
+    double *dA = (double *)o->buf[0];
+    double *dB = (double *)(o->buf[0] + abytes);
+    double *dC = (double *)(o->buf[0] + abytes + bbytes);
+    std::vector<cudaEvent_t> ev((size_t)(I + J + 2 * I * J), nullptr);
+    for (auto &x : ev) CUDA_TRY(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    cudaEvent_t *a_done = ev.data(), *b_done = a_done + I, *in_done = b_done + J, *cmp_done = in_done + I * J;
     cudaStream_t user = t_stream;
     CUDA_TRY(cudaEventRecord(o->start, user));
     CUDA_TRY(cudaStreamWaitEvent(o->h2d, o->start, 0));
-    CUDA_TRY(cudaMemcpyAsync(dA, c.A, (size_t)spanA * es, cudaMemcpyHostToDevice, o->h2d));
-    const int64_t np = (c.n + panel - 1) / panel;
-    int rc = 0;
-    for (int64_t p = 0; p < np && !rc; ++p) {
-        const int set = (int)(p & 1);
-        const int64_t j0 = p * panel, w = std::min<int64_t>(panel, c.n - j0);
-        double *dB = (double *)pb[set];
-        double *dC = (double *)(pb[set] + bbytes);
-        if (p >= 2) CUDA_TRY(cudaStreamWaitEvent(o->h2d, o->out_done[set], 0));   // panel set reuse
-        const char *hB = (const char *)c.B + (size_t)(c.tb == 'N' ? j0 * c.ldb : j0) * es;
-        if (c.tb == 'N')
-            CUDA_TRY(cudaMemcpy2DAsync(dB, (size_t)bl * es, hB, (size_t)c.ldb * es, (size_t)c.k * es, (size_t)w,
+    auto copy_a = [&](int64_t i) -> int {   // op(A) rows [i0, i1)
+        const int64_t i0 = i * rb, h = std::min<int64_t>(rb, c.m - i0);
+        if (an)
+            CUDA_TRY(cudaMemcpy2DAsync(dA + ew * i0, ar * es, (const char *)c.A + i0 * es, c.lda * es, h * es, c.k,
                                        cudaMemcpyHostToDevice, o->h2d));
         else
-            CUDA_TRY(cudaMemcpy2DAsync(dB, (size_t)bl * es, hB, (size_t)c.ldb * es, (size_t)w * es, (size_t)c.k,
+            CUDA_TRY(cudaMemcpy2DAsync(dA + ew * i0 * ar, ar * es, (const char *)c.A + i0 * c.lda * es, c.lda * es,
+                                       c.k * es, h, cudaMemcpyHostToDevice, o->h2d));
+        CUDA_TRY(cudaEventRecord(a_done[i], o->h2d));
+        return 0;
+    };
+    auto copy_b = [&](int64_t j) -> int {   // op(B) columns [j0, j1)
+        const int64_t j0 = j * cb, w = std::min<int64_t>(cb, c.n - j0);
+        if (bn)
+            CUDA_TRY(cudaMemcpy2DAsync(dB + ew * j0 * br, br * es, (const char *)c.B + j0 * c.ldb * es, c.ldb * es,
+                                       c.k * es, w, cudaMemcpyHostToDevice, o->h2d));
+        else
+            CUDA_TRY(cudaMemcpy2DAsync(dB + ew * j0, br * es, (const char *)c.B + j0 * es, c.ldb * es, w * es, c.k,
                                        cudaMemcpyHostToDevice, o->h2d));
-        char *hC = (char *)c.C + (size_t)j0 * c.ldc * es;
-        if (readC)
-            CUDA_TRY(cudaMemcpy2DAsync(dC, (size_t)c.m * es, hC, (size_t)c.ldc * es, (size_t)c.m * es, (size_t)w,
-                                       cudaMemcpyHostToDevice, o->h2d));
-        CUDA_TRY(cudaEventRecord(o->in_done[set], o->h2d));
-        CUDA_TRY(cudaStreamWaitEvent(o->comp, o->in_done[set], 0));
-        Call d = c;
-        d.A = dA;
-        d.B = dB;
-        d.ldb = bl;
-        d.C = dC;
-        d.ldc = c.m;
-        d.n = w;
-        d.sA = d.sB = d.sC = 0;
-        t_stream = o->comp;
-        const int ovs = t_overlap;
-        t_overlap = 0;
-        rc = run(d);
-        t_overlap = ovs;
-        t_stream = user;
-        if (rc) break;
-        CUDA_TRY(cudaEventRecord(o->comp_done[set], o->comp));
-        CUDA_TRY(cudaStreamWaitEvent(o->d2h, o->comp_done[set], 0));
-        CUDA_TRY(cudaMemcpy2DAsync(hC, (size_t)c.ldc * es, dC, (size_t)c.m * es, (size_t)c.m * es, (size_t)w,
-                                   cudaMemcpyDeviceToHost, o->d2h));
-        CUDA_TRY(cudaEventRecord(o->out_done[set], o->d2h));
+        CUDA_TRY(cudaEventRecord(b_done[j], o->h2d));
+        return 0;
+    };
+    int rc = 0;
+    for (int64_t i = 0; i < I && !rc; ++i) {
+        rc = copy_a(i);
+        for (int64_t j = 0; j < J && !rc; ++j) {
+            if (i == 0 && (rc = copy_b(j))) break;
+            const int64_t i0 = i * rb, h = std::min<int64_t>(rb, c.m - i0);
+            const int64_t j0 = j * cb, w = std::min<int64_t>(cb, c.n - j0);
+            double *dCij = dC + ew * (i0 + j0 * c.m);
+            char *hC = (char *)c.C + (i0 + j0 * c.ldc) * es;
+            const int64_t q = i * J + j;
+            if (readC) {
+                CUDA_TRY(cudaMemcpy2DAsync(dCij, c.m * es, hC, c.ldc * es, h * es, w, cudaMemcpyHostToDevice, o->h2d));
+                CUDA_TRY(cudaEventRecord(in_done[q], o->h2d));
+                CUDA_TRY(cudaStreamWaitEvent(o->comp, in_done[q], 0));
+            }
+            CUDA_TRY(cudaStreamWaitEvent(o->comp, a_done[i], 0));
+            CUDA_TRY(cudaStreamWaitEvent(o->comp, b_done[j], 0));
+            Call d = c;
+            d.A = dA + ew * (an ? i0 : i0 * ar);
+            d.lda = ar;
+            d.B = dB + ew * (bn ? j0 * br : j0);
+            d.ldb = br;
+            d.C = dCij;
+            d.ldc = c.m;
+            d.m = h;
+            d.n = w;
+            d.sA = d.sB = d.sC = 0;
+            t_stream = o->comp;
+            const int ovs = t_overlap;
+            t_overlap = 0;
+            rc = run(d);
+            t_overlap = ovs;
+            t_stream = user;
+            if (rc) break;
+            CUDA_TRY(cudaEventRecord(cmp_done[q], o->comp));
+            CUDA_TRY(cudaStreamWaitEvent(o->d2h, cmp_done[q], 0));
+            CUDA_TRY(cudaMemcpy2DAsync(hC, c.ldc * es, dCij, c.m * es, h * es, w, cudaMemcpyDeviceToHost, o->d2h));
+        }
     }
     cudaEventRecord(o->start, o->d2h);
     cudaStreamWaitEvent(user, o->start, 0);
     cudaError_t e = cudaStreamSynchronize(o->d2h);
+    cudaStreamSynchronize(o->comp);
+    for (auto &x : ev) cudaEventDestroy(x);
     if (!rc && e != cudaSuccess) rc = fail(OZAKI_ERR_CUDA, "offload: %s", cudaGetErrorString(e));
     return rc;
 }
@@ -1732,13 +1778,15 @@ int run(const Call &c0) {
                 return fail(OZAKI_ERR_UNSUPPORTED, "A, B, C must all be device or all be host pointers");
             if (!readsAB && c.be[0] == 1.0 && c.be[1] == 0.0) return 0;   // quick return, C unchanged
             if (readsAB && c.batch == 1) {
-                // one large GEMM: column panels of ~96 MB of op(B) + C (multiples of the 128-column
-                // tile; every panel call re-splits op(A), so panels are not made smaller)
+                // one large GEMM: 2-D blocks of ~128 MB row panels of op(A) / column panels of op(B)
+                // (multiples of the 256-row / 128-column super-tile; every block call re-splits its
+                // panels, which the GPU hides under the PCIe time)
                 const size_t es = (c.kind == KIND_REAL) ? 8 : 16;
-                int64_t panel = (int64_t)((96ull << 20) / std::max<size_t>(1, (size_t)(c.k + c.m) * es));
-                if (const char *pe = ozenv("OZAKI_OFFLOAD_PANEL_COLS")) panel = atoll(pe);
-                panel = std::max<int64_t>(128, panel / 128 * 128);
-                if (c.n >= 2 * panel) return run_offload_panels(c, panel);
+                const int64_t per = (int64_t)((128ull << 20) / std::max<size_t>(1, (size_t)c.k * es));
+                int64_t rb = std::max<int64_t>(256, per / 256 * 256), cb = std::max<int64_t>(128, per / 128 * 128);
+                if (const char *pe = ozenv("OZAKI_OFFLOAD_PANEL_COLS")) cb = std::max<int64_t>(1, atoll(pe));
+                if (const char *pe = ozenv("OZAKI_OFFLOAD_PANEL_ROWS")) rb = std::max<int64_t>(1, atoll(pe));
+                if (c.n > cb || c.m > rb) return run_offload_blocks(c, rb, cb);
             }
             return run_offload(c);   // (alpha == 0 or k == 0: C = beta C staged through k_scale_*)
         }

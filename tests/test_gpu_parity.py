@@ -467,12 +467,15 @@ def test_lazy_conj_views(orc):
         oz.zgemm("N", "N", 1.0, Ad.mH, Bd, 0.0, C.conj(), 7)
 
 
+@pytest.mark.parametrize("rows,cols", [(None, "128"), ("100", "128"), ("64", "1000")])
 @pytest.mark.parametrize("ta,tb", [("N", "N"), ("T", "T"), ("N", "C")])
-def test_host_offload_column_panels(orc, ta, tb, monkeypatch):
-    """One large GEMM on host pointers moves op(B) and C in column panels (H2D / GEMM / D2H
-    overlapped): forced 128-column panels (6 panels, ragged last), transposes, beta != 0 and
-    ldc > m -- bitwise equal to the oracle, padding rows of C untouched."""
-    monkeypatch.setenv("OZAKI_OFFLOAD_PANEL_COLS", "128")
+def test_host_offload_column_panels(orc, ta, tb, rows, cols, monkeypatch):
+    """One large GEMM on host pointers moves in 2-D blocks (row panels of op(A), column panels of
+    op(B), C blocks; H2D / GEMM / D2H overlapped): forced block sizes (ragged last blocks),
+    transposes, beta != 0 and ldc > m -- bitwise equal to the oracle, padding rows untouched."""
+    monkeypatch.setenv("OZAKI_OFFLOAD_PANEL_COLS", cols)
+    if rows:
+        monkeypatch.setenv("OZAKI_OFFLOAD_PANEL_ROWS", rows)
     m, n, k, ld, s = 300, 700, 90, 333, 6
     Aop = synth.uniform(m, k, seed=31, complex_=True)
     Bop = synth.spread(k, n, seed=32, phi=1.0, complex_=True)

@@ -10,8 +10,18 @@
 
 using namespace ozk;
 
+__device__ __forceinline__ void bulk_store(void *gdst, uint32_t ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(ssrc), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit_wait() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 template <int EPI, int MODE>
 __global__ void __launch_bounds__(576, 1) k_mb(GemmParams p, unsigned long long *out, int reps) {
+    extern __shared__ __align__(1024) double sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp < 2) return;
     const int ew = warp - 2, q = warp & 3, half = ew >> 2;
@@ -28,6 +38,21 @@ __global__ void __launch_bounds__(576, 1) k_mb(GemmParams p, unsigned long long 
             double *cp = p.C + grow + half * 32 * p.ldc;
 #pragma unroll
             for (int j = 0; j < 32; ++j) cp[(int64_t)j * p.ldc] = acc[j];
+        }
+        if (MODE == 2) {   // stage column segments in SMEM, one bulk copy per (column, 32 rows)
+            // smem tile column-major [128 cols][128 rows]; this warp: rows q*32.., cols half*32..
+            double *st = sm + (int64_t)(half * 32) * 128 + q * 32 + lane;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) st[j * 128] = acc[j];
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane < 32) {   // each lane issues one column's 256-B segment
+                const int j = lane;
+                const uint32_t src = (uint32_t)__cvta_generic_to_shared(sm + (int64_t)(half * 32 + j) * 128 + q * 32);
+                bulk_store(p.C + q * 32 + (half * 32 + j) * p.ldc, src, 256);
+            }
+            bulk_commit_wait();
+            __syncwarp();
         }
         acc[0] += 1.0;
     }
@@ -59,6 +84,10 @@ int main() {
         p.ldc = M;
         k_mb<EPI_CPLX4M, 0><<<1, 576>>>(p, out, reps); cudaMemcpy(h, out, sizeof h, cudaMemcpyDeviceToHost);
         printf("cplx lv_store  reps=%d cycles/warp/rep: %.0f %.0f\n", reps, (double)h[0] / reps, (double)h[15] / reps);
+        cudaFuncSetAttribute(k_mb<EPI_REAL, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 128 * 8);
+        k_mb<EPI_REAL, 2><<<1, 576, 128 * 128 * 8>>>(p, out, reps); cudaDeviceSynchronize();
+        k_mb<EPI_REAL, 2><<<1, 576, 128 * 128 * 8>>>(p, out, reps); cudaMemcpy(h, out, sizeof h, cudaMemcpyDeviceToHost);
+        printf("smem + bulk   reps=%d cycles/warp/rep: %.0f %.0f\n", reps, (double)h[0] / reps, (double)h[15] / reps);
     }
     printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
