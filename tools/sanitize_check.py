@@ -51,5 +51,43 @@ Cd = dev(np.zeros((200, 150)))
 oz.dgemm("N", "N", 1.0, dev(A), dev(synth.uniform(70, 150, seed=14)), 0.0, Cd, 7)
 oz.dgemm("N", "N", 1.0, Cd, dev(synth.uniform(150, 150, seed=15)), 0.0, C, 7)
 oz.set_overlap(False)
+# round-2 additions: split-K (forced S = 3, real / 4M / 3M / full pairs, and a split-K call under
+# cross-call overlap), the general alpha / beta (GAB) store, the emulated TRSM (all sides, real
+# and complex, host pointers), the 2-D block host offload
+os.environ["OZAKI_SPLITK"] = "3"
+oz.dgemm("N", "N", -1.0, dev(synth.uniform(130, 400, seed=16)), dev(synth.uniform(400, 90, seed=17)), 1.0,
+         dev(synth.uniform(130, 90, seed=18)), 7)
+oz.zgemm("N", "C", 0.5 - 0.5j, dev(synth.kkr(70, 300, seed=19)), dev(synth.kkr(60, 300, seed=20)), 1.0,
+         dev(synth.uniform(70, 60, seed=21, complex_=True)), 6)
+oz.zgemm3m("N", "N", 1.0, dev(synth.kkr(70, 300, seed=22)), dev(synth.kkr(300, 60, seed=23)), 0.0,
+           dev(np.zeros((70, 60), np.complex128)), 5)
+oz.set_pair_set("full")
+oz.dgemm("N", "N", 1.0, dev(synth.uniform(130, 400, seed=24)), dev(synth.uniform(400, 90, seed=25)), 0.0,
+         dev(np.zeros((130, 90))), 4)
+oz.set_pair_set("triangular")
+oz.set_overlap(True)
+for _ in range(2):
+    oz.dgemm("N", "N", 1.0, dev(synth.uniform(130, 400, seed=26)), dev(synth.uniform(400, 90, seed=27)), 0.0,
+             dev(np.zeros((130, 90))), 6)
+oz.set_overlap(False)
+del os.environ["OZAKI_SPLITK"]
+oz.set_trsm_block(32)
+for side, uplo, ta in (("L", "L", "N"), ("L", "U", "T"), ("R", "U", "N"), ("R", "L", "C")):
+    Tm = np.tril(synth.uniform(70, 70, seed=28, complex_=True)) * 0.2 + 2 * np.eye(70)
+    Tm = Tm if uplo == "L" else Tm.T.copy()
+    Bm = synth.uniform(70, 40, seed=29, complex_=True) if side == "L" else synth.uniform(40, 70, seed=29, complex_=True)
+    oz.ztrsm(side, uplo, ta, "N", 0.5 + 0.5j, dev(Tm), dev(Bm), 6)
+    oz.dtrsm(side, uplo, "T" if ta == "C" else ta, "U", 1.0, dev(Tm.real.copy()), dev(Bm.real.copy()), 6)
+hT = torch.from_numpy(np.asfortranarray(np.tril(synth.uniform(50, 50, seed=30)) + 2 * np.eye(50)))
+hB = torch.from_numpy(np.asfortranarray(synth.uniform(50, 20, seed=31)))
+oz.dtrsm("L", "L", "N", "N", 1.0, hT, hB, 7)
+oz.set_trsm_block(128)
+os.environ["OZAKI_OFFLOAD_PANEL_COLS"] = "64"
+os.environ["OZAKI_OFFLOAD_PANEL_ROWS"] = "96"
+hA = torch.from_numpy(np.asfortranarray(synth.uniform(200, 90, seed=32)))
+hBB = torch.from_numpy(np.asfortranarray(synth.uniform(90, 150, seed=33)))
+hC = torch.from_numpy(np.asfortranarray(synth.uniform(200, 150, seed=34)))
+oz.dgemm("N", "N", 1.0, hA, hBB, 0.5, hC, 7)
+del os.environ["OZAKI_OFFLOAD_PANEL_COLS"], os.environ["OZAKI_OFFLOAD_PANEL_ROWS"]
 torch.cuda.synchronize()
 print("sanitize_check done")
