@@ -153,8 +153,11 @@ __global__ void __launch_bounds__(256) k_crt(const __grid_constant__ CrtParams P
                 s[l] = (uint32_t)diff;
                 br = (uint32_t)(diff >> 63);
             }
-#pragma unroll
-            for (int it = 0; it < 2; ++it) {
+            // qe is floor(S / M) - 1, floor(S / M) or floor(S / M) + 1: the FP64 estimate has a
+            // relative error below 2^-51 on a quotient below 2^13 (absolute < 2^-38), and the
+            // dropped low limbs add less than 2^(32(L-1)) / M < 2^-15.  So S - qe M lies in
+            // [-M, 2M) and ONE correction (add M if negative, else subtract M if >= M) is exact.
+            {
                 if ((int32_t)s[L] < 0) {                     // negative: add M
                     unsigned long long cc = 0;
 #pragma unroll

@@ -90,7 +90,7 @@ enum DbgSlot : int {
     DBG_MMA_WAIT_FULL0,  // part of DBG_MMA_WAIT_FULL at the first k-block of a pass
     DBG_MMA_WAIT_FULLP0, // part of DBG_MMA_WAIT_FULL inside pass 0
     DBG_TL0 = 32,        // timeline of CTA 0 (globaltimer ns): slots DBG_TL0 + event
-    DBG_NSLOT = 48
+    DBG_NSLOT = 64
 };
 
 // debug timers (cold path): accumulate straight into the device buffer so no
@@ -99,16 +99,21 @@ __device__ __forceinline__ void dbg_add(const GemmParams &p, int slot, long long
     atomicAdd(p.dbg + slot, (unsigned long long)v);
 }
 
+// Tile index -> (batch entry, row tile, column tile), raster groups of kRasterGroup row tiles.
+// 32-bit arithmetic: the host keeps batch x tiles (x split-K units) below 2^31 (make_plan), and
+// a 64-bit division is a long software sequence on the critical path of every tile.
 __device__ __forceinline__ void decode_tile(const GemmParams &p, int64_t tile, int64_t &b,
                                             int64_t &tm, int64_t &tn) {
-    const int64_t per_batch = p.tiles_m * p.tiles_n;
-    b = tile / per_batch;
-    int64_t r = tile - b * per_batch;
-    const int64_t gsize = (int64_t)kRasterGroup * p.tiles_n;
-    const int64_t group = r / gsize;
-    const int64_t first_m = group * kRasterGroup;
-    const int64_t gm = min((int64_t)kRasterGroup, p.tiles_m - first_m);
-    const int64_t in_g = r - group * gsize;
+    const uint32_t t = (uint32_t)tile, tiles_m = (uint32_t)p.tiles_m, tiles_n = (uint32_t)p.tiles_n;
+    const uint32_t per_batch = tiles_m * tiles_n;
+    const uint32_t bb = t / per_batch;
+    const uint32_t r = t - bb * per_batch;
+    const uint32_t gsize = (uint32_t)kRasterGroup * tiles_n;
+    const uint32_t group = r / gsize;
+    const uint32_t first_m = group * kRasterGroup;
+    const uint32_t gm = min((uint32_t)kRasterGroup, tiles_m - first_m);
+    const uint32_t in_g = r - group * gsize;
+    b = bb;
     tm = first_m + in_g % gm;
     tn = in_g / gm;
 }

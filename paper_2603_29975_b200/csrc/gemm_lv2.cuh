@@ -40,7 +40,15 @@ struct Lv2Params {
 // Debug timeline (ozaki_debug_timing): globaltimer at fixed events of CTA 0.
 enum TlEvent : int { TL_ENTRY = 0, TL_PROLOGUE, TL_DEPWAIT, TL_TMA0, TL_FULL0, TL_MMA_PASS0, TL_MMA_END,
                      TL_EPI_PASS0, TL_EPI_LAST, TL_EPI_STORE, TL_EXIT, TL_EPI_DRAINED, TL_EPI_F, TL_MMA_SLOT1, TL_EPI_REL0,
-                     TL_MMA_FULL1 };
+                     TL_MMA_FULL1, TL_ENTRY_MAX, TL_EXIT_MAX, TL_MMA_END_MAX };
+// latest event over all CTAs (atomicMax of globaltimer)
+__device__ __forceinline__ void tl_max(const GemmParams &p, int ev) {
+    if (p.dbg) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMax(p.dbg + DBG_TL0 + ev, t);
+    }
+}
 __device__ __forceinline__ void tl_mark(const GemmParams &p, int ev) {
     if (p.dbg && blockIdx.x == 0) {
         unsigned long long t;
@@ -53,12 +61,17 @@ __device__ __forceinline__ void tl_mark(const GemmParams &p, int ev) {
 // share of [kb_begin, kb_end); splitk == 1 is the whole range).
 __device__ __forceinline__ void lv2_unit(const GemmParams &p, int64_t u, int64_t &tile, int64_t &kb0,
                                          int64_t &kb1, int &q) {
-    const int sk = p.splitk;
-    tile = u / sk;
-    q = (int)(u - tile * sk);
-    const int64_t span = p.kb_end - p.kb_begin;
-    kb0 = p.kb_begin + span * q / sk;
-    kb1 = p.kb_begin + span * (q + 1) / sk;
+    const uint32_t sk = (uint32_t)p.splitk, uu = (uint32_t)u;   // < 2^31 (make_plan)
+    tile = uu / sk;
+    q = (int)(uu - (uint32_t)tile * sk);
+    if (sk == 1) {
+        kb0 = p.kb_begin;
+        kb1 = p.kb_end;
+        return;
+    }
+    const uint32_t span = (uint32_t)(p.kb_end - p.kb_begin);   // split-K runs unchunked: span = KB
+    kb0 = p.kb_begin + (uint32_t)(((uint64_t)span * (uint32_t)q) / sk);
+    kb1 = p.kb_begin + (uint32_t)(((uint64_t)span * (uint32_t)(q + 1)) / sk);
 }
 
 template <int S, bool FULL = false>
@@ -144,6 +157,7 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
         }
     }
     tl_mark(p, TL_MMA_END);
+    tl_max(p, TL_MMA_END_MAX);
     if (p.dbg && (threadIdx.x & 31) == 0) dbg_add(p, DBG_MMA_TOTAL, clock64() - t_begin);
 }
 
@@ -172,7 +186,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     const int s = p.s;
     const int Lmax = FULL ? 2 * s : s + 1;   // levels Lmax (least significant) .. 2 (R1 / R21)
     const int64_t total = p.batch * p.tiles_m * p.tiles_n * p.splitk;   // work units
-    if (threadIdx.x == 0) tl_mark(p, TL_ENTRY);
+    if (threadIdx.x == 0) {
+        tl_mark(p, TL_ENTRY);
+        tl_max(p, TL_ENTRY_MAX);
+    }
 
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < S; ++i) {
@@ -503,7 +520,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 
     tc_fence_before();
     cluster_sync();          // all MMAs done and all TMEM reads of both CTAs finished
-    if (threadIdx.x == 0) tl_mark(p, TL_EXIT);
+    if (threadIdx.x == 0) {
+        tl_mark(p, TL_EXIT);
+        tl_max(p, TL_EXIT_MAX);
+    }
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc_pair(tbase, 512);

@@ -403,6 +403,9 @@ int make_plan(Kind kind, int64_t m, int64_t n, int64_t k, int64_t batch, int s, 
         P.smem = (size_t)P.stages * P.kps * kb_bytes + 1024 /*align*/ + 256 /*barriers*/;
     }
     if (P.stages < 2) return fail(OZAKI_ERR_UNSUPPORTED, "pipeline does not fit in shared memory");
+    // the kernels decode (batch, tile, split-K unit) in 32-bit arithmetic
+    if ((double)P.batch * (double)P.tiles_m * (double)P.tiles_n * 16.0 >= 2147483648.0)
+        return fail(OZAKI_ERR_UNSUPPORTED, "batch x tiles = %lld exceeds 2^27", (long long)(P.batch * P.tiles_m * P.tiles_n));
     return 0;
 }
 
@@ -1175,6 +1178,8 @@ struct OffloadCtx {
     cudaEvent_t in_done[2] = {}, comp_done[2] = {}, out_done[2] = {}, start = nullptr;
     char *buf[2] = {nullptr, nullptr};   // staging buffer sets, cached across calls
     size_t cap = 0;
+    char *blk = nullptr;                 // one-GEMM 2-D block staging (op(A), op(B), C), cached
+    size_t blk_cap = 0;
 };
 thread_local OffloadCtx t_off[kMaxDev];
 
@@ -1215,21 +1220,29 @@ int run_offload_blocks(const Call &c, int64_t rb, int64_t cb) {
     if (int rc = offload_ctx(&o)) return rc;
     const size_t abytes = al256((size_t)c.m * c.k * es), bbytes = al256((size_t)c.k * c.n * es);
     const size_t need = abytes + bbytes + (size_t)c.m * c.n * es;
-    if (o->cap < need) {
+    if (o->blk_cap < need) {
         CUDA_TRY(cudaStreamSynchronize(o->d2h));
-        for (int q = 0; q < 2; ++q) {
-            if (o->buf[q]) cudaFree(o->buf[q]);
-            o->buf[q] = nullptr;
-        }
-        o->cap = 0;
-        cudaError_t e = cudaMalloc(&o->buf[0], need);
+        CUDA_TRY(cudaStreamSynchronize(o->comp));
+        if (o->blk) cudaFree(o->blk);
+        o->blk = nullptr;
+        o->blk_cap = 0;
+        cudaError_t e = cudaMalloc(&o->blk, need);
         if (e != cudaSuccess) return fail(OZAKI_ERR_ALLOC, "offload staging (%zu B): %s", need, cudaGetErrorString(e));
-        o->cap = need;
+        o->blk_cap = need;
     }
-    double *dA = (double *)o->buf[0];
-    double *dB = (double *)(o->buf[0] + abytes);
-    double *dC = (double *)(o->buf[0] + abytes + bbytes);
-    std::vector<cudaEvent_t> ev((size_t)(I + J + 2 * I * J), nullptr);
+    double *dA = (double *)o->blk;
+    double *dB = (double *)(o->blk + abytes);
+    double *dC = (double *)(o->blk + abytes + bbytes);
+    // events: released on every path (RAII), after the streams are drained
+    struct Events {
+        std::vector<cudaEvent_t> v;
+        ~Events() {
+            for (auto &x : v)
+                if (x) cudaEventDestroy(x);
+        }
+    } evs;
+    evs.v.assign((size_t)(I + J + 2 * I * J), nullptr);
+    std::vector<cudaEvent_t> &ev = evs.v;
     for (auto &x : ev) CUDA_TRY(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
     cudaEvent_t *a_done = ev.data(), *b_done = a_done + I, *in_done = b_done + J, *cmp_done = in_done + I * J;
     cudaStream_t user = t_stream;
@@ -1300,7 +1313,7 @@ int run_offload_blocks(const Call &c, int64_t rb, int64_t cb) {
     cudaStreamWaitEvent(user, o->start, 0);
     cudaError_t e = cudaStreamSynchronize(o->d2h);
     cudaStreamSynchronize(o->comp);
-    for (auto &x : ev) cudaEventDestroy(x);
+    cudaStreamSynchronize(o->h2d);
     if (!rc && e != cudaSuccess) rc = fail(OZAKI_ERR_CUDA, "offload: %s", cudaGetErrorString(e));
     return rc;
 }

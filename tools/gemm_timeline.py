@@ -14,7 +14,7 @@ import synth  # noqa: E402
 import paper_2603_29975_b200 as oz  # noqa: E402
 
 EV = ["entry", "prologue", "depwait", "tma0_issued", "full0", "mma_pass0_done", "mma_end", "epi_pass0",
-      "epi_last_pass", "epi_store_done", "exit", "epi_drained", "epi_probe_loads", "mma_slots_pass1", "epi_release_slot0", "mma_full_pass1"]
+      "epi_last_pass", "epi_store_done", "exit", "epi_drained", "epi_probe_loads", "mma_slots_pass1", "epi_release_slot0", "mma_full_pass1", "entry_latest_cta", "exit_latest_cta", "mma_end_latest"]
 
 
 def dev(x):
@@ -26,11 +26,11 @@ def timeline(name, fn):
         fn()
     torch.cuda.synchronize()
     L = oz.lib()
-    buf = (ctypes.c_uint64 * 48)()
-    L.ozaki_debug_timing(1, buf, 48)
+    buf = (ctypes.c_uint64 * 64)()
+    L.ozaki_debug_timing(1, buf, 64)
     fn()
     torch.cuda.synchronize()
-    L.ozaki_debug_timing(0, buf, 48)
+    L.ozaki_debug_timing(0, buf, 64)
     t = [int(buf[32 + i]) for i in range(len(EV))]
     t0 = t[0]
     print(json.dumps({"case": name, **{e: (round((v - t0) / 1e3, 2) if v else None) for e, v in zip(EV, t)}}))
@@ -47,3 +47,8 @@ os.environ.pop("OZAKI_SPLITK")
 n = 2048
 A, B, C = dev(synth.uniform(n, n, 1)), dev(synth.uniform(n, n, 2)), dev(np.zeros((n, n)))
 timeline(f"DGEMM {n}^3 s=7", lambda: oz.dgemm("N", "N", 1.0, A, B, 0.0, C, 7))
+import bench  # noqa: E402
+A_h, B_h = bench.make_inputs(30, 512, 3.0, 1000)
+Az, Bz = bench.to_dev_batched(torch, A_h, "cuda"), bench.to_dev_batched(torch, B_h, "cuda")
+Cz = torch.zeros((30, 512, 512), dtype=torch.complex128, device="cuda").transpose(1, 2)
+timeline("C2x30 ZGEMM 512^3 4M s=7", lambda: oz.zgemm_strided_batched("N", "N", 1.0, Az, Bz, 0.0, Cz, 7))
