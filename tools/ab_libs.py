@@ -1,0 +1,27 @@
+"""A/B timing of library builds (experiment aid): C2x30 (4M s=7) and C3 DGEMM 8192^3 s=7 with
+the library at paper_2603_29975_b200/<lib>.  usage: python tools/ab_libs.py libozaki.so ..."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import paper_2603_29975_b200 as oz  # noqa: E402
+
+oz.LIB_PATH = os.path.join(ROOT, "paper_2603_29975_b200", sys.argv[1])
+import bench  # noqa: E402
+
+st = torch.cuda.current_stream()
+A_h, B_h = bench.make_inputs(30, 512, 3.0, 1000)
+Az, Bz = bench.to_dev_batched(torch, A_h, "cuda"), bench.to_dev_batched(torch, B_h, "cuda")
+Cz = torch.zeros((30, 512, 512), dtype=torch.complex128, device="cuda").transpose(1, 2)
+res = {"lib": sys.argv[1]}
+for s in (5, 7):
+    call = lambda s=s: oz.zgemm_strided_batched("N", "N", 1.0, Az, Bz, 0.0, Cz, s)   # noqa: E731
+    for _ in range(5):
+        call()
+    ms, clk = bench.timed(torch, st, call, 50, 0)
+    res[f"c2x30_s{s}"] = {"ms": round(ms, 4), "mhz": clk.get("sm_mhz")}
+print(json.dumps(res), flush=True)
