@@ -24,4 +24,16 @@ for s in (5, 7):
         call()
     ms, clk = bench.timed(torch, st, call, 50, 0)
     res[f"c2x30_s{s}"] = {"ms": round(ms, 4), "mhz": clk.get("sm_mhz")}
+if len(sys.argv) > 2 and sys.argv[2] == "oz2":       # Ozaki-II C3 phases
+    A_h, B_h = bench.c3_inputs(8192, "U")
+    A = oz.colmajor(torch.from_numpy(A_h).cuda())
+    B = oz.colmajor(torch.from_numpy(B_h).cuda())
+    C = torch.zeros((8192, 8192), dtype=torch.float64, device="cuda").t()
+    for nmod in (12, 14):
+        call = lambda nmod=nmod: oz.ozaki2_dgemm("N", "N", 1.0, A, B, 0.0, C, nmod)   # noqa: E731
+        for _ in range(2):
+            call()
+        _, g, ph, clk = bench.profiled(torch, oz, st, call, 3, 0)
+        res[f"c3_oz2_N{nmod}"] = {"split": ph.get("k1_slice"), "crt": ph.get("other"), "gemm": round(g, 4),
+                                  "mhz": clk.get("sm_mhz")}
 print(json.dumps(res), flush=True)
