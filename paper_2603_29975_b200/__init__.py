@@ -208,15 +208,26 @@ def _on(device):
     return torch.cuda.device(device)
 
 
+_raw_stream = None   # torch's raw current-stream query (no Stream object per call), if present
+
+
+def _current_stream_handle(device):
+    import torch
+    global _raw_stream
+    if _raw_stream is None:
+        _raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", False)
+    idx = device.index if (device is not None and device.type == "cuda" and device.index is not None) \
+        else torch.cuda.current_device()
+    if _raw_stream:
+        return int(_raw_stream(idx))
+    return torch.cuda.current_stream(idx).cuda_stream
+
+
 def _bind_stream(stream=None, device=None):
     import torch
     if stream is None and not torch.cuda.is_available():
         raise RuntimeError("no CUDA device: the Ozaki library has no CPU path")
-    if stream is None:
-        s = torch.cuda.current_stream(device if device is not None and device.type == "cuda" else None)
-    else:
-        s = stream
-    h = s.cuda_stream
+    h = _current_stream_handle(device) if stream is None else stream.cuda_stream
     if getattr(_bound, "h", None) != h:      # the library's stream is thread-local too
         lib().ozaki_set_stream(ctypes.c_void_p(h))
         _bound.h = h
@@ -231,9 +242,20 @@ def _dims(transa, transb, A, B):
     return m, n, k
 
 
+_cpairs = {}
+
+
 def _cpair(z):
+    """(re, im) as a C double[2]; the arrays of recently used values are reused (read-only)."""
+    import math
     z = complex(z)
-    return (ctypes.c_double * 2)(z.real, z.imag)
+    key = (z.real, z.imag, math.copysign(1.0, z.real), math.copysign(1.0, z.imag))   # -0.0 != +0.0
+    a = _cpairs.get(key)
+    if a is None:
+        if len(_cpairs) > 64:
+            _cpairs.clear()
+        a = _cpairs[key] = (ctypes.c_double * 2)(z.real, z.imag)
+    return a
 
 
 # ------------------------------------------------------------------ GEMMs
