@@ -82,12 +82,13 @@ def lib():
     L.ozaki_set_exponent_block.restype = i32
     L.ozaki_get_exponent_block.argtypes = []
     L.ozaki_get_exponent_block.restype = i64
-    L.ozaki_dtrsm.argtypes = [c, c, c, c, i64, i64, dbl, p, i64, p, i64, i32]
-    L.ozaki_ztrsm.argtypes = [c, c, c, c, i64, i64, dP, p, i64, p, i64, i32]
-    L.ozaki_set_trsm_block.argtypes = [i64]
-    L.ozaki_set_trsm_block.restype = i32
-    L.ozaki_get_trsm_block.argtypes = []
-    L.ozaki_get_trsm_block.restype = i64
+    if hasattr(L, "ozaki_dtrsm"):   # (a library built before round 2 lacks the TRSM entry points)
+        L.ozaki_dtrsm.argtypes = [c, c, c, c, i64, i64, dbl, p, i64, p, i64, i32]
+        L.ozaki_ztrsm.argtypes = [c, c, c, c, i64, i64, dP, p, i64, p, i64, i32]
+        L.ozaki_set_trsm_block.argtypes = [i64]
+        L.ozaki_set_trsm_block.restype = i32
+        L.ozaki_get_trsm_block.argtypes = []
+        L.ozaki_get_trsm_block.restype = i64
     L.ozaki_set_pair_set.argtypes = [i32]
     L.ozaki_set_pair_set.restype = i32
     L.ozaki_get_pair_set.argtypes = []

@@ -318,26 +318,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     const int64_t off = (b * p.N + c0) * p.Mp + grow;
                     uint32_t v[16];
                     if (ps == 0) {
-                        // level by level: both 16-column halves in flight, then the slot goes back
-                        // to the MMA issuer at once (the next pass waits for these slots)
                         long long t0[16], t1[16];
-                        uint32_t v1[16];
-#pragma unroll 1
-                        for (int j = 0; j < nlev; ++j) {
-                            tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN), v);
-                            tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + 16), v1);
-                            tmem_wait_ld();
-                            tc_fence_before();
-                            __syncwarp();
-                            if (lane == 0) mbar_arrive_cluster(slot_remote0 + 8u * (uint32_t)j);
-                            if (dbgw && j == 0 && u == (blockIdx.x >> 1)) tl_mark(p, TL_EPI_REL0);
-                            const long long w = 1ll << (8 * j);
+                        tmem_ld_32x32b_x16(tl, v);
+                        tmem_wait_ld();
 #pragma unroll
-                            for (int i = 0; i < 16; ++i) {
-                                t0[i] = (j == 0 ? 0ll : t0[i]) + (long long)(int)v[i] * w;
-                                t1[i] = (j == 0 ? 0ll : t1[i]) + (long long)(int)v1[i] * w;
-                            }
+                        for (int i = 0; i < 16; ++i) t0[i] = (long long)(int)v[i];
+#pragma unroll 1
+                        for (int j = 1; j < nlev; ++j) {
+                            tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN), v);
+                            tmem_wait_ld();
+                            const int w = 1 << (8 * j);
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) t0[i] += (long long)(int)v[i] * w;
                         }
+                        tmem_ld_32x32b_x16(tl + 16u, v);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) t1[i] = (long long)(int)v[i];
+#pragma unroll 1
+                        for (int j = 1; j < nlev; ++j) {
+                            tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + 16), v);
+                            tmem_wait_ld();
+                            const int w = 1 << (8 * j);
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) t1[i] += (long long)(int)v[i] * w;
+                        }
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0)
+                            for (int j = 0; j < nlev; ++j) mbar_arrive_cluster(slot_remote0 + 8u * (uint32_t)j);
                         if (rok) {
                             long long *dst = reinterpret_cast<long long *>(p.P0) + (int64_t)sq * plane + off;
 #pragma unroll
@@ -348,13 +357,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                                 if (c0 + 16 + i < p.N) dst[(int64_t)(16 + i) * p.Mp] = t1[i];
                         }
                     } else {
-                        uint32_t v1[16];
 #pragma unroll 1
                         for (int j = 0; j < nlev; ++j) {
                             const int li = (Lmax - np0) - (pa.hi - j);
                             int32_t *dst = p.PL + ((int64_t)sq * p.pk_nl + li) * plane + off;
                             tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN), v);
-                            tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + 16), v1);
+                            tmem_wait_ld();
+                            if (rok) {
+#pragma unroll
+                                for (int i = 0; i < 16; ++i)
+                                    if (c0 + i < p.N) dst[(int64_t)i * p.Mp] = (int32_t)v[i];
+                            }
+                            tmem_ld_32x32b_x16(tl + (uint32_t)(j * kLvBN + 16), v);
                             tmem_wait_ld();
                             tc_fence_before();
                             __syncwarp();
@@ -362,10 +376,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                             if (rok) {
 #pragma unroll
                                 for (int i = 0; i < 16; ++i)
-                                    if (c0 + i < p.N) dst[(int64_t)i * p.Mp] = (int32_t)v[i];
-#pragma unroll
-                                for (int i = 0; i < 16; ++i)
-                                    if (c0 + 16 + i < p.N) dst[(int64_t)(16 + i) * p.Mp] = (int32_t)v1[i];
+                                    if (c0 + 16 + i < p.N) dst[(int64_t)(16 + i) * p.Mp] = (int32_t)v[i];
                             }
                         }
                     }
