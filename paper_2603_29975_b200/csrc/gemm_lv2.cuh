@@ -41,6 +41,13 @@ struct Lv2Params {
 enum TlEvent : int { TL_ENTRY = 0, TL_PROLOGUE, TL_DEPWAIT, TL_TMA0, TL_FULL0, TL_MMA_PASS0, TL_MMA_END,
                      TL_EPI_PASS0, TL_EPI_LAST, TL_EPI_STORE, TL_EXIT, TL_EPI_DRAINED, TL_EPI_F, TL_MMA_SLOT1, TL_EPI_REL0,
                      TL_MMA_FULL1, TL_ENTRY_MAX, TL_EXIT_MAX, TL_MMA_END_MAX };
+// The timeline is compiled only into a -DOZK_TIMELINE build (tools/gemm_timeline.py builds one):
+// even predicated-off checks in the MMA issuer's loop cost ~9 % of the C3 s=4 GEMM.
+#ifdef OZK_TIMELINE
+#define OZK_TL(...) __VA_ARGS__
+#else
+#define OZK_TL(...)
+#endif
 // latest event over all CTAs (atomicMax of globaltimer)
 __device__ __forceinline__ void tl_max(const GemmParams &p, int ev) {
     if (p.dbg) {
@@ -59,8 +66,16 @@ __device__ __forceinline__ void tl_mark(const GemmParams &p, int ev) {
 
 // Work unit u of the persistent loop: tile u / splitk, k-blocks of split u % splitk (an equal
 // share of [kb_begin, kb_end); splitk == 1 is the whole range).
+template <bool SPLIT>
 __device__ __forceinline__ void lv2_unit(const GemmParams &p, int64_t u, int64_t &tile, int64_t &kb0,
                                          int64_t &kb1, int &q) {
+    if constexpr (!SPLIT) {   // unsplit kernels: the original per-tile loop (uniform K bounds)
+        tile = u;
+        q = 0;
+        kb0 = p.kb_begin;
+        kb1 = p.kb_end;
+        return;
+    }
     const uint32_t sk = (uint32_t)p.splitk, uu = (uint32_t)u;   // < 2^31 (make_plan)
     tile = uu / sk;
     q = (int)(uu - (uint32_t)tile * sk);
@@ -74,7 +89,7 @@ __device__ __forceinline__ void lv2_unit(const GemmParams &p, int64_t u, int64_t
     kb1 = p.kb_begin + (uint32_t)(((uint64_t)span * (uint32_t)(q + 1)) / sk);
 }
 
-template <int S, bool FULL = false>
+template <int S, bool FULL = false, bool SPLIT = false>
 __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem, uint64_t *full,
                                              uint64_t *empty, uint64_t *pass_full,
                                              uint64_t *slot_empty, uint32_t tbase) {
@@ -82,7 +97,7 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
     constexpr uint32_t idesc = idesc_i8(256, kLvBN);
     const LvParams &lp = P2.lv;
     const GemmParams &p = lp.g;
-    const int64_t total = p.batch * p.tiles_m * p.tiles_n * p.splitk;   // units of super-tiles (256 x 128)
+    const int64_t total = p.batch * p.tiles_m * p.tiles_n * (SPLIT ? p.splitk : 1);   // units of 256 x 128 super-tiles
     const int Sg = p.stages;
     uint32_t stage = 0, phase = 0;
     uint32_t slot_par = (1u << kSlots) - 1u;    // bit j: parity to wait for on slot j
@@ -92,7 +107,7 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
     for (int64_t u = blockIdx.x >> 1; u < total; u += gridDim.x >> 1) {
         int64_t tile, ub, ue;
         int q;
-        lv2_unit(p, u, tile, ub, ue, q);
+        lv2_unit<SPLIT>(p, u, tile, ub, ue, q);
 #pragma unroll
         for (int ps = 0; ps < PP.npass; ++ps) {
             const int hi = PP.hi[ps], lo = PP.lo[ps], tlo = PP.tlo[ps], n = PP.n[ps];
@@ -103,8 +118,8 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
                 const bool kfirst = (kb0 == ub);
                 long long w0 = p.dbg ? clock64() : 0;
                 mbar_wait(&full[stage], phase);
-                if (kfirst && ps == 0 && u == (blockIdx.x >> 1)) tl_mark(p, TL_FULL0);
-                if (kfirst && ps == 1 && u == (blockIdx.x >> 1)) tl_mark(p, TL_MMA_FULL1);
+                OZK_TL(if (kfirst && ps == 0 && u == (blockIdx.x >> 1)) tl_mark(p, TL_FULL0);)
+                OZK_TL(if (kfirst && ps == 1 && u == (blockIdx.x >> 1)) tl_mark(p, TL_MMA_FULL1);)
                 if (p.dbg && (threadIdx.x & 31) == 0) {
                     const long long dw = clock64() - w0;
                     dbg_add(p, DBG_MMA_WAIT_FULL, dw);
@@ -130,7 +145,7 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
                             }
                         }
                         tc_fence_after();
-                        if (ps == 1 && u == (blockIdx.x >> 1)) tl_mark(p, TL_MMA_SLOT1);
+                        OZK_TL(if (ps == 1 && u == (blockIdx.x >> 1)) tl_mark(p, TL_MMA_SLOT1);)
                     }
 #pragma unroll
                     for (int r = 0; r < S; ++r) {
@@ -153,11 +168,10 @@ __device__ __forceinline__ void lv2_mma_role(const Lv2Params &P2, uint8_t *smem,
                 if (++stage == (uint32_t)Sg) { stage = 0; phase ^= 1; }
             }
             mma_commit_pair_elect(pass_full);
-            if (ps == 0 && u == (blockIdx.x >> 1)) tl_mark(p, TL_MMA_PASS0);
+            OZK_TL(if (ps == 0 && u == (blockIdx.x >> 1)) tl_mark(p, TL_MMA_PASS0);)
         }
     }
-    tl_mark(p, TL_MMA_END);
-    tl_max(p, TL_MMA_END_MAX);
+    OZK_TL(tl_mark(p, TL_MMA_END); tl_max(p, TL_MMA_END_MAX);)
     if (p.dbg && (threadIdx.x & 31) == 0) dbg_add(p, DBG_MMA_TOTAL, clock64() - t_begin);
 }
 
@@ -185,10 +199,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     const uint32_t rank = cluster_ctarank();
     const int s = p.s;
     const int Lmax = FULL ? 2 * s : s + 1;   // levels Lmax (least significant) .. 2 (R1 / R21)
-    const int64_t total = p.batch * p.tiles_m * p.tiles_n * p.splitk;   // work units
+    constexpr bool SPLIT = (CHUNK == 3);   // split-K units (compile time: the other kernels keep the tile loop)
+    const int64_t total = p.batch * p.tiles_m * p.tiles_n * (SPLIT ? p.splitk : 1);   // work units
     if (threadIdx.x == 0) {
-        tl_mark(p, TL_ENTRY);
-        tl_max(p, TL_ENTRY_MAX);
+        OZK_TL(tl_mark(p, TL_ENTRY); tl_max(p, TL_ENTRY_MAX);)
     }
 
     if (warp == 0 && lane == 0) {
@@ -209,11 +223,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     cluster_sync();          // barriers of both CTAs initialised, TMEM allocated
     tc_fence_after();
     const uint32_t tbase = *tholder;
-    if (threadIdx.x == 0) tl_mark(p, TL_PROLOGUE);
+    OZK_TL(if (threadIdx.x == 0) tl_mark(p, TL_PROLOGUE);)
     // Programmatic dependent launch: the prologue above overlaps the producer kernel's tail
     // (K1); everything below reads its output (slices, exponents), so wait for its completion.
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (threadIdx.x == 0) tl_mark(p, TL_DEPWAIT);
+    OZK_TL(if (threadIdx.x == 0) tl_mark(p, TL_DEPWAIT);)
     // ... and let a dependent launched with PDL (the next call's split, ozaki_set_overlap) start
     // on the SMs this grid's last wave leaves idle; it orders itself after this grid (split_fast.cuh)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -225,7 +239,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             for (int64_t u = blockIdx.x >> 1; u < total; u += gridDim.x >> 1) {
                 int64_t tile, ub, ue, b, tm, tn;
                 int q;
-                lv2_unit(p, u, tile, ub, ue, q);
+                lv2_unit<SPLIT>(p, u, tile, ub, ue, q);
                 decode_tile(p, tile, b, tm, tn);
                 // A tiles of 128 rows: this CTA's is 2*tm + rank;  B tiles of 64 rows: 2*tn + rank
                 const int64_t arow0 = ((b * (2 * p.tiles_m) + 2 * tm + rank) * p.KB) * (int64_t)s * (kBlk / 256);
@@ -249,7 +263,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                             tma_load_2d_pair(dst + abytes, &P2.tmB[ps], 0, rb, leader_full);
                             dst += abytes + bbytes;
                         }
-                        if (u == (blockIdx.x >> 1) && ps == 0 && kb0 == ub) tl_mark(p, TL_TMA0);
+                        OZK_TL(if (u == (blockIdx.x >> 1) && ps == 0 && kb0 == ub) tl_mark(p, TL_TMA0);)
                         if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
                     }
                 }
@@ -260,7 +274,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         if (rank == 0) {
             if constexpr (FULL) {
                 switch (s) {
-#define OZK_MMA2_CASE(SS) case SS: lv2_mma_role<SS, true>(P2, smem, full, empty, pass_full, slot_empty, tbase); break;
+#define OZK_MMA2_CASE(SS) case SS: lv2_mma_role<SS, true, SPLIT>(P2, smem, full, empty, pass_full, slot_empty, tbase); break;
                     OZK_MMA2_CASE(1) OZK_MMA2_CASE(2) OZK_MMA2_CASE(3) OZK_MMA2_CASE(4)
                     OZK_MMA2_CASE(5) OZK_MMA2_CASE(6) OZK_MMA2_CASE(7) OZK_MMA2_CASE(8)
 #undef OZK_MMA2_CASE
@@ -268,7 +282,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 }
             } else {
                 switch (s) {
-#define OZK_MMA2_CASE(SS) case SS: lv2_mma_role<SS>(P2, smem, full, empty, pass_full, slot_empty, tbase); break;
+#define OZK_MMA2_CASE(SS) case SS: lv2_mma_role<SS, false, SPLIT>(P2, smem, full, empty, pass_full, slot_empty, tbase); break;
                     OZK_MMA2_CASE(1) OZK_MMA2_CASE(2) OZK_MMA2_CASE(3) OZK_MMA2_CASE(4)
                     OZK_MMA2_CASE(5) OZK_MMA2_CASE(6) OZK_MMA2_CASE(7) OZK_MMA2_CASE(8)
                     OZK_MMA2_CASE(9) OZK_MMA2_CASE(10) OZK_MMA2_CASE(11) OZK_MMA2_CASE(12)
@@ -290,7 +304,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         for (int64_t u = blockIdx.x >> 1; u < total; u += gridDim.x >> 1) {
             int64_t tile, ub, ue, b, tm, tn;
             int sq;
-            lv2_unit(p, u, tile, ub, ue, sq);
+            lv2_unit<SPLIT>(p, u, tile, ub, ue, sq);
             decode_tile(p, tile, b, tm, tn);
             const int64_t grow = (2 * tm + rank) * kBM + q * 32 + lane;
             const int32_t e = (grow < p.Mp) ? __ldg(p.ea + b * p.Mp + grow) : 0;
@@ -301,7 +315,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 const LvPass pa = lp.pass[ps];
                 long long w0 = p.dbg ? clock64() : 0;
                 mbar_wait(pass_full, pphase);
-                if (dbgw && u == (blockIdx.x >> 1)) tl_mark(p, ps == 0 ? TL_EPI_PASS0 : TL_EPI_LAST);
+                OZK_TL(if (dbgw && u == (blockIdx.x >> 1)) tl_mark(p, ps == 0 ? TL_EPI_PASS0 : TL_EPI_LAST);)
                 long long w1 = p.dbg ? clock64() : 0;
                 if (dbgw) dbg_add(p, DBG_EPI_WAIT, w1 - w0);
                 pphase ^= 1;
@@ -419,7 +433,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive_cluster(slot_remote0);
-                        if (dbgw && u == (blockIdx.x >> 1)) tl_mark(p, TL_EPI_REL0);
+                        OZK_TL(if (dbgw && u == (blockIdx.x >> 1)) tl_mark(p, TL_EPI_REL0);)
                         if (dbgw) dbg_add(p, DBG_EPI_FIRST_ARRIVE, clock64() - w1);
 #pragma unroll
                         for (int i = 0; i < 16; ++i) t1[i] = (long long)(int)v[i];
@@ -513,6 +527,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 if (dbgw) dbg_add(p, DBG_EPI_DRAIN, clock64() - w1);
             }
             const long long s0 = p.dbg ? clock64() : 0;
+#ifdef OZK_TIMELINE
             if (dbgw) {
                 tl_mark(p, TL_EPI_DRAINED);
                 // probe: latency of one column-exponent load and one load of C (debug timeline only)
@@ -522,18 +537,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
                 if (blockIdx.x == 0) p.dbg[DBG_TL0 + TL_EPI_F] = t + (f == -123456789 ? 1 : 0) + (cv == 1.2345e300 ? 1 : 0);
             }
+#endif
             if constexpr (EPI != EPI_LEVELS && CHUNK != 1 && CHUNK != 3)
                 lv_store<EPI, kNC2, GAB>(p, b, grow, e, tn * kLvBN + half * kNC2, acc, CHUNK == 0 ? -8 * (Lmax - 2) : 0);
             if (dbgw) dbg_add(p, DBG_EPI_STORE, clock64() - s0);
-            if (dbgw) tl_mark(p, TL_EPI_STORE);
+            OZK_TL(if (dbgw) tl_mark(p, TL_EPI_STORE);)
         }
     }
 
     tc_fence_before();
     cluster_sync();          // all MMAs done and all TMEM reads of both CTAs finished
     if (threadIdx.x == 0) {
-        tl_mark(p, TL_EXIT);
-        tl_max(p, TL_EXIT_MAX);
+        OZK_TL(tl_mark(p, TL_EXIT); tl_max(p, TL_EXIT_MAX);)
     }
     if (warp == 1) {
         tc_fence_after();

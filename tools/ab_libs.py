@@ -24,6 +24,18 @@ for s in (5, 7):
         call()
     ms, clk = bench.timed(torch, st, call, 50, 0)
     res[f"c2x30_s{s}"] = {"ms": round(ms, 4), "mhz": clk.get("sm_mhz")}
+if len(sys.argv) > 2 and sys.argv[2] == "c3":        # C3 DGEMM 8192^3: step and GEMM kernel time
+    A_h, B_h = bench.c3_inputs(8192, "U")
+    A = oz.colmajor(torch.from_numpy(A_h).cuda())
+    B = oz.colmajor(torch.from_numpy(B_h).cuda())
+    C = torch.zeros((8192, 8192), dtype=torch.float64, device="cuda").t()
+    for s in (4, 7):
+        call = lambda s=s: oz.dgemm("N", "N", 1.0, A, B, 0.0, C, s)   # noqa: E731
+        for _ in range(2):
+            call()
+        ms, clk = bench.timed(torch, st, call, 5, 0)
+        _, g, ph, clk2 = bench.profiled(torch, oz, st, call, 3, 0)
+        res[f"c3_s{s}"] = {"ms": round(ms, 4), "mhz": clk.get("sm_mhz"), "gemm": round(g, 4), "mhz2": clk2.get("sm_mhz")}
 if len(sys.argv) > 2 and sys.argv[2] == "oz2":       # Ozaki-II C3 phases
     A_h, B_h = bench.c3_inputs(8192, "U")
     A = oz.colmajor(torch.from_numpy(A_h).cuda())
