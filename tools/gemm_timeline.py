@@ -1,5 +1,7 @@
 """Timeline of CTA 0 of the pair GEMM (globaltimer ns, relative to kernel entry) for small
-problems: where the fixed per-launch time goes.  usage: python tools/gemm_timeline.py"""
+problems: where the fixed per-launch time goes.  The timeline is compiled only with
+-DOZK_TIMELINE: this tool builds paper_2603_29975_b200/libozaki_timeline.so (once, ~3 min) and
+loads it instead of the production library.  usage: python tools/gemm_timeline.py"""
 import ctypes
 import json
 import os
@@ -12,6 +14,15 @@ import torch  # noqa: E402
 
 import synth  # noqa: E402
 import paper_2603_29975_b200 as oz  # noqa: E402
+from paper_2603_29975_b200 import _build  # noqa: E402
+
+TL_LIB = os.path.join(_build.PKG, "libozaki_timeline.so")
+if not os.path.exists(TL_LIB):
+    import subprocess
+    cmd = [_build.nvcc(), *_build.NVCC_FLAGS, "-DOZK_TIMELINE", "-I", os.path.join(ROOT, "include"), "-I",
+           _build.CSRC, os.path.join(_build.CSRC, "ozaki.cu"), "-o", TL_LIB]
+    subprocess.run(cmd, check=True, capture_output=True)
+oz.LIB_PATH = TL_LIB
 
 EV = ["entry", "prologue", "depwait", "tma0_issued", "full0", "mma_pass0_done", "mma_end", "epi_pass0",
       "epi_last_pass", "epi_store_done", "exit", "epi_drained", "epi_probe_loads", "mma_slots_pass1", "epi_release_slot0", "mma_full_pass1", "entry_latest_cta", "exit_latest_cta", "mma_end_latest"]
