@@ -866,7 +866,7 @@ def run_c3(args):
             "kernel_pass_clocks": clocks2,
         },
         "roofline_split": {
-            "bound": "hbm", "kernel": "k_split_exps + k_split_fast (exponent scan, INT8 digits, both operands)",
+            "bound": "hbm", "kernel": "k_split_cluster (one HBM read per operand: clusters of up to 16 CTAs along K, partial row maxima exchanged through distributed shared memory, INT8 digits of both operands)",
             "achieved": round(c3_split_bytes(n, s) / (split_ms * 1e-3) / 1e9, 1) if split_ms else None,
             "peak": hbm[0], "unit": "GB/s",
             "frac": round(c3_split_bytes(n, s) / (split_ms * 1e-3) / 1e9 / hbm[0], 4) if split_ms else None,

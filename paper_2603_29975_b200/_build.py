@@ -11,7 +11,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libozaki.so")
 SHIM = os.path.join(PKG, "libozaki_blas.so")   # Fortran dgemm_/zgemm_ interposition (NEXT-2)
 SOURCES = ["ozaki.cu"]
-HEADERS = ["trsm.cuh", "crt.cuh", "crt_kernel.cuh", "gemm_crt.cuh", "gemm_lv2.cuh", "passplan.cuh", "gemm_lv.cuh", "gemm.cuh", "split.cuh", "split_fast.cuh", "numerics.cuh", "ptx.cuh"]
+HEADERS = ["split_cluster.cuh", "trsm.cuh", "crt.cuh", "crt_kernel.cuh", "gemm_crt.cuh", "gemm_lv2.cuh", "passplan.cuh", "gemm_lv.cuh", "gemm.cuh", "split.cuh", "split_fast.cuh", "numerics.cuh", "ptx.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

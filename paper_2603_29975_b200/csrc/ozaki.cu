@@ -30,6 +30,7 @@
 #include "ozaki.h"
 #include "split.cuh"
 #include "split_fast.cuh"
+#include "split_cluster.cuh"
 #include "trsm.cuh"
 
 using namespace ozk;
@@ -205,6 +206,21 @@ cudaError_t smem_optin(const void *fn, size_t smem) {
     if (have >= smem) return cudaSuccess;
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess) have = smem;
+    return e;
+}
+
+// Cluster sizes above 8 (non-portable) opt-in, per device and kernel, cached like smem_optin.
+std::unordered_map<const void *, bool> g_cl16[kMaxDev];
+cudaError_t cluster16_optin(const void *fn) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    bool &have = g_cl16[dev][fn];
+    if (have) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess) have = true;
     return e;
 }
 
@@ -629,6 +645,76 @@ int launch_exps(SplitPair &pp, unsigned batch, int nx, int mode, bool crt, cudaS
 // pdl = launch with PDL after the previous call's GEMM; early = may read / write before it ends.
 thread_local bool t_split_pdl = false, t_split_early = false;
 
+// Long real rows in one HBM read (split_cluster.cuh): a cluster of CS CTAs per 8-row group
+// (OZAKI_SPLIT_RG=16: 16 rows), chunk KC <= KCMAX values of K per CTA (32 KB of shared memory at 512).  Returns 1 when the
+// shape does not qualify (the two-kernel LONG form runs).  OZAKI_SPLIT_CLUSTER=0 disables it,
+// OZAKI_SPLIT_KC sets KCMAX (tuning hook).
+// sw: the slice count s (Ozaki-I) or the moduli word count (CRT: a multiple of 4).
+template <bool CRT>
+int launch_split_cluster(int sw, const SplitPair &pp, unsigned batch, cudaStream_t st, bool pdl, bool early) {
+    if (const char *e = ozenv("OZAKI_SPLIT_CLUSTER"))
+        if (atoi(e) == 0) return 1;
+    // 8 rows x 512 values (32 KB, six CTAs per SM) measured best on C3: split 0.28 ms at s = 3,
+    // 0.41 ms at s = 7 (16 rows: 0.31 / 0.45; 8 x 1024: 0.31 / 0.45; two-kernel form 0.57 / 0.74)
+    int kcmax = 512, rg = 8;
+    if (const char *e = ozenv("OZAKI_SPLIT_KC")) {
+        const int v = atoi(e);
+        if (v >= 64 && v <= 1024 && v % 32 == 0) kcmax = v;
+    }
+    if (const char *e = ozenv("OZAKI_SPLIT_RG"))
+        if (atoi(e) == 16) rg = 16;
+    for (int sd = 0; sd < 2; ++sd) {
+        const SplitParams &q = pp.side[sd];
+        if (q.mode != SPLIT_REAL || (q.rs != 1 && q.ls != 1)) return 1;
+    }
+    const int64_t kpad = pp.side[0].KB * 32;
+    const int64_t cs = (kpad + kcmax - 1) / kcmax;
+    if (cs < 2 || cs > 16) return 1;
+    const int KC = (int)(((kpad + cs - 1) / cs + 31) / 32 * 32);
+    const int64_t groups = (std::max(pp.side[0].rows_grid, pp.side[1].rows_grid) + rg - 1) / rg;
+    if (groups * cs > INT32_MAX) return 1;
+    const size_t smem = (size_t)rg * (KC + 2) * 8;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(groups * cs), batch, 2);
+    cfg.blockDim = dim3(rg == 16 ? 256 : 128);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    auto prep = [&](const void *kern) -> int {
+        CUDA_TRY(smem_optin(kern, smem));
+        if (cs > 8) CUDA_TRY(cluster16_optin(kern));
+        return 0;
+    };
+    auto go = [&](auto kern) -> int {
+        if (int rc = prep((const void *)kern)) return rc;
+        cfg.numAttrs = pdl ? 2 : 1;
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, pp, KC, early ? 1 : 0));
+        return 0;
+    };
+    ProfScope ps(st, PH_SLICE);
+#define OZK_CL(S)                                                                                          \
+    case S:                                                                                                \
+        return rg == 16 ? go(k_split_cluster<S, 16, 256, CRT>) : go(k_split_cluster<S, 8, 128, CRT>);
+    if constexpr (CRT) {
+        switch (sw) { OZK_CL(4) OZK_CL(8) OZK_CL(12) OZK_CL(16) OZK_CL(20) }
+    } else {
+        switch (sw) {
+            OZK_CL(1) OZK_CL(2) OZK_CL(3) OZK_CL(4) OZK_CL(5) OZK_CL(6)
+            OZK_CL(7) OZK_CL(8) OZK_CL(9) OZK_CL(10) OZK_CL(11) OZK_CL(12)
+        }
+    }
+#undef OZK_CL
+    return 1;
+}
+
 int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b, dim3 grid, cudaStream_t st) {
     const bool pdl = t_split_pdl, early = t_split_early;
     if (!b || !P.pair || P.s < 1 || P.s > 12) return 1;
@@ -658,6 +744,16 @@ int launch_split_fast(const Plan &P, const SplitParams &a, const SplitParams *b,
     }
     bool lng = nwin >= 3;
     if (const char *lg = ozenv("OZAKI_SPLIT_LONG")) lng = (atoi(lg) != 0) && nwin > 1;
+    if (lng && real) {   // one HBM read through a thread-block cluster when the rows fit 16 chunks
+        SplitPair pc;
+        pc.side[0] = a;
+        pc.side[1] = *b;
+        const int rc = launch_split_cluster<false>(P.s, pc, grid.y, st, pdl, early);
+        if (rc <= 0) {
+            if (rc == 0) g_stats.launches += 1;
+            return rc;
+        }
+    }
     if (lng) {   // short windows, more rows per CTA: 128-B reads per l when rows are adjacent
         RG = real ? 16 : 8;
         KW = 256;
@@ -1561,6 +1657,14 @@ int launch_split_fast_crt(const SplitParams &a, const SplitParams &b, int64_t ba
     SplitPair pp;
     pp.side[0] = a;
     pp.side[1] = b;
+    if (lng && real) {   // one HBM read through a thread-block cluster (split_cluster.cuh)
+        const int nmx = (a.crt.n + 3) / 4 * 4;
+        const int rc = launch_split_cluster<true>(nmx > 20 ? 20 : nmx, pp, (unsigned)batch, st, false, false);
+        if (rc <= 0) {
+            if (rc == 0) g_stats.launches += 1;
+            return rc;
+        }
+    }
     dim3 grid((unsigned)((rows_grid + RG - 1) / RG) * (lng ? nwin : 1), (unsigned)batch, 2);
     uint32_t *emax = nullptr;
     if (lng) {

@@ -146,3 +146,36 @@ def test_more_moduli_more_accurate():
         oz.ozaki2_dgemm("N", "N", 1.0, dev(A), dev(B), 0.0, C, nmod)
         errs.append(float(np.max(np.abs(C.cpu().numpy() - T) / (np.abs(A) @ np.abs(B)))))
     assert all(b <= a for a, b in zip(errs, errs[1:])) and errs[-1] < 1e-15, errs
+
+
+@pytest.mark.parametrize("nmod", [6, 12, 14, 20])
+@pytest.mark.parametrize("shape", [(40, 36, 5000), (33, 17, 8192)])
+def test_dgemm_long_rows_cluster_split(nmod, shape):
+    """Long real rows (k > 2048) take the single-read cluster split (split_cluster.cuh, residues
+    emitted from shared memory): NN and TT layouts, a padded leading dimension, a non-finite
+    row found in a middle K chunk; bit-exact vs the oracle and vs the two-kernel form."""
+    import os
+    m, n, k = shape
+    A = synth.spread(m, k, seed=nmod + k, phi=2.0)
+    B = synth.uniform(k, n, seed=nmod + k + 1)
+    A[3, k // 2 + 7] = np.inf
+    ref = o2.dgemm("N", "N", 1.0, A, B, 0.0, None, nmod)
+    got = dev(np.zeros((m, n)))
+    oz.ozaki2_dgemm("N", "N", 1.0, dev(A), dev(B), 0.0, got, nmod)
+    assert same(got.cpu().numpy(), ref)
+    assert np.isnan(got.cpu().numpy()[3]).all()
+    got_t = dev(np.zeros((m, n)))
+    oz.ozaki2_dgemm("T", "T", 1.0, dev(A.T.copy()), dev(B.T.copy()), 0.0, got_t, nmod)
+    assert same(got_t.cpu().numpy(), ref)
+    big = np.full((m + 1, k), 3.0)
+    big[:m] = A
+    got_p = dev(np.zeros((m, n)))
+    oz.ozaki2_dgemm("N", "N", 1.0, dev(big)[:m], dev(B), 0.0, got_p, nmod)
+    assert same(got_p.cpu().numpy(), ref)
+    os.environ["OZAKI_SPLIT_CLUSTER"] = "0"
+    try:
+        two = dev(np.zeros((m, n)))
+        oz.ozaki2_dgemm("N", "N", 1.0, dev(A), dev(B), 0.0, two, nmod)
+    finally:
+        del os.environ["OZAKI_SPLIT_CLUSTER"]
+    assert same(two.cpu().numpy(), ref)
