@@ -47,3 +47,39 @@ def both():
 
 t = timed(both)
 print(f"H2D 256 MB + D2H 128 MB concurrently: {t * 1e3:.2f} ms ({384 * MB / t / 1e9:.1f} GB/s total)")
+
+
+# 2-D copies (the offload path's row panels of a column-major A), through cudaMemcpy2DAsync
+# itself (torch copies strided host views another way): width = rows * 8 B, pitch 64 KB
+import ctypes  # noqa: E402
+
+rt = None
+for name in ("libcudart.so.12", "libcudart.so"):
+    try:
+        rt = ctypes.CDLL(name)
+        break
+    except OSError:
+        pass
+if rt is None:
+    import glob
+    import os
+    cands = glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "cuda_runtime", "lib", "libcudart.so*"))
+    rt = ctypes.CDLL(cands[0])
+rt.cudaMemcpy2DAsync.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_size_t,
+                                 ctypes.c_size_t, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]
+A = torch.empty((8192, 8192), dtype=torch.float64).pin_memory()   # 512 MB, column j at j * 64 KB
+dA = torch.empty((8192, 8192), dtype=torch.float64, device="cuda")
+for rows in (512, 1024, 2048, 4096, 8192):
+    def h2d2():
+        rc = rt.cudaMemcpy2DAsync(ctypes.c_void_p(dA.data_ptr()), rows * 8, ctypes.c_void_p(A.data_ptr()),
+                                  8192 * 8, rows * 8, 8192, 1, ctypes.c_void_p(s1.cuda_stream))
+        assert rc == 0, rc
+    t = timed(h2d2, 3)
+    print(f"H2D cudaMemcpy2DAsync: {rows} rows x 8192 columns (pitch 64 KB, {rows * 8 // 1024} KB rows): "
+          f"{rows * 8192 * 8 / t / 1e9:.1f} GB/s")
+    def d2h2():
+        rc = rt.cudaMemcpy2DAsync(ctypes.c_void_p(A.data_ptr()), 8192 * 8, ctypes.c_void_p(dA.data_ptr()),
+                                  rows * 8, rows * 8, 8192, 2, ctypes.c_void_p(s2.cuda_stream))
+        assert rc == 0, rc
+    t = timed(d2h2, 3)
+    print(f"D2H cudaMemcpy2DAsync: {rows} rows x 8192 columns: {rows * 8192 * 8 / t / 1e9:.1f} GB/s")
