@@ -871,7 +871,14 @@ def run_c3(args):
             "peak": hbm[0], "unit": "GB/s",
             "frac": round(c3_split_bytes(n, s) / (split_ms * 1e-3) / 1e9 / hbm[0], 4) if split_ms else None,
             "algorithmic_bytes_per_step": c3_split_bytes(n, s), "peak_source": hbm[1],
-            "ms_per_step": round(split_ms, 5)},
+            "ms_per_step": round(split_ms, 5),
+            "traffic": ncu_s.get("split_dram_bytes"),
+            "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + write.sum, profiles/ncu_c3.json)",
+            "ncu_isolated": ({"ms": round(ncu_s["split_ms"], 5),
+                              "frac": round(c3_split_bytes(n, s) / (ncu_s["split_ms"] * 1e-3) / 1e9 / hbm[0], 4),
+                              "note": "the same launch timed alone under ncu (cold L2, no power-capped GEMM "
+                                      "beside it); the bench pass above runs between the GEMMs of the step"}
+                             if ncu_s.get("split_ms") else None)},
         "phase_ms_per_step": phase,
         "gpu_launches": launches,
         "clocks": clocks,

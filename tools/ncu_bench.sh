@@ -12,9 +12,10 @@ for s in 3 4 5 6 7 8 9; do
   ncu --metrics $M --clock-control none -k regex:k_gemm_lv2 -s 2 -c 1 --csv \
       --log-file $O/${TAG}_c3_s${s}.csv python tools/ncu_c3.py --s $s > /dev/null 2>&1
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-      -k regex:k_split -s 4 -c 2 --csv --log-file $O/${TAG}_c3_split_s${s}.csv python tools/ncu_c3.py --s $s > /dev/null 2>&1
+      -k regex:k_split -s 2 -c 1 --csv --log-file $O/${TAG}_c3_split_s${s}.csv python tools/ncu_c3.py --s $s > /dev/null 2>&1
 done
 ncu --set full --import-source on --clock-control none -k regex:k_gemm_lv2 -s 2 -c 1 \
     -o $O/${TAG}_c3_s7_full -f python tools/ncu_c3.py --s 7 > $O/${TAG}_full.log 2>&1
 ncu -i $O/${TAG}_c3_s7_full.ncu-rep --page raw --csv > $O/${TAG}_c3_s7_full_raw.csv 2>/dev/null
+rm -f $O/${TAG}_c3_s7_full.ncu-rep
 echo ncu_done

@@ -50,9 +50,11 @@ def main(tag):
         rec = {"tensor_pipe_pct": m["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"],
                "dram_bytes": int(dram), "algorithmic_bytes": alg, "gemm_ms": m["gpu__time_duration.sum"] / 1e6,
                "sm_hz": m["sm__cycles_elapsed.avg.per_second"], "kernel": k[1]}
-        ps = os.path.join(OUT, f"{tag}_c3_split_s{s}.csv")
-        if os.path.exists(ps):
-            ks = per_kernel(ps)
+        ps = os.path.join(OUT, f"{tag}_split_s{s}.csv")          # tools/ncu_split_cluster.sh
+        if not os.path.exists(ps) or not per_kernel(ps):
+            ps = os.path.join(OUT, f"{tag}_c3_split_s{s}.csv")    # tools/ncu_bench.sh
+        ks = per_kernel(ps) if os.path.exists(ps) else {}
+        if ks:
             rec["split_ms"] = sum(v["gpu__time_duration.sum"] for v in ks.values()) / 1e6
             rec["split_dram_bytes"] = int(sum(v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"] for v in ks.values()))
             rec["split_algorithmic_bytes"] = 16 * n * n + 2 * s * n * n
@@ -90,6 +92,21 @@ def main(tag):
         full = {k: f"{val[hdr.index(k)]} {unit[hdr.index(k)]}".strip() for k in keys if k in hdr}
         res["full_set_s7"] = full
         md += ["", "`ncu --set full` of the s=7 GEMM launch:", ""] + [f"- `{k}`: {v}" for k, v in full.items()]
+    sp = os.path.join(OUT, f"{tag}_split_full_raw.csv")
+    if os.path.exists(sp):   # tools/ncu_split_cluster.sh: --set full of the s=7 split launch
+        with open(sp) as fh:
+            r = list(csv.reader(fh))
+        hdr, unit, val = r[0], r[1], r[2]
+        keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+                "dram__throughput.avg.pct_of_peak_sustained_elapsed", "launch__cluster_dim_x",
+                "launch__occupancy_cluster_pct", "launch__registers_per_thread",
+                "sm__warps_active.avg.pct_of_peak_sustained_active", "sm__cycles_elapsed.avg.per_second"]
+        full = {k: f"{val[hdr.index(k)]} {unit[hdr.index(k)]}".strip() for k in keys if k in hdr}
+        if "Kernel Name" in hdr:
+            full["kernel"] = val[hdr.index("Kernel Name")]
+        res["split_full_set_s7"] = full
+        md += ["", "`ncu --set full` of the s=7 split launch (`k_split_cluster`, tools/ncu_split_cluster.sh):", ""] + \
+              [f"- `{k}`: {v}" for k, v in full.items()]
     with open(os.path.join(PROF, "ncu_c3.json"), "w") as fh:
         json.dump(res, fh, indent=1)
     with open(os.path.join(PROF, f"{tag}_ncu_c3.md"), "w") as fh:
