@@ -20,19 +20,20 @@ res = {"lib": sys.argv[1]}
 A_h, B_h = bench.make_inputs(30, 512, 3.0, 1000)
 Az, Bz = bench.to_dev_batched(torch, A_h, "cuda"), bench.to_dev_batched(torch, B_h, "cuda")
 Cz = torch.zeros((30, 512, 512), dtype=torch.complex128, device="cuda").transpose(1, 2)
-n = 4096
+n = int(os.environ.get("EXP_N", "4096"))
 A = oz.colmajor(torch.from_numpy(synth.uniform(n, n, 1)).cuda())
 B = oz.colmajor(torch.from_numpy(synth.uniform(n, n, 2)).cuda())
 C = torch.zeros((n, n), dtype=torch.float64, device="cuda").t()
-for name, (al, be) in (("unit", (1.0, 0.0)), ("lu", (-1.0, 1.0))):
-    call = lambda al=al, be=be: oz.zgemm_strided_batched("N", "N", al, Az, Bz, be, Cz, 7)   # noqa: E731
-    for _ in range(3):
-        call()
-    ms, clk = bench.timed(torch, st, call, 30, 0)
-    res[f"c2x30_{name}"] = {"ms": round(ms, 4), "mhz": clk.get("sm_mhz")}
-    call = lambda al=al, be=be: oz.dgemm("N", "N", al, A, B, be, C, 7)   # noqa: E731
-    for _ in range(3):
-        call()
-    ms, clk = bench.timed(torch, st, call, 10, 0)
-    res[f"d4096_{name}"] = {"ms": round(ms, 4), "mhz": clk.get("sm_mhz")}
+for s in [int(x) for x in os.environ.get("EXP_S", "7").split(",")]:
+    for name, (al, be) in (("unit", (1.0, 0.0)), ("lu", (-1.0, 1.0))):
+        call = lambda al=al, be=be: oz.zgemm_strided_batched("N", "N", al, Az, Bz, be, Cz, s)   # noqa: E731
+        for _ in range(3):
+            call()
+        ms, clk = bench.timed(torch, st, call, 30, 0)
+        res[f"c2x30_s{s}_{name}"] = {"ms": round(ms, 4), "mhz": clk.get("sm_mhz")}
+        call = lambda al=al, be=be: oz.dgemm("N", "N", al, A, B, be, C, s)   # noqa: E731
+        for _ in range(3):
+            call()
+        ms, clk = bench.timed(torch, st, call, 10, 0)
+        res[f"d{n}_s{s}_{name}"] = {"ms": round(ms, 4), "mhz": clk.get("sm_mhz")}
 print(json.dumps(res))
