@@ -1895,6 +1895,21 @@ int run(const Call &c0) {
         if (c.tb == 'C') c.tb = 'T';
     }
     if (c.m == 0 || c.n == 0 || c.batch == 0) return 0;
+    // the kernels index batch entries with blockIdx.y / z (at most 65535): larger batches run as
+    // consecutive sub-batches, each entry's computation unchanged
+    constexpr int64_t kMaxGridBatch = 65535;
+    if (c.batch > kMaxGridBatch && !c.S_out) {
+        const int64_t ew = (c.kind == KIND_REAL) ? 1 : 2;   // doubles per element
+        for (int64_t b0 = 0; b0 < c.batch; b0 += kMaxGridBatch) {
+            Call cb = c;
+            cb.batch = std::min(kMaxGridBatch, c.batch - b0);
+            cb.A = c.A + ew * b0 * c.sA;
+            cb.B = c.B + ew * b0 * c.sB;
+            cb.C = c.C + ew * b0 * c.sC;
+            if (int rc = run(cb)) return rc;
+        }
+        return 0;
+    }
     DevState *dev = nullptr;
     if (int rc = device_state(&dev)) return rc;
     if (!c.S_out) {   // host operands -> pipelined offload (all three must be host)

@@ -532,3 +532,26 @@ def test_zgemm_lu_update_signed_zeros(orc, alpha, method):
         g_, w_ = part(got), part(want)
         z = (g_ == 0) & (w_ == 0)
         assert (np.signbit(g_[z]) == np.signbit(w_[z])).all()
+
+
+def test_batch_above_grid_limit(orc):
+    """More than 65535 batch entries (the kernels index entries with blockIdx.y / z): the call
+    runs as consecutive sub-batches; entries on both sides of the 65535 boundary bit-exact."""
+    s, batch, m, n, k = 3, 65540, 8, 6, 5
+    rng = np.random.default_rng(7)
+    A = rng.uniform(-1, 1, (batch, m, k))
+    B = rng.uniform(-1, 1, (batch, k, n))
+    tA = torch.from_numpy(A).cuda().transpose(1, 2).contiguous().transpose(1, 2)
+    tB = torch.from_numpy(B).cuda().transpose(1, 2).contiguous().transpose(1, 2)
+    tC = torch.full((batch, n, m), np.nan, dtype=torch.float64, device="cuda").transpose(1, 2)
+    oz.dgemm_strided_batched("N", "N", 1.0, tA, tB, 0.0, tC, s)
+    got = tC.cpu().numpy()
+    for i in (0, 65534, 65535, 65536, batch - 1):
+        assert same(got[i], orc.dgemm("N", "N", 1.0, A[i], B[i], 0.0, None, s)), i
+    Z = (A[:, :4, :4] + 1j * A[:, 4:, :4]).copy()
+    tZ = torch.from_numpy(Z).cuda().transpose(1, 2).contiguous().transpose(1, 2)
+    tW = torch.zeros((batch, 4, 4), dtype=torch.complex128, device="cuda").transpose(1, 2)
+    oz.zgemm_strided_batched("N", "C", 0.5 - 0.25j, tZ, tZ, 0.0, tW, s)
+    gz = tW.cpu().numpy()
+    for i in (0, 65535, batch - 1):
+        assert same(gz[i], orc.zgemm("N", "C", 0.5 - 0.25j, Z[i], Z[i], 0.0, None, s, "4m")), i
