@@ -89,5 +89,29 @@ hBB = torch.from_numpy(np.asfortranarray(synth.uniform(90, 150, seed=33)))
 hC = torch.from_numpy(np.asfortranarray(synth.uniform(200, 150, seed=34)))
 oz.dgemm("N", "N", 1.0, hA, hBB, 0.5, hC, 7)
 del os.environ["OZAKI_OFFLOAD_PANEL_COLS"], os.environ["OZAKI_OFFLOAD_PANEL_ROWS"]
+# round-2 session-3 additions: the single-read cluster split (k_split_cluster: DSMEM pushes of the
+# partial row maxima, Ozaki-I digits and Ozaki-II residues, 8- and 16-row groups, padded leading
+# dimensions, TT layouts, a batch, and a PDL launch under cross-call overlap)
+Ak = synth.uniform(40, 3000, seed=35)
+Bk = synth.spread(3000, 36, seed=36, phi=1.0)
+Ck = dev(np.zeros((40, 36)))
+oz.dgemm("N", "N", 1.0, dev(Ak), dev(Bk), 0.0, Ck, 7)
+oz.dgemm("T", "T", 1.0, dev(Ak.T.copy()), dev(Bk.T.copy()), 0.0, Ck, 4)
+os.environ["OZAKI_SPLIT_RG"] = "16"
+big = np.zeros((41, 3000)); big[:40] = Ak
+oz.dgemm("N", "N", 1.0, dev(big)[:40], dev(Bk), 0.0, Ck, 9)
+del os.environ["OZAKI_SPLIT_RG"]
+oz.dgemm("N", "N", 1.0, dev(synth.uniform(20, 8192, seed=37)), dev(synth.uniform(8192, 24, seed=38)), 0.0,
+         dev(np.zeros((20, 24))), 5)
+oz.ozaki2_dgemm("N", "N", 1.0, dev(Ak), dev(Bk), 0.0, Ck, 14)
+tAk = torch.stack([dev(Ak), dev(Ak)]).transpose(1, 2).contiguous().transpose(1, 2)
+tBk = torch.stack([dev(Bk), dev(Bk)]).transpose(1, 2).contiguous().transpose(1, 2)
+tCk = torch.zeros((2, 36, 40), dtype=torch.float64, device="cuda").transpose(1, 2)
+oz.dgemm_strided_batched("N", "N", 1.0, tAk, tBk, 0.0, tCk, 6)
+oz.set_overlap(True)
+Akd, Bkd = dev(Ak), dev(Bk)
+for _ in range(3):
+    oz.dgemm("N", "N", 1.0, Akd, Bkd, 0.0, Ck, 7)
+oz.set_overlap(False)
 torch.cuda.synchronize()
 print("sanitize_check done")
