@@ -8,7 +8,11 @@
 // a CTA pair computes a 256 x 256 tile (cta_group::2, M = 256, N = 256, K = 32,
 // 128 clk per SM per instruction) reading 4 KB of A and 4 KB of B per CTA.
 // TMEM holds two 256-column accumulator slots: the MMA of modulus q+1 runs
-// while the epilogue reduces modulus q (no pass-boundary stall).  The
+// while the epilogue reduces modulus q (no pass-boundary stall).
+// NW = 2 (wide tiles, 256 x 512): each k-block's A tile feeds TWO N = 256 MMAs
+// (B tiles t and t + 2 of the pair), so the shared-memory port moves 12 KB in and
+// reads 16 KB per two MMAs instead of 8 + 8 KB per one; the two accumulators fill
+// TMEM, so the MMA of modulus q+1 waits for the epilogue's loads of modulus q.  The
 // epilogue is integer-only (mod p by folding + a 40-bit reciprocal multiply)
 // and writes centred residue bytes in 16-byte row chunks:
 //   R[q][b][col / 16][row][16]        (plane q, batch b; rows padded to 256)
@@ -38,8 +42,10 @@ struct CrtGemmParams {
     CrtTab crt;
 };
 
+template <int NW>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCrtThreads, 1)
     k_gemm_crt(const __grid_constant__ CrtGemmParams P) {
+    constexpr int NSLOT = (NW == 1) ? 2 : 1;   // accumulator slots of 256 * NW columns
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = P.stages;
@@ -60,7 +66,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCrtThreads, 1)
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
         }
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < NSLOT; ++j) {
             mbar_init(&slot_full[j], 1);
             mbar_init(&slot_empty[j], 2 * kCrtEpi);
         }
@@ -84,17 +90,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCrtThreads, 1)
                 const int64_t b = tile / per_b, r = tile - b * per_b;
                 const int64_t tm = r / P.tiles_n, tn = r - tm * P.tiles_n;
                 const int64_t ta = b * (2 * P.tiles_m) + 2 * tm + rank;   // this CTA's 128-row A tile
-                const int64_t tb = b * (2 * P.tiles_n) + 2 * tn + rank;   // this CTA's 128-row B tile
+                // this CTA's 128-row B tiles: j-th MMA of the tile uses tiles 2 (NW tn + j) + rank
+                const int64_t tb = b * (2 * NW * P.tiles_n) + 2 * NW * tn + rank;
                 for (int q = 0; q < n; ++q) {
                     for (int64_t kb0 = 0; kb0 < P.KB; kb0 += P.kpp) {
                         mbar_wait(&empty[stage], phase ^ 1);
                         const uint32_t lf = leader_full0 + 8u * stage;
-                        if (rank == 0) mbar_arrive_expect_tx(&full[stage], 4u * abytes);
+                        if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2u * (1 + NW) * abytes);
                         uint8_t *dst = smem + (size_t)stage * P.stage_bytes;
                         const int rowA = (int)(((ta * n + q) * P.KB + kb0) * (kCrtBlk / 256));
-                        const int rowB = (int)(((tb * n + q) * P.KB + kb0) * (kCrtBlk / 256));
                         tma_load_2d_pair(dst, &P.tmA, 0, rowA, lf);
-                        tma_load_2d_pair(dst + abytes, &P.tmB, 0, rowB, lf);
+#pragma unroll
+                        for (int j = 0; j < NW; ++j) {
+                            const int rowB = (int)((((tb + 2 * j) * n + q) * P.KB + kb0) * (kCrtBlk / 256));
+                            tma_load_2d_pair(dst + (1 + j) * abytes, &P.tmB, 0, rowB, lf);
+                        }
                         if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
                     }
                 }
@@ -109,7 +119,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCrtThreads, 1)
             uint32_t g = 0;                               // global modulus-pass counter
             for (int64_t tile = blockIdx.x >> 1; tile < total; tile += gridDim.x >> 1) {
                 for (int q = 0; q < n; ++q, ++g) {
-                    const uint32_t slot = g & 1u;
+                    const uint32_t slot = (NSLOT == 2) ? (g & 1u) : 0u;
                     mbar_wait(&slot_empty[slot], (spar >> slot) & 1u);
                     spar ^= 1u << slot;
                     tc_fence_after();
@@ -120,8 +130,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCrtThreads, 1)
                         const uint32_t sb = smem_u32(smem + (size_t)stage * P.stage_bytes);
                         for (int kk = 0; kk < P.kpp; ++kk) {
                             const uint64_t ad = dsc + ((sb + (uint32_t)kk * kCrtBlk) >> 4);
-                            const uint64_t bd = dsc + ((sb + (uint32_t)(P.kpp + kk) * kCrtBlk) >> 4);
-                            mma_i8_pair_elect(d, ad, bd, idesc, (kb0 + kk > 0) ? 1u : 0u);
+#pragma unroll
+                            for (int j = 0; j < NW; ++j) {
+                                const uint64_t bd = dsc + ((sb + (uint32_t)((1 + j) * P.kpp + kk) * kCrtBlk) >> 4);
+                                mma_i8_pair_elect(d + 256u * j, ad, bd, idesc, (kb0 + kk > 0) ? 1u : 0u);
+                            }
                         }
                         mma_commit_pair_elect(&empty[stage]);
                         if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
@@ -134,8 +147,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCrtThreads, 1)
         // ------------------------------------------------ epilogue (16 warps per CTA)
         const int ew = warp - 2;
         const int qd = warp & 3;            // TMEM lane quarter this warp may access
-        const int ch = ew >> 2;             // column quarter [64 ch, 64 ch + 64)
-        const uint32_t tl = tbase + ((uint32_t)(qd * 32) << 16) + (uint32_t)(64 * ch);
+        const int ch = ew >> 2;             // column quarter [64 NW ch, 64 NW (ch + 1))
+        const uint32_t tl = tbase + ((uint32_t)(qd * 32) << 16) + (uint32_t)(64 * NW * ch);
         const uint32_t slot_remote0 = mapa_shared(smem_u32(&slot_empty[0]), 0);
         uint32_t fpar = 0;                  // bit j: parity of the next completion of slot_full[j]
         uint32_t g = 0;
@@ -143,20 +156,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCrtThreads, 1)
             const int64_t b = tile / per_b, r = tile - b * per_b;
             const int64_t tm = r / P.tiles_n, tn = r - tm * P.tiles_n;
             const int64_t row = (2 * tm + rank) * 128 + qd * 32 + lane;
-            int8_t *rb = P.R + b * P.batch_bytes + row * 16 + (tn * 16 + 4 * ch) * P.rows_pad * 16;
+            int8_t *rb = P.R + b * P.batch_bytes + row * 16 + (tn * 16 * NW + 4 * NW * ch) * P.rows_pad * 16;
             for (int q = 0; q < n; ++q, ++g) {
-                const uint32_t slot = g & 1u;
+                const uint32_t slot = (NSLOT == 2) ? (g & 1u) : 0u;
                 mbar_wait(&slot_full[slot], (fpar >> slot) & 1u);
                 fpar ^= 1u << slot;
                 tc_fence_after();
                 int8_t *dst = rb + (int64_t)q * P.plane_bytes;
 #pragma unroll
-                for (int gp = 0; gp < 2; ++gp) {   // two 16-column groups in flight per TMEM wait
+                for (int gp = 0; gp < 2 * NW; ++gp) {   // two 16-column groups in flight per TMEM wait
                     uint32_t v[2][16];
                     tmem_ld_32x32b_x16(tl + slot * 256u + (uint32_t)(32 * gp), v[0]);
                     tmem_ld_32x32b_x16(tl + slot * 256u + (uint32_t)(32 * gp + 16), v[1]);
                     tmem_wait_ld();
-                    if (gp == 1) {          // all four loads of this slot done: hand it back
+                    if (gp == 2 * NW - 1) {   // all loads of this slot done: hand it back
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive_cluster(slot_remote0 + 8u * slot);

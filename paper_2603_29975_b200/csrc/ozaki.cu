@@ -1712,11 +1712,17 @@ int run_crt(const Call &c, DevState *dev, cudaStream_t st) {
     const int64_t kh = cplx ? rup(c.k, 32) : 0;
     const int64_t Kp = cplx ? 2 * kh : rup(c.k, 32);
     const int64_t KB = Kp / 32;
-    const int64_t tiles_m = (Mp + 255) / 256, tiles_n = (Np + 255) / 256;
+    // residue-GEMM tile width 256 NW (gemm_crt.cuh): NW = 2 reuses each A tile for two MMAs but
+    // gives up the accumulator double buffer, which pays off when each modulus's K sweep is long
+    // (C3, KB = 256: residue GEMM 10-17 % faster; C2 x 30, KB = 64: 4 % slower).  OZAKI_CRT_NW
+    // forces 1 or 2.
+    int NW = (KB >= 128) ? 2 : 1;
+    if (const char *e = ozenv("OZAKI_CRT_NW")) NW = (atoi(e) == 2) ? 2 : 1;
+    const int64_t tiles_m = (Mp + 255) / 256, tiles_n = (Np + 256 * NW - 1) / (256 * NW);
     const size_t a_bytes = al256((size_t)n * kCrtBlk * KB * 2 * tiles_m * c.batch);
-    const size_t b_bytes = al256((size_t)n * kCrtBlk * KB * 2 * tiles_n * c.batch);
+    const size_t b_bytes = al256((size_t)n * kCrtBlk * KB * 2 * NW * tiles_n * c.batch);
     const size_t ea_bytes = al256(sizeof(int32_t) * Mp * c.batch), fb_bytes = al256(sizeof(int32_t) * Np * c.batch);
-    const int64_t rows_pad = 256 * tiles_m, groups = 16 * tiles_n;
+    const int64_t rows_pad = 256 * tiles_m, groups = 16 * NW * tiles_n;
     const int64_t batch_bytes = rows_pad * groups * 16;
     const size_t plane_bytes = (size_t)batch_bytes * c.batch;
     const size_t ws = a_bytes + b_bytes + ea_bytes + fb_bytes + al256(plane_bytes * n);
@@ -1745,7 +1751,7 @@ int run_crt(const Call &c, DevState *dev, cudaStream_t st) {
         sp.conj = op.conj;
         sp.s = n;
         sp.tile_h = 128;
-        sp.tiles = 2 * (sideA ? tiles_m : tiles_n);
+        sp.tiles = 2 * (sideA ? tiles_m : NW * tiles_n);
         sp.KB = KB;
         sp.kh = kh;
         sp.rows_out = (op.mode == SPLIT_B4M) ? 2 * op.rows : op.rows;
@@ -1796,7 +1802,7 @@ int run_crt(const Call &c, DevState *dev, cudaStream_t st) {
         int kpp = 4;
         while (KB % kpp) kpp >>= 1;
         G.kpp = kpp;
-        G.stage_bytes = (uint32_t)kpp * 2 * kCrtBlk;
+        G.stage_bytes = (uint32_t)kpp * (1 + NW) * kCrtBlk;
         G.stages = (int)std::min<int64_t>(8, (int64_t)(224 * 1024) / G.stage_bytes);
         const size_t smem = (size_t)G.stages * G.stage_bytes + 1024 + 512;
         G.batch = c.batch;
@@ -1812,12 +1818,13 @@ int run_crt(const Call &c, DevState *dev, cudaStream_t st) {
         rc = rows_map(&G.tmA, sa, a_bytes, (uint32_t)kpp * (kCrtBlk / 256));
         if (!rc) rc = rows_map(&G.tmB, sb, b_bytes, (uint32_t)kpp * (kCrtBlk / 256));
         if (!rc) {
-            CUDA_TRY(smem_optin((const void *)k_gemm_crt, smem));
+            auto kern = (NW == 2) ? k_gemm_crt<2> : k_gemm_crt<1>;
+            CUDA_TRY(smem_optin((const void *)kern, smem));
             const int64_t tiles = c.batch * tiles_m * tiles_n;
             const unsigned pairs = (unsigned)std::min<int64_t>(tiles, dev->sms / 2);
             {
                 ProfScope ps(st, PH_GEMM);
-                k_gemm_crt<<<2 * pairs, kCrtThreads, smem, st>>>(G);
+                kern<<<2 * pairs, kCrtThreads, smem, st>>>(G);
             }
             cudaError_t e = cudaGetLastError();
             if (e != cudaSuccess) rc = fail(OZAKI_ERR_CUDA, "k_gemm_crt: %s", cudaGetErrorString(e));

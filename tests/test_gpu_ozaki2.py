@@ -179,3 +179,28 @@ def test_dgemm_long_rows_cluster_split(nmod, shape):
     finally:
         del os.environ["OZAKI_SPLIT_CLUSTER"]
     assert same(two.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("nw", ["1", "2"])
+@pytest.mark.parametrize("shape", [(300, 700, 200), (257, 1030, 4200)])
+def test_residue_gemm_tile_widths(nw, shape):
+    """Residue-GEMM tiles of 256 x 256 (double-buffered accumulators) and 256 x 512 (each A tile
+    feeds two MMAs; the default when K spans >= 128 k-blocks), forced both ways on a short-K and a
+    long-K shape with ragged columns: bit-exact vs the oracle."""
+    import os
+    m, n, k = shape
+    A = synth.spread(m, k, seed=m + k, phi=1.0)
+    B = synth.uniform(k, n, seed=n + k)
+    ref = o2.dgemm("N", "N", 1.0, A, B, 0.0, None, 12)
+    os.environ["OZAKI_CRT_NW"] = nw
+    try:
+        C = torch.zeros((n, m), dtype=torch.float64, device="cuda").t()
+        oz.ozaki2_dgemm("N", "N", 1.0, dev(A), dev(B), 0.0, C, 12)
+        Z = synth.kkr(m // 2, k // 2, seed=5, gamma=1.0)
+        W = synth.kkr(k // 2, n // 2, seed=6, gamma=1.0)
+        Cz = torch.zeros((n // 2, m // 2), dtype=torch.complex128, device="cuda").t()
+        oz.ozaki2_zgemm("N", "N", 1.0, dev(Z), dev(W), 0.0, Cz, 10)
+    finally:
+        del os.environ["OZAKI_CRT_NW"]
+    assert same(C.cpu().numpy(), ref)
+    assert same(Cz.cpu().numpy(), o2.zgemm("N", "N", 1.0, Z, W, 0.0, None, 10))
