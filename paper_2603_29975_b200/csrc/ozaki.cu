@@ -705,9 +705,15 @@ int launch_split_cluster(int sw, const SplitPair &pp, unsigned batch, cudaStream
         return 0;
     };
     auto go = [&](auto kern) -> int {
-        if (int rc = prep((const void *)kern)) return rc;
+        if (prep((const void *)kern)) {   // no cluster opt-in on this device: the two-kernel form
+            cudaGetLastError();
+            return 1;
+        }
         cfg.numAttrs = pdl ? 2 : 1;
-        CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, pp, KC, early ? 1 : 0));
+        if (cudaLaunchKernelEx(&cfg, kern, pp, KC, early ? 1 : 0) != cudaSuccess) {
+            cudaGetLastError();   // e.g. a cluster shape the device cannot co-schedule
+            return 1;
+        }
         return 0;
     };
     ProfScope ps(st, PH_SLICE);

@@ -66,6 +66,16 @@ def run_sequence(overlap):
         oz.dgemm("N", "N", 1.0, hA, hB, 0.0, hC, s)
         oz.dgemm("N", "N", 1.0, C1, B[:, :200], 0.0, C2, s)
         out += [hC.numpy().copy(), C2.cpu().numpy()]
+        # long real rows (k > 2048: the single-read cluster split, PDL-launched after the GEMM):
+        # repeated C, then the previous C as the next call's A
+        Al = dev(synth.uniform(96, 3000, seed=11))
+        Bl = dev(synth.spread(3000, 3000, seed=12, phi=1.0))
+        Cl = dev(np.zeros((96, 3000)))
+        Cm = dev(np.zeros((96, 3000)))
+        for _ in range(2):
+            oz.dgemm("N", "N", 1.0, Al, Bl, 0.0, Cl, 6)
+        oz.dgemm("N", "N", 1.0, Cl, Bl, 0.0, Cm, 6)
+        out += [Cl.cpu().numpy(), Cm.cpu().numpy()]
         torch.cuda.synchronize()
         return out
     finally:
