@@ -124,10 +124,12 @@ def blocked_trsm(T, B, nb: int, gemm, lower: bool, unit: bool, stats: dict | Non
     return B
 
 
-def blocked_lu_invert(M, nb: int, gemm, stats: dict | None = None, emulated_trsm: bool = False):
+def blocked_lu_invert(M, nb: int, gemm, stats: dict | None = None, emulated_trsm: bool = False,
+                      check: bool = True):
     """Inverse of a square complex128 CUDA tensor by right-looking blocked LU with partial
     pivoting; the trailing updates A22 -= L21 U12 go through ``gemm``.  Returns (Minv,
-    residual max|M Minv - I|)."""
+    residual max|M Minv - I|); with check=False the residual (a native n^3 product) is skipped
+    and None is returned in its place, so that timing covers the inversion alone."""
     import torch
     if M.is_cuda:
         torch.backends.cuda.preferred_linalg_library("cusolver")
@@ -167,9 +169,16 @@ def blocked_lu_invert(M, nb: int, gemm, stats: dict | None = None, emulated_trsm
     else:
         Y = torch.linalg.solve_triangular(L, Pm, upper=False, unitriangular=True)
         Minv = torch.linalg.solve_triangular(U, Y, upper=True)
-    I = torch.eye(n, dtype=A.dtype, device=A.device)
-    resid = float((M @ Minv - I).abs().max())
-    return Minv, resid
+    if not check:
+        return Minv, None
+    return Minv, residual(M, Minv)
+
+
+def residual(M, Minv) -> float:
+    """max |M Minv - I| in native FP64."""
+    import torch
+    I = torch.eye(M.shape[0], dtype=M.dtype, device=M.device)
+    return float((M @ Minv - I).abs().max())
 
 
 # ------------------------------------------------------------------ sweep

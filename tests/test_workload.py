@@ -49,6 +49,9 @@ def test_blocked_lu_cpu_native():
     st = {}
     Minv, r = W.blocked_lu_invert(Mt, 16, _cpu_native(), st)
     assert r <= 1e-12 and st["trailing_updates"] == W.trailing_updates(n, 16) == 3
+    # check=False (timed runs): same inverse, no residual; the residual helper gives the same value
+    Minv2, r2 = W.blocked_lu_invert(Mt, 16, _cpu_native(), check=False)
+    assert r2 is None and torch.equal(Minv2, Minv) and W.residual(Mt, Minv2) == r
     I = torch.eye(8, dtype=torch.complex128)
     Iinv, r = W.blocked_lu_invert(I, 3, _cpu_native())
     assert r == 0.0 and torch.equal(Iinv, I)
