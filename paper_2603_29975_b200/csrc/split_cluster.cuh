@@ -17,8 +17,9 @@
 // from shared memory.  The max is order-free, so the exponent is bit-identical to the two-pass
 // form.
 //
-// Real operands only (DGEMM long rows: C3, C5), Ozaki-I digits or Ozaki-II residues.  Layout of the staged chunk:
-//   rows adjacent in memory (rs == 1, op(A) = A): slab[l][row]   (RG * 8 = 128 B per l)
+// Real operands only (DGEMM long rows: C3, C5), Ozaki-I digits or Ozaki-II residues.  Layout of
+// the staged chunk:
+//   rows adjacent in memory (rs == 1, op(A) = A): slab[l][row]   (RG * 8 B per l: 64 / 128 B)
 //   rows contiguous along K (ls == 1, op(B) = B):  slab[row][l]   (row pitch KC + 2 values)
 #pragma once
 #include <cstdint>
@@ -36,12 +37,6 @@ __device__ __forceinline__ uint32_t cluster_nctarank() {
     asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
     return r;
 }
-__device__ __forceinline__ uint64_t ld_dsmem_u64(uint32_t cluster_addr) {
-    uint64_t v;
-    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(cluster_addr) : "memory");
-    return v;
-}
-
 
 // Geometry of one work item (row group r0 of batch entry b, this CTA's K chunk).
 struct ClItem {
