@@ -67,6 +67,28 @@ def test_c3_dgemm_8192(orc):
     assert (got == want).all()
 
 
+@pytest.mark.parametrize("s", [3, 9])
+def test_c3_dgemm_8192_other_slices(orc, s):
+    """The C3 sweep's ends at full size: s = 3 (one-pass plan, 54-KB stages of three k-blocks)
+    and s = 9 (three passes, 128-bit fixed point in the split); both through the single-read
+    cluster split.  Plus Ozaki-II N = 12 (256 x 512 residue tiles) on the same problem."""
+    n = 8192
+    A = synth.spread(n, n, 3, phi=1.0)
+    B = synth.spread(n, n, 4, phi=1.0)
+    C = torch.zeros((n, n), dtype=torch.float64, device="cuda").t()
+    oz.dgemm("N", "N", 1.0, dev(A), dev(B), 0.0, C, s)
+    r, c = rows_sample(n), cols_sample(n)
+    got = C.cpu().numpy()[np.ix_(r, c)]
+    want = orc.dgemm("N", "N", 1.0, A[r], B[:, c], 0.0, None, s)
+    assert (got == want).all()
+    if s == 3:
+        from oracle import ozaki2 as o2
+        oz.ozaki2_dgemm("N", "N", 1.0, dev(A), dev(B), 0.0, C, 12)
+        got = C.cpu().numpy()[np.ix_(r[:8], c[:8])]
+        want = o2.dgemm("N", "N", 1.0, A[r[:8]], B[:, c[:8]], 0.0, None, 12)
+        assert (got == want).all()
+
+
 def test_c4_batched_256_zgemm_1024(orc):
     """256 x ZGEMM 1024^3 KKR(gamma=1), s=7, one strided-batched call (8 distinct blocks tiled,
     as bench.py --workload c4)."""
