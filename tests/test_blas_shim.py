@@ -72,7 +72,7 @@ L = ctypes.CDLL(%r)
 i = lambda v: ctypes.byref(ctypes.c_int(v))
 P = lambda a: a.ctypes.data_as(ctypes.c_void_p)
 s = %d
-m, n, k = 77, 61, 130
+m, n, k = 77, 61, %d
 A = synth.spread(m, k, seed=3, phi=2.0); B = synth.spread(k, n, seed=4, phi=2.0)
 C = np.asfortranarray(synth.uniform(m, n, seed=5))
 C0 = C.copy(order="F")
@@ -92,10 +92,12 @@ print("OK" if ok_d and ok_z else "MISMATCH", ok_d, ok_z)
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("s,method", [(7, "4m"), (5, "3m")])
-def test_shim_bitexact_vs_oracle(shim, s, method):
+@pytest.mark.parametrize("s,method,k", [(7, "4m", 130), (5, "3m", 130), (6, "4m", 3000)])
+def test_shim_bitexact_vs_oracle(shim, s, method, k):
+    """dgemm_ / zgemm_ on host arrays (the shim loaded with dlopen); k = 3000 takes the long-row
+    forms (the single-read cluster split for the real operands)."""
     env = {"OZAKI_NUM_SLICES": str(s), "OZAKI_ZGEMM": method}
-    r = _run_py(_CALL % (ROOT, shim, s, method), env)
+    r = _run_py(_CALL % (ROOT, shim, s, k, method), env)
     assert r.returncode == 0, r.stderr[-2000:]
     assert r.stdout.startswith("OK"), r.stdout + r.stderr[-2000:]
 
