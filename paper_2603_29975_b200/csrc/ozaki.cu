@@ -710,13 +710,13 @@ int launch_split_cluster(int sw, const SplitPair &pp, unsigned batch, cudaStream
             return 1;
         }
         cfg.numAttrs = pdl ? 2 : 1;
+        ProfScope ps(st, PH_SLICE);
         if (cudaLaunchKernelEx(&cfg, kern, pp, KC, early ? 1 : 0) != cudaSuccess) {
             cudaGetLastError();   // e.g. a cluster shape the device cannot co-schedule
             return 1;
         }
         return 0;
     };
-    ProfScope ps(st, PH_SLICE);
 #define OZK_CL(S)                                                                                          \
     case S:                                                                                                \
         return rg == 16 ? go(k_split_cluster<S, 16, 256, CRT>) : go(k_split_cluster<S, 8, 128, CRT>);
